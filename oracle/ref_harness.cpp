@@ -1,0 +1,226 @@
+// ref_harness.cpp -- TEST INFRASTRUCTURE ONLY (oracle side).
+//
+// A C-ABI shim over the reference implementation compiled from its own
+// sources (/root/reference/proj/src/{pauli,hamiltonian,tableau,diagonalize,
+// statevector}.cpp) into oracle/_ref/libsimdiag_ref.so by oracle/Makefile.
+// It lets tests/ and bench.py (--impl reference, cpu_baseline) drive the
+// reference's public C++ API through ctypes. evolve.cpp needs Eigen (absent
+// in this image), so evolve_grouped's 12-line loop (proj/src/evolve.cpp:47-58)
+// is restated here with the same calls in the same order; S2 is the
+// composition SURVEY §8a D1 defines (the reference has no S2).
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "simdiag/diagonalize.hpp"
+#include "simdiag/hamiltonian.hpp"
+#include "simdiag/statevector.hpp"
+
+namespace {
+thread_local std::string g_err;
+
+struct RefGroups {
+    int n = 0;
+    std::vector<simdiag::CommutingGroup> parts;
+    std::vector<simdiag::DiagonalGroup> diags;
+    std::vector<std::vector<int>> cnots, czs;
+};
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::out_of_range& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 3;
+    }
+}
+
+void apply_group(simdiag::StateVector& psi, const simdiag::DiagonalGroup& g, double dt) {
+    psi.apply_clifford(g.circuit);
+    psi.apply_diagonal_exp(g, dt);
+    psi.apply_clifford_inverse(g.circuit);
+}
+
+void load_state(simdiag::StateVector& psi, const double* re_im) {
+    for (std::uint64_t i = 0; i < psi.dim(); ++i) psi[i] = {re_im[2 * i], re_im[2 * i + 1]};
+}
+void store_state(const simdiag::StateVector& psi, double* re_im) {
+    for (std::uint64_t i = 0; i < psi.dim(); ++i) {
+        re_im[2 * i] = psi[i].real();
+        re_im[2 * i + 1] = psi[i].imag();
+    }
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// Hamiltonian::load -> greedy_partition -> diagonalize_group for each group.
+int ref_partition_text(const char* text, size_t len, int synthesize, void** out) {
+    return guarded([&] {
+        std::istringstream in(std::string(text, len));
+        auto h = simdiag::Hamiltonian::load(in);
+        auto r = std::make_unique<RefGroups>();
+        r->n = h.n_qubits();
+        r->parts = simdiag::greedy_partition(h);
+        for (const auto& p : r->parts) {
+            simdiag::DiagonalGroup d;
+            if (synthesize) d = simdiag::diagonalize_group(p);
+            std::vector<int> cx, cz;
+            for (auto [a, b] : d.circuit.cnots) cx.insert(cx.end(), {a, b});
+            for (auto [a, b] : d.circuit.czs) cz.insert(cz.end(), {a, b});
+            r->cnots.push_back(std::move(cx));
+            r->czs.push_back(std::move(cz));
+            r->diags.push_back(std::move(d));
+        }
+        *out = r.release();
+    });
+}
+
+// Hamiltonian::load + save (round trip text).
+int ref_load_save(const char* text, size_t len, char* buf, size_t cap, size_t* out_len) {
+    return guarded([&] {
+        std::istringstream in(std::string(text, len));
+        auto h = simdiag::Hamiltonian::load(in);
+        std::ostringstream os;
+        h.save(os);
+        const std::string s = os.str();
+        *out_len = s.size();
+        if (buf && cap) {
+            const size_t n = s.size() < cap - 1 ? s.size() : cap - 1;
+            std::memcpy(buf, s.data(), n);
+            buf[n] = 0;
+        }
+    });
+}
+
+// diagonalize_group on an explicit term list.
+int ref_diagonalize_terms(int n, const uint64_t* x, const uint64_t* z, const double* c, size_t m, void** out) {
+    return guarded([&] {
+        simdiag::CommutingGroup g;
+        for (size_t k = 0; k < m; ++k) g.terms.push_back({c[k], simdiag::PauliString::from_masks(n, x[k], z[k])});
+        auto r = std::make_unique<RefGroups>();
+        r->n = n;
+        r->parts.push_back(g);
+        auto d = simdiag::diagonalize_group(g);
+        std::vector<int> cx, cz;
+        for (auto [a, b] : d.circuit.cnots) cx.insert(cx.end(), {a, b});
+        for (auto [a, b] : d.circuit.czs) cz.insert(cz.end(), {a, b});
+        r->cnots.push_back(std::move(cx));
+        r->czs.push_back(std::move(cz));
+        r->diags.push_back(std::move(d));
+        *out = r.release();
+    });
+}
+
+void ref_groups_free(void* h) { delete static_cast<RefGroups*>(h); }
+int ref_groups_count(void* h) { return static_cast<int>(static_cast<RefGroups*>(h)->parts.size()); }
+int ref_groups_nqubits(void* h) { return static_cast<RefGroups*>(h)->n; }
+
+// sizes[0..5] = h_pre, cnots, czs, s, h_post, terms
+void ref_group_sizes(void* h, int g, int64_t* sizes) {
+    auto* r = static_cast<RefGroups*>(h);
+    const auto& c = r->diags[g].circuit;
+    sizes[0] = c.h_pre.size();
+    sizes[1] = c.cnots.size();
+    sizes[2] = c.czs.size();
+    sizes[3] = c.s_layer.size();
+    sizes[4] = c.h_post.size();
+    sizes[5] = r->parts[g].terms.size();
+}
+
+void ref_group_data(void* h, int g, int32_t* h_pre, int32_t* cnots, int32_t* czs, int32_t* s, int32_t* h_post,
+                    uint64_t* src_x, uint64_t* src_z, double* src_c, uint64_t* zm, double* cf) {
+    auto* r = static_cast<RefGroups*>(h);
+    const auto& d = r->diags[g];
+    const auto& c = d.circuit;
+    for (size_t i = 0; i < c.h_pre.size(); ++i) h_pre[i] = c.h_pre[i];
+    for (size_t i = 0; i < r->cnots[g].size(); ++i) cnots[i] = r->cnots[g][i];
+    for (size_t i = 0; i < r->czs[g].size(); ++i) czs[i] = r->czs[g][i];
+    for (size_t i = 0; i < c.s_layer.size(); ++i) s[i] = c.s_layer[i];
+    for (size_t i = 0; i < c.h_post.size(); ++i) h_post[i] = c.h_post[i];
+    const auto& t = r->parts[g].terms;
+    for (size_t i = 0; i < t.size(); ++i) {
+        src_x[i] = t[i].pauli.x_mask();
+        src_z[i] = t[i].pauli.z_mask();
+        src_c[i] = t[i].coeff;
+        if (i < d.z_masks.size()) {
+            zm[i] = d.z_masks[i];
+            cf[i] = d.signed_coeffs[i];
+        }
+    }
+}
+
+// evolve_grouped (evolve.cpp:47-58) over every group of `h`, in place on
+// re_im (2^n interleaved doubles). order 2 = S2 composition. stats (may be
+// NULL) receives KernelStats {reads, writes, calls}.
+int ref_evolve_grouped(void* h, double* re_im, int n, double dt, int steps, int order, uint64_t* stats) {
+    return guarded([&] {
+        auto* r = static_cast<RefGroups*>(h);
+        simdiag::StateVector psi(n);
+        load_state(psi, re_im);
+        const auto& gs = r->diags;
+        const size_t G = gs.size();
+        for (int s = 0; s < steps; ++s) {
+            if (order == 1 || G <= 1) {
+                for (const auto& g : gs) apply_group(psi, g, dt);
+            } else {
+                for (size_t g = 0; g + 1 < G; ++g) apply_group(psi, gs[g], 0.5 * dt);
+                apply_group(psi, gs[G - 1], dt);
+                for (size_t g = G - 1; g-- > 0;) apply_group(psi, gs[g], 0.5 * dt);
+            }
+        }
+        store_state(psi, re_im);
+        if (stats) {
+            stats[0] = psi.stats().amp_reads;
+            stats[1] = psi.stats().amp_writes;
+            stats[2] = psi.stats().kernel_calls;
+        }
+    });
+}
+
+int ref_random_state(int n, uint64_t seed, double* re_im) {
+    return guarded([&] { store_state(simdiag::StateVector::random_state(n, seed), re_im); });
+}
+
+int ref_plus_state(int n, double* re_im) {
+    return guarded([&] { store_state(simdiag::StateVector::plus_state(n), re_im); });
+}
+
+// Single-kernel entry points (statevector.cpp:156-286) on a host buffer.
+int ref_kernel(int which, double* re_im, int n, int a, uint64_t mask, const int32_t* pairs, size_t np,
+               const uint64_t* zm, const double* cf, size_t m, double dt) {
+    return guarded([&] {
+        simdiag::StateVector psi(n);
+        load_state(psi, re_im);
+        std::vector<std::pair<int, int>> pv;
+        for (size_t k = 0; k < np; ++k) pv.emplace_back(pairs[2 * k], pairs[2 * k + 1]);
+        switch (which) {
+            case 0: psi.apply_hadamard(a); break;
+            case 1: psi.apply_batched_cnot(a, mask); break;
+            case 2: psi.apply_phase_layer(mask, pv, a != 0); break;
+            case 3: psi.apply_diagonal_exp(std::span<const uint64_t>(zm, m), std::span<const double>(cf, m), dt); break;
+            default: throw std::invalid_argument("unknown kernel");
+        }
+        store_state(psi, re_im);
+    });
+}
+
+double ref_norm(const double* re_im, int n) {
+    simdiag::StateVector psi(n);
+    for (std::uint64_t i = 0; i < psi.dim(); ++i) psi[i] = {re_im[2 * i], re_im[2 * i + 1]};
+    return simdiag::norm(psi);
+}
+
+}  // extern "C"

@@ -1,0 +1,34 @@
+"""simdiag-b200: B200-native Trotter hot path of arXiv 2206.11664.
+
+Grouping and Clifford synthesis run in from-scratch host C++ (bit-exact with
+the reference); the state-vector work runs as hand-written sm_100a CUDA tile
+passes behind the C ABI in include/simdiag_c.h. This package is the Python
+mirror of the reference's C++ API over that ABI.
+"""
+from .simdiag import (  # noqa: F401
+    K_DROP_TOLERANCE,
+    K_MAX_QUBITS,
+    CliffordCircuit,
+    CommutingGroup,
+    DiagonalGroup,
+    EvolutionPlan,
+    Hamiltonian,
+    PauliString,
+    StateVector,
+    TrotterPlan,
+    WeightedTerm,
+    commutes,
+    diagonalize_group,
+    evolve_grouped,
+    fidelity,
+    greedy_partition,
+    norm,
+    partition_and_diagonalize,
+)
+from . import models  # noqa: F401
+
+__all__ = [
+    "CliffordCircuit", "CommutingGroup", "DiagonalGroup", "EvolutionPlan", "Hamiltonian",
+    "PauliString", "StateVector", "TrotterPlan", "WeightedTerm", "commutes", "diagonalize_group",
+    "evolve_grouped", "fidelity", "greedy_partition", "norm", "partition_and_diagonalize", "models",
+]

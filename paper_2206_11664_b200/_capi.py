@@ -1,0 +1,195 @@
+"""ctypes declarations for libsimdiag_b200.so (include/simdiag_c.h).
+
+The shared library is the product: host grouping/synthesis in C++ and the
+sm_100a kernels. There is no fallback: if the library is missing, importing
+this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libsimdiag_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(no CPU fallback exists by design)"
+    )
+
+lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+
+u64 = C.c_uint64
+i32 = C.c_int32
+P = C.c_void_p
+sz = C.c_size_t
+dbl = C.c_double
+
+
+class GroupDesc(C.Structure):
+    _fields_ = [
+        ("group_index", C.c_int),
+        ("n_qubits", C.c_int),
+        ("n_h_pre", sz), ("h_pre", C.POINTER(i32)),
+        ("n_cnots", sz), ("cnots", C.POINTER(i32)),
+        ("n_czs", sz), ("czs", C.POINTER(i32)),
+        ("n_s", sz), ("s_layer", C.POINTER(i32)),
+        ("n_h_post", sz), ("h_post", C.POINTER(i32)),
+        ("n_terms", sz),
+        ("z_masks", C.POINTER(u64)),
+        ("signed_coeffs", C.POINTER(dbl)),
+        ("src_x", C.POINTER(u64)),
+        ("src_z", C.POINTER(u64)),
+        ("src_coeffs", C.POINTER(dbl)),
+    ]
+
+
+class KernelStats(C.Structure):
+    _fields_ = [("amp_reads", u64), ("amp_writes", u64), ("kernel_calls", u64)]
+
+
+class PlanOptions(C.Structure):
+    _fields_ = [
+        ("order", C.c_int),
+        ("tile_qubits", C.c_int),
+        ("fuse", C.c_int),
+        ("use_graph", C.c_int),
+        ("relabel", C.c_int),
+        ("reserved", C.c_int * 7),
+    ]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [
+        ("n_passes_per_step", C.c_int),
+        ("n_ref_sweeps_per_step", C.c_int),
+        ("n_group_applications", C.c_int),
+        ("n_exchanges_per_step", C.c_int),
+        ("tile_qubits", C.c_int),
+        ("n_kernels_per_step", C.c_int),
+        ("bytes_per_step", dbl),
+    ]
+
+
+def _sig(name, argtypes, restype=C.c_int):
+    f = getattr(lib, name)
+    f.argtypes = argtypes
+    f.restype = restype
+    return f
+
+
+PP = C.POINTER(P)
+sd_last_error = _sig("sd_last_error", [], C.c_char_p)
+sd_version = _sig("sd_version", [], C.c_char_p)
+sd_hamiltonian_from_terms = _sig(
+    "sd_hamiltonian_from_terms",
+    [C.c_int, C.POINTER(u64), C.POINTER(u64), C.POINTER(dbl), sz, dbl, C.POINTER(sz), PP],
+)
+sd_hamiltonian_load_text = _sig("sd_hamiltonian_load_text", [C.c_char_p, sz, dbl, PP])
+sd_hamiltonian_load_file = _sig("sd_hamiltonian_load_file", [C.c_char_p, dbl, PP])
+sd_hamiltonian_save_text = _sig("sd_hamiltonian_save_text", [P, C.c_char_p, sz, C.POINTER(sz)])
+sd_hamiltonian_info = _sig("sd_hamiltonian_info", [P, C.POINTER(C.c_int), C.POINTER(sz)])
+sd_hamiltonian_terms = _sig("sd_hamiltonian_terms", [P, C.POINTER(u64), C.POINTER(u64), C.POINTER(dbl)])
+sd_hamiltonian_destroy = _sig("sd_hamiltonian_destroy", [P], None)
+sd_partition = _sig("sd_partition", [P, PP])
+sd_partition_only = _sig("sd_partition_only", [P, PP])
+sd_diagonalize_terms = _sig(
+    "sd_diagonalize_terms", [C.c_int, C.POINTER(u64), C.POINTER(u64), C.POINTER(dbl), sz, PP]
+)
+sd_groups_count = _sig("sd_groups_count", [P, C.POINTER(sz)])
+sd_groups_destroy = _sig("sd_groups_destroy", [P], None)
+sd_group_get = _sig("sd_group_get", [P, sz, C.POINTER(GroupDesc)])
+
+sd_state_create = _sig("sd_state_create", [C.c_int, C.c_int, PP])
+sd_state_create_shard = _sig("sd_state_create_shard", [C.c_int, C.c_int, C.c_int, C.c_int, PP])
+sd_state_destroy = _sig("sd_state_destroy", [P], None)
+sd_state_info = _sig("sd_state_info", [P] + [C.POINTER(C.c_int)] * 4)
+sd_state_stream = _sig("sd_state_stream", [P, PP])
+sd_state_device_ptr = _sig("sd_state_device_ptr", [P, PP])
+sd_sync = _sig("sd_sync", [P])
+sd_state_set_basis = _sig("sd_state_set_basis", [P, u64])
+sd_state_set_plus = _sig("sd_state_set_plus", [P])
+sd_state_set_random = _sig("sd_state_set_random", [P, u64])
+sd_state_upload = _sig("sd_state_upload", [P, P, u64])
+sd_state_download = _sig("sd_state_download", [P, P, u64])
+sd_state_norm_sq = _sig("sd_state_norm_sq", [P, C.POINTER(dbl)])
+sd_state_inner = _sig("sd_state_inner", [P, P, C.POINTER(dbl), C.POINTER(dbl)])
+sd_state_copy = _sig("sd_state_copy", [P, P])
+sd_kernel_stats_get = _sig("sd_kernel_stats_get", [P, C.POINTER(KernelStats)])
+sd_kernel_stats_reset = _sig("sd_kernel_stats_reset", [P])
+sd_apply_hadamard = _sig("sd_apply_hadamard", [P, C.c_int])
+sd_apply_batched_cnot = _sig("sd_apply_batched_cnot", [P, C.c_int, u64])
+sd_apply_phase_layer = _sig("sd_apply_phase_layer", [P, u64, C.POINTER(i32), sz, C.c_int])
+sd_apply_diagonal_exp = _sig("sd_apply_diagonal_exp", [P, C.POINTER(u64), C.POINTER(dbl), sz, dbl])
+sd_apply_clifford = _sig("sd_apply_clifford", [P, C.POINTER(GroupDesc)])
+sd_apply_clifford_inverse = _sig("sd_apply_clifford_inverse", [P, C.POINTER(GroupDesc)])
+
+sd_plan_options_default = _sig("sd_plan_options_default", [C.POINTER(PlanOptions)])
+sd_plan_create = _sig("sd_plan_create", [P, C.POINTER(GroupDesc), sz, C.POINTER(PlanOptions), PP])
+sd_plan_destroy = _sig("sd_plan_destroy", [P], None)
+sd_plan_get_info = _sig("sd_plan_get_info", [P, C.POINTER(PlanInfo)])
+sd_plan_describe = _sig("sd_plan_describe", [P, C.c_char_p, sz, C.POINTER(sz)])
+sd_evolve = _sig("sd_evolve", [P, dbl, C.c_int])
+sd_evolve_async = _sig("sd_evolve_async", [P, dbl, C.c_int])
+sd_plan_set_profiling = _sig("sd_plan_set_profiling", [P, C.c_int])
+sd_plan_kernel_times = _sig(
+    "sd_plan_kernel_times", [P, C.POINTER(dbl), C.POINTER(u64), C.POINTER(dbl), C.c_int]
+)
+sd_comm_unique_id = _sig("sd_comm_unique_id", [C.c_char_p])
+sd_state_attach_comm = _sig("sd_state_attach_comm", [P, C.c_char_p])
+
+EXPORTED = [
+    "sd_last_error", "sd_version",
+    "sd_hamiltonian_from_terms", "sd_hamiltonian_load_text", "sd_hamiltonian_load_file",
+    "sd_hamiltonian_save_text", "sd_hamiltonian_info", "sd_hamiltonian_terms",
+    "sd_hamiltonian_destroy", "sd_partition", "sd_partition_only", "sd_diagonalize_terms",
+    "sd_groups_count", "sd_groups_destroy", "sd_group_get",
+    "sd_state_create", "sd_state_create_shard", "sd_state_destroy", "sd_state_info",
+    "sd_state_stream", "sd_state_device_ptr", "sd_sync", "sd_state_set_basis", "sd_state_set_plus",
+    "sd_state_set_random", "sd_state_upload", "sd_state_download", "sd_state_norm_sq",
+    "sd_state_inner", "sd_state_copy", "sd_kernel_stats_get", "sd_kernel_stats_reset",
+    "sd_apply_hadamard", "sd_apply_batched_cnot", "sd_apply_phase_layer", "sd_apply_diagonal_exp",
+    "sd_apply_clifford", "sd_apply_clifford_inverse",
+    "sd_plan_options_default", "sd_plan_create", "sd_plan_destroy", "sd_plan_get_info",
+    "sd_plan_describe", "sd_evolve", "sd_evolve_async", "sd_plan_set_profiling",
+    "sd_plan_kernel_times", "sd_comm_unique_id", "sd_state_attach_comm",
+]
+
+
+class SimdiagError(RuntimeError):
+    pass
+
+
+class CudaError(SimdiagError):
+    pass
+
+
+class NcclError(SimdiagError):
+    pass
+
+
+class OutOfMemory(SimdiagError, MemoryError):
+    pass
+
+
+def check(status: int) -> None:
+    """Map sd_status onto the reference's exception types
+    (invalid_argument -> ValueError, out_of_range -> IndexError,
+    runtime_error -> RuntimeError)."""
+    if status == 0:
+        return
+    msg = (sd_last_error() or b"").decode(errors="replace")
+    if status == 1:
+        raise ValueError(msg)
+    if status == 2:
+        raise IndexError(msg)
+    if status == 3:
+        raise RuntimeError(msg)
+    if status == 4:
+        raise CudaError(msg)
+    if status == 5:
+        raise NcclError(msg)
+    if status == 6:
+        raise OutOfMemory(msg)
+    raise SimdiagError(f"status {status}: {msg}")

@@ -1,0 +1,774 @@
+// extern "C" device entry points: state lifecycle, the reference's
+// single-sweep kernels, and the fused Trotter plan (evolve_grouped).
+#include <cuda_runtime_api.h>
+
+#include <algorithm>
+#include <bit>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+
+#include "../plan/planner.hpp"
+#include "guard.hpp"
+
+namespace sdb {
+void write_text_out(const std::string& s, char* buf, size_t cap, size_t* len);
+}
+
+struct sd_state {
+    sdb::StateImpl impl;
+};
+
+struct sd_plan {
+    sd_state* state = nullptr;
+    std::vector<sdb::GroupSpec> groups;
+    sd_plan_options opts{};
+    sdb::StepPlan step;
+    std::vector<sdb::PassDev> host_passes;
+    std::vector<int> pass_class;  // 0 fused, 1 diagonal-only
+    sdb::PlanDev dev{};
+    void* dev_block = nullptr;    // one allocation backing every PlanDev array
+    bool profiling = false;
+    double ms[4] = {0, 0, 0, 0};
+    uint64_t launches[4] = {0, 0, 0, 0};
+    double bytes[4] = {0, 0, 0, 0};
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
+    std::vector<int> ev_class;
+    size_t ev_used = 0;
+    cudaGraphExec_t graph = nullptr;
+    double graph_dt = 0.0;
+    int n_ref_sweeps = 0;
+};
+
+namespace {
+
+using sdb::guard;
+using sdb::require;
+
+sdb::StateImpl& st(sd_state* s) {
+    if (!s) throw std::invalid_argument("null state");
+    return s->impl;
+}
+
+void check_qubit(const sdb::StateImpl& s, int q) {
+    if (q < 0 || q >= s.n) throw std::out_of_range("qubit index out of range");
+}
+
+void require_unsharded(const sdb::StateImpl& s) {
+    if (s.world != 1) throw std::invalid_argument("single-sweep kernels need an unsharded state");
+}
+
+void require_identity_layout(const sdb::StateImpl& s) {
+    for (int q = 0; q < s.n; ++q) {
+        if (s.phys_of[q] != q) throw std::logic_error("state layout is relabelled");
+    }
+}
+
+void bump(sdb::StateImpl& s, uint64_t reads, uint64_t writes) {
+    s.stats.amp_reads += reads;
+    s.stats.amp_writes += writes;
+    s.stats.kernel_calls += 1;
+}
+
+void hadamard(sdb::StateImpl& s, int t) {
+    check_qubit(s, t);
+    sdb::launch_hadamard(s, t);
+    bump(s, s.amps_count(), s.amps_count());
+}
+
+void batched_cnot(sdb::StateImpl& s, int c, uint64_t targets) {
+    check_qubit(s, c);
+    const uint64_t all = s.amps_count() - 1;
+    if (targets == 0) throw std::invalid_argument("batched cnot needs at least one target");
+    if ((targets & ~all) || (targets & (1ull << c))) {
+        throw std::invalid_argument("batched cnot targets overlap control or exceed register");
+    }
+    sdb::launch_batched_cnot(s, c, targets);
+    bump(s, s.amps_count() >> 1, s.amps_count() >> 1);
+}
+
+void phase_layer(sdb::StateImpl& s, uint64_t s_mask, const int32_t* pairs, size_t n_pairs, bool dagger) {
+    if (s_mask & ~(s.amps_count() - 1)) throw std::invalid_argument("phase layer s_mask exceeds register");
+    require(n_pairs == 0 || pairs != nullptr, "null cz pair array");
+    std::vector<uint64_t> pm;
+    for (size_t k = 0; k < n_pairs; ++k) {
+        const int a = pairs[2 * k], b = pairs[2 * k + 1];
+        check_qubit(s, a);
+        check_qubit(s, b);
+        if (a == b) throw std::invalid_argument("cz pair with equal qubits");
+        pm.push_back((1ull << a) | (1ull << b));
+    }
+    sdb::launch_phase_layer(s, s_mask, pm, dagger);
+    bump(s, s.amps_count(), s.amps_count());
+}
+
+void diag_exp(sdb::StateImpl& s, const uint64_t* masks, const double* coeffs, size_t m, double dt) {
+    require(m == 0 || (masks && coeffs), "null diagonal arrays");
+    if (!std::isfinite(dt)) throw std::invalid_argument("diagonal exp: non-finite time step");
+    const uint64_t all = s.amps_count() - 1;
+    for (size_t k = 0; k < m; ++k) {
+        if (masks[k] & ~all) throw std::invalid_argument("diagonal exp: mask exceeds register");
+    }
+    sdb::launch_diag_exp(s, std::vector<uint64_t>(masks, masks + m), std::vector<double>(coeffs, coeffs + m), dt);
+    bump(s, s.amps_count(), s.amps_count());
+}
+
+sdb::GroupSpec spec_of(const sd_group_desc& d) {
+    sdb::GroupSpec g;
+    g.h_pre.assign(d.h_pre, d.h_pre + d.n_h_pre);
+    g.s_layer.assign(d.s_layer, d.s_layer + d.n_s);
+    g.h_post.assign(d.h_post, d.h_post + d.n_h_post);
+    for (size_t k = 0; k < d.n_cnots; ++k) g.cnots.emplace_back(d.cnots[2 * k], d.cnots[2 * k + 1]);
+    for (size_t k = 0; k < d.n_czs; ++k) g.czs.emplace_back(d.czs[2 * k], d.czs[2 * k + 1]);
+    if (d.n_terms) {
+        require(d.z_masks && d.signed_coeffs, "group has no diagonal (not synthesised)");
+        g.z_masks.assign(d.z_masks, d.z_masks + d.n_terms);
+        g.coeffs.assign(d.signed_coeffs, d.signed_coeffs + d.n_terms);
+    }
+    return g;
+}
+
+// Reference apply_clifford / apply_clifford_inverse (statevector.cpp:339-381).
+void clifford_unfused(sdb::StateImpl& s, const sdb::GroupSpec& g, bool inverse) {
+    std::vector<std::pair<int, uint64_t>> runs;
+    for (size_t k = 0; k < g.cnots.size();) {
+        const int c = g.cnots[k].first;
+        uint64_t t = 0;
+        while (k < g.cnots.size() && g.cnots[k].first == c) t |= 1ull << g.cnots[k++].second;
+        runs.emplace_back(c, t);
+    }
+    std::vector<int32_t> pairs;
+    for (auto [a, b] : g.czs) pairs.insert(pairs.end(), {a, b});
+    uint64_t smask = 0;
+    for (int q : g.s_layer) smask |= 1ull << q;
+    const bool ph = !g.czs.empty() || !g.s_layer.empty();
+    if (!inverse) {
+        for (int q : g.h_pre) hadamard(s, q);
+        for (auto [c, t] : runs) batched_cnot(s, c, t);
+        if (ph) phase_layer(s, smask, pairs.data(), g.czs.size(), false);
+        for (int q : g.h_post) hadamard(s, q);
+    } else {
+        for (int q : g.h_post) hadamard(s, q);
+        if (ph) phase_layer(s, smask, pairs.data(), g.czs.size(), true);
+        for (auto it = runs.rbegin(); it != runs.rend(); ++it) batched_cnot(s, it->first, it->second);
+        for (int q : g.h_pre) hadamard(s, q);
+    }
+}
+
+// ---------------------------------------------------------------- plan build
+constexpr int kTableThreshold = 8;  // terms per POINT stage above which the WHT table is used
+
+void build_device_plan(sd_plan& p) {
+    sdb::StateImpl& s = p.state->impl;
+    std::vector<sdb::PassDev> passes;
+    std::vector<sdb::StageDev> stages;
+    std::vector<sdb::PointDev> points;
+    std::vector<sdb::SegDev> segs;
+    std::vector<uint64_t> czm, tmask;
+    std::vector<double> tcoef;
+    p.pass_class.clear();
+    for (const sdb::PassPlan& pp : p.step.passes) {
+        sdb::PassDev pd{};
+        pd.k = static_cast<int>(pp.lpos.size());
+        uint64_t Lphys = 0;
+        for (size_t j = 0; j < pp.lpos.size(); ++j) {
+            pd.lpos[j] = pp.lpos[j];
+            Lphys |= 1ull << pp.lpos[j];
+        }
+        int no = 0;
+        for (int b = 0; b < s.n_local; ++b) {
+            if (!(Lphys & (1ull << b))) pd.opos[no++] = b;
+        }
+        pd.n_outer = no;
+        pd.stage_off = static_cast<int>(stages.size());
+        pd.n_stages = static_cast<int>(pp.stages.size());
+        pd.scale = std::ldexp(1.0, -pp.scale_exp);
+        pd.flags = 0;
+        bool only_point = true;
+        for (const sdb::PassStage& ps : pp.stages) {
+            sdb::StageDev sd{};
+            sd.kind = ps.kind == sdb::PassStage::WHT ? sdb::kStageWht
+                      : ps.kind == sdb::PassStage::CX ? sdb::kStageCx
+                                                      : sdb::kStagePoint;
+            sd.mask = ps.mask;
+            sd.ctrl_local = ps.ctrl_local;
+            sd.ctrl_phys = ps.ctrl_phys;
+            sd.point = -1;
+            if (ps.kind != sdb::PassStage::POINT) only_point = false;
+            if (ps.kind == sdb::PassStage::POINT) {
+                const sdb::PointSpec& spec = pp.points[ps.point];
+                sdb::PointDev pt{};
+                pt.s1 = spec.s1;
+                pt.s2 = spec.s2;
+                pt.cz_off = static_cast<int>(czm.size());
+                pt.n_cz = static_cast<int>(spec.cz_masks.size());
+                czm.insert(czm.end(), spec.cz_masks.begin(), spec.cz_masks.end());
+                pt.term_off = static_cast<int>(tmask.size());
+                pt.n_terms = static_cast<int>(spec.terms.size());
+                if (pt.n_terms > kTableThreshold) {
+                    // group terms by local part (stable: keeps term order inside a segment)
+                    struct T {
+                        uint32_t u;
+                        uint64_t zh;
+                        double c;
+                    };
+                    std::vector<T> ts;
+                    for (const sdb::PointTerm& t : spec.terms) {
+                        uint32_t u = 0;
+                        for (size_t j = 0; j < pp.lpos.size(); ++j) {
+                            if (t.mask & (1ull << pp.lpos[j])) u |= 1u << j;
+                        }
+                        ts.push_back({u, t.mask & ~Lphys, t.coeff * t.dt_scale});
+                    }
+                    std::stable_sort(ts.begin(), ts.end(), [](const T& a, const T& b) { return a.u < b.u; });
+                    pt.seg_off = static_cast<int>(segs.size());
+                    uint32_t tm = 0;
+                    for (size_t i = 0; i < ts.size();) {
+                        size_t j = i;
+                        while (j < ts.size() && ts[j].u == ts[i].u) ++j;
+                        segs.push_back({ts[i].u, static_cast<int>(i), static_cast<int>(j), 0});
+                        tm |= ts[i].u;
+                        i = j;
+                    }
+                    pt.n_seg = static_cast<int>(segs.size()) - pt.seg_off;
+                    pt.table_mask = tm;
+                    for (const T& t : ts) {
+                        tmask.push_back(t.zh);
+                        tcoef.push_back(t.c);
+                    }
+                    pd.flags |= sdb::kPassNeedsTable;
+                } else {
+                    for (const sdb::PointTerm& t : spec.terms) {
+                        tmask.push_back(t.mask);
+                        tcoef.push_back(t.coeff * t.dt_scale);
+                    }
+                }
+                sd.point = static_cast<int>(points.size());
+                points.push_back(pt);
+            }
+            stages.push_back(sd);
+        }
+        passes.push_back(pd);
+        p.pass_class.push_back(only_point ? 1 : 0);
+    }
+    // one device block, 16-byte aligned sub-arrays
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t b_pass = al(passes.size() * sizeof(sdb::PassDev));
+    const size_t b_stage = al(std::max<size_t>(1, stages.size()) * sizeof(sdb::StageDev));
+    const size_t b_point = al(std::max<size_t>(1, points.size()) * sizeof(sdb::PointDev));
+    const size_t b_seg = al(std::max<size_t>(1, segs.size()) * sizeof(sdb::SegDev));
+    const size_t b_cz = al(std::max<size_t>(1, czm.size()) * 8);
+    const size_t b_tm = al(std::max<size_t>(1, tmask.size()) * 8);
+    const size_t b_tc = al(std::max<size_t>(1, tcoef.size()) * 8);
+    const size_t total = b_pass + b_stage + b_point + b_seg + b_cz + b_tm + b_tc;
+    SDB_CUDA(cudaSetDevice(s.device));
+    if (p.dev_block) SDB_CUDA(cudaFree(p.dev_block));
+    SDB_CUDA(cudaMalloc(&p.dev_block, total));
+    std::vector<unsigned char> host(total, 0);
+    size_t off = 0;
+    auto put = [&](const void* src, size_t bytes, size_t span) {
+        if (bytes) std::memcpy(host.data() + off, src, bytes);
+        void* dptr = static_cast<unsigned char*>(p.dev_block) + off;
+        off += span;
+        return dptr;
+    };
+    p.dev.passes = static_cast<const sdb::PassDev*>(put(passes.data(), passes.size() * sizeof(sdb::PassDev), b_pass));
+    p.dev.stages = static_cast<const sdb::StageDev*>(put(stages.data(), stages.size() * sizeof(sdb::StageDev), b_stage));
+    p.dev.points = static_cast<const sdb::PointDev*>(put(points.data(), points.size() * sizeof(sdb::PointDev), b_point));
+    p.dev.segs = static_cast<const sdb::SegDev*>(put(segs.data(), segs.size() * sizeof(sdb::SegDev), b_seg));
+    p.dev.cz_masks = static_cast<const uint64_t*>(put(czm.data(), czm.size() * 8, b_cz));
+    p.dev.term_masks = static_cast<const uint64_t*>(put(tmask.data(), tmask.size() * 8, b_tm));
+    p.dev.term_coeffs = static_cast<const double*>(put(tcoef.data(), tcoef.size() * 8, b_tc));
+    SDB_CUDA(cudaMemcpy(p.dev_block, host.data(), total, cudaMemcpyHostToDevice));
+    p.host_passes = std::move(passes);
+}
+
+void plan_build(sd_plan& p) {
+    sdb::StateImpl& s = p.state->impl;
+    const int order = p.opts.order;
+    require(order == 1 || order == 2, "trotter order must be 1 or 2");
+    p.n_ref_sweeps = static_cast<int>(std::lround(sdb::reference_sweeps(p.groups, order)));
+    if (!p.opts.fuse) return;
+    int k = p.opts.tile_qubits > 0 ? p.opts.tile_qubits : 12;
+    k = std::min({k, sdb::max_tile_qubits(), s.n_local});
+    const auto ops = sdb::step_ops(p.groups, s.n, order);
+    p.step = sdb::plan_step(ops, p.groups, s.n_local, k, 3, s.phys_of);
+    p.step.ref_sweeps = sdb::reference_sweeps(p.groups, order);
+    build_device_plan(p);
+}
+
+void record_start(sd_plan& p, int cls) {
+    if (!p.profiling) return;
+    if (p.ev_used == p.ev_pool.size()) {
+        cudaEvent_t a, b;
+        SDB_CUDA(cudaEventCreate(&a));
+        SDB_CUDA(cudaEventCreate(&b));
+        p.ev_pool.emplace_back(a, b);
+        p.ev_class.push_back(0);
+    }
+    p.ev_class[p.ev_used] = cls;
+    SDB_CUDA(cudaEventRecord(p.ev_pool[p.ev_used].first, p.state->impl.stream));
+}
+
+void record_end(sd_plan& p, double bytes) {
+    if (!p.profiling) return;
+    SDB_CUDA(cudaEventRecord(p.ev_pool[p.ev_used].second, p.state->impl.stream));
+    p.bytes[p.ev_class[p.ev_used]] += bytes;
+    p.launches[p.ev_class[p.ev_used]] += 1;
+    ++p.ev_used;
+}
+
+void harvest(sd_plan& p) {
+    if (!p.profiling || p.ev_used == 0) return;
+    SDB_CUDA(cudaStreamSynchronize(p.state->impl.stream));
+    for (size_t i = 0; i < p.ev_used; ++i) {
+        float ms = 0.f;
+        SDB_CUDA(cudaEventElapsedTime(&ms, p.ev_pool[i].first, p.ev_pool[i].second));
+        p.ms[p.ev_class[i]] += ms;
+    }
+    p.ev_used = 0;
+}
+
+void run_step_fused(sd_plan& p, double dt) {
+    sdb::StateImpl& s = p.state->impl;
+    const uint64_t rank_bits = uint64_t(s.rank) << s.n_local;
+    const double bytes = 2.0 * 16.0 * double(s.amps_count());
+    for (size_t i = 0; i < p.host_passes.size(); ++i) {
+        record_start(p, p.pass_class[i]);
+        sdb::launch_tile_pass(s, p.host_passes[i], static_cast<int>(i), p.dev, dt, rank_bits);
+        record_end(p, bytes);
+        bump(s, s.amps_count(), s.amps_count());
+        if (p.profiling && p.ev_used >= 4096) harvest(p);
+    }
+}
+
+void run_step_unfused(sd_plan& p, double dt) {
+    sdb::StateImpl& s = p.state->impl;
+    auto apply = [&](const sdb::GroupSpec& g, double f) {
+        clifford_unfused(s, g, false);
+        diag_exp(s, g.z_masks.data(), g.coeffs.data(), g.z_masks.size(), dt * f);
+        clifford_unfused(s, g, true);
+    };
+    const int G = static_cast<int>(p.groups.size());
+    if (p.opts.order == 1 || G <= 1) {
+        for (const auto& g : p.groups) apply(g, 1.0);
+    } else {
+        for (int g = 0; g < G - 1; ++g) apply(p.groups[g], 0.5);
+        apply(p.groups[G - 1], 1.0);
+        for (int g = G - 2; g >= 0; --g) apply(p.groups[g], 0.5);
+    }
+}
+
+void evolve(sd_plan& p, double dt, int n_steps, bool wait) {
+    require(std::isfinite(dt), "plan needs finite total_time");
+    if (n_steps < 0) throw std::invalid_argument("plan needs n_steps >= 0");
+    sdb::StateImpl& s = p.state->impl;
+    SDB_CUDA(cudaSetDevice(s.device));
+    for (int step = 0; step < n_steps; ++step) {
+        if (p.opts.fuse) run_step_fused(p, dt);
+        else run_step_unfused(p, dt);
+    }
+    if (wait) SDB_CUDA(cudaStreamSynchronize(s.stream));
+    harvest(p);
+}
+
+}  // namespace
+
+extern "C" {
+
+sd_status sd_state_create_shard(int n, int rank, int world, int device, sd_state** out) {
+    return guard([&] {
+        require(out != nullptr, "out is null");
+        if (n < 0 || n > 40) throw std::invalid_argument("state vector qubit count out of range");
+        require(world >= 1 && (world & (world - 1)) == 0, "world size must be a power of two");
+        require(rank >= 0 && rank < world, "rank out of range");
+        const int g = std::countr_zero(static_cast<unsigned>(world));
+        require(n - g >= 1, "too many ranks for this state");
+        auto h = std::make_unique<sd_state>();
+        sdb::StateImpl& s = h->impl;
+        s.n = n;
+        s.n_local = n - g;
+        s.rank = rank;
+        s.world = world;
+        s.device = device;
+        s.phys_of.resize(n);
+        std::iota(s.phys_of.begin(), s.phys_of.end(), 0);
+        SDB_CUDA(cudaSetDevice(device));
+        SDB_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+        const size_t bytes = sizeof(double) * 2 * s.amps_count();
+        cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&s.amps), bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            cudaStreamDestroy(s.stream);
+            throw sdb::OomError("cannot allocate " + std::to_string(bytes) + " bytes of state");
+        }
+        sdb::launch_set_basis(s, rank == 0 ? 0 : ~0ull);
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+        *out = h.release();
+    });
+}
+
+
+sd_status sd_state_create(int n, int device, sd_state** out) { return sd_state_create_shard(n, 0, 1, device, out); }
+
+void sd_state_destroy(sd_state* h) {
+    if (!h) return;
+    sdb::StateImpl& s = h->impl;
+    cudaSetDevice(s.device);
+    if (s.stream) cudaStreamSynchronize(s.stream);
+    if (s.amps) cudaFree(s.amps);
+    if (s.xbuf) cudaFree(s.xbuf);
+    if (s.reduce_buf) cudaFree(s.reduce_buf);
+    if (s.stream) cudaStreamDestroy(s.stream);
+    delete h;
+}
+
+sd_status sd_state_info(const sd_state* h, int* n, int* nl, int* rank, int* world) {
+    return guard([&] {
+        require(h != nullptr, "null state");
+        if (n) *n = h->impl.n;
+        if (nl) *nl = h->impl.n_local;
+        if (rank) *rank = h->impl.rank;
+        if (world) *world = h->impl.world;
+    });
+}
+
+sd_status sd_state_stream(const sd_state* h, void** stream) {
+    return guard([&] {
+        require(h != nullptr && stream != nullptr, "null argument");
+        *stream = h->impl.stream;
+    });
+}
+
+sd_status sd_state_device_ptr(const sd_state* h, void** ptr) {
+    return guard([&] {
+        require(h != nullptr && ptr != nullptr, "null argument");
+        *ptr = h->impl.amps;
+    });
+}
+
+sd_status sd_sync(sd_state* h) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        SDB_CUDA(cudaSetDevice(s.device));
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
+sd_status sd_state_set_basis(sd_state* h, uint64_t index) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        if (s.n < 64 && (index >> s.n) != 0) throw std::out_of_range("basis index out of range");
+        SDB_CUDA(cudaSetDevice(s.device));
+        std::iota(s.phys_of.begin(), s.phys_of.end(), 0);
+        const uint64_t owner = index >> s.n_local;
+        sdb::launch_set_basis(s, owner == uint64_t(s.rank) ? (index & (s.amps_count() - 1)) : ~0ull);
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
+sd_status sd_state_set_plus(sd_state* h) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        SDB_CUDA(cudaSetDevice(s.device));
+        std::iota(s.phys_of.begin(), s.phys_of.end(), 0);
+        // plus_state: 1/sqrt(dim) everywhere (statevector.cpp:74-79)
+        const double a = 1.0 / std::sqrt(std::ldexp(1.0, s.n));
+        sdb::launch_fill(s, a, 0.0);
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
+sd_status sd_state_set_random(sd_state* h, uint64_t seed) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require(s.world == 1, "sharded random_state needs a cross-rank norm; use set_random_unnormalized + norm");
+        SDB_CUDA(cudaSetDevice(s.device));
+        std::iota(s.phys_of.begin(), s.phys_of.end(), 0);
+        sdb::launch_random(s, seed);
+        const double nsq = sdb::device_norm_sq(s);
+        sdb::launch_scale(s, 1.0 / std::sqrt(nsq));
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
+sd_status sd_state_upload(sd_state* h, const double* re_im, uint64_t n_amps) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require(re_im != nullptr, "null host buffer");
+        require(n_amps == s.amps_count(), "upload size does not match the shard");
+        SDB_CUDA(cudaSetDevice(s.device));
+        std::iota(s.phys_of.begin(), s.phys_of.end(), 0);
+        SDB_CUDA(cudaMemcpyAsync(s.amps, re_im, n_amps * 16, cudaMemcpyHostToDevice, s.stream));
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
+sd_status sd_state_download(sd_state* h, double* re_im, uint64_t n_amps) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require(re_im != nullptr, "null host buffer");
+        require(n_amps == s.amps_count(), "download size does not match the shard");
+        require_identity_layout(s);
+        SDB_CUDA(cudaSetDevice(s.device));
+        SDB_CUDA(cudaMemcpyAsync(re_im, s.amps, n_amps * 16, cudaMemcpyDeviceToHost, s.stream));
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
+sd_status sd_state_norm_sq(sd_state* h, double* out) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require(out != nullptr, "null output");
+        SDB_CUDA(cudaSetDevice(s.device));
+        *out = sdb::device_norm_sq(s);
+    });
+}
+
+sd_status sd_state_inner(sd_state* a, sd_state* b, double* re, double* im) {
+    return guard([&] {
+        sdb::StateImpl& x = st(a);
+        sdb::StateImpl& y = st(b);
+        require(re != nullptr, "null output");
+        if (x.n != y.n || x.n_local != y.n_local) throw std::invalid_argument("fidelity: dimension mismatch");
+        require_identity_layout(x);
+        require_identity_layout(y);
+        SDB_CUDA(cudaSetDevice(x.device));
+        SDB_CUDA(cudaStreamSynchronize(y.stream));
+        sdb::device_inner(x, y, re, im);
+    });
+}
+
+sd_status sd_state_copy(sd_state* dst, const sd_state* src) {
+    return guard([&] {
+        sdb::StateImpl& d = st(dst);
+        require(src != nullptr, "null state");
+        const sdb::StateImpl& s = src->impl;
+        require(d.n == s.n && d.n_local == s.n_local, "state shapes differ");
+        SDB_CUDA(cudaSetDevice(d.device));
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+        SDB_CUDA(cudaMemcpyAsync(d.amps, s.amps, d.amps_count() * 16, cudaMemcpyDeviceToDevice, d.stream));
+        SDB_CUDA(cudaStreamSynchronize(d.stream));
+        d.phys_of = s.phys_of;
+    });
+}
+
+sd_status sd_kernel_stats_get(const sd_state* h, sd_kernel_stats* out) {
+    return guard([&] {
+        require(h != nullptr && out != nullptr, "null argument");
+        *out = h->impl.stats;
+    });
+}
+
+sd_status sd_kernel_stats_reset(sd_state* h) {
+    return guard([&] { st(h).stats = sd_kernel_stats{0, 0, 0}; });
+}
+
+sd_status sd_apply_hadamard(sd_state* h, int t) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require_unsharded(s);
+        require_identity_layout(s);
+        SDB_CUDA(cudaSetDevice(s.device));
+        hadamard(s, t);
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
+sd_status sd_apply_batched_cnot(sd_state* h, int c, uint64_t targets) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require_unsharded(s);
+        require_identity_layout(s);
+        SDB_CUDA(cudaSetDevice(s.device));
+        batched_cnot(s, c, targets);
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
+sd_status sd_apply_phase_layer(sd_state* h, uint64_t s_mask, const int32_t* pairs, size_t n_pairs, int dagger) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require_unsharded(s);
+        require_identity_layout(s);
+        SDB_CUDA(cudaSetDevice(s.device));
+        phase_layer(s, s_mask, pairs, n_pairs, dagger != 0);
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
+sd_status sd_apply_diagonal_exp(sd_state* h, const uint64_t* masks, const double* coeffs, size_t m, double dt) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require_unsharded(s);
+        require_identity_layout(s);
+        SDB_CUDA(cudaSetDevice(s.device));
+        diag_exp(s, masks, coeffs, m, dt);
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
+sd_status sd_apply_clifford(sd_state* h, const sd_group_desc* g) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require(g != nullptr, "null group");
+        require_unsharded(s);
+        require_identity_layout(s);
+        SDB_CUDA(cudaSetDevice(s.device));
+        clifford_unfused(s, spec_of(*g), false);
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
+sd_status sd_apply_clifford_inverse(sd_state* h, const sd_group_desc* g) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require(g != nullptr, "null group");
+        require_unsharded(s);
+        require_identity_layout(s);
+        SDB_CUDA(cudaSetDevice(s.device));
+        clifford_unfused(s, spec_of(*g), true);
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
+sd_status sd_plan_options_default(sd_plan_options* o) {
+    return guard([&] {
+        require(o != nullptr, "null options");
+        std::memset(o, 0, sizeof(*o));
+        o->order = 1;
+        o->tile_qubits = 0;
+        o->fuse = 1;
+        o->use_graph = 0;
+        o->relabel = 1;
+    });
+}
+
+sd_status sd_plan_create(sd_state* h, const sd_group_desc* groups, size_t n_groups, const sd_plan_options* opts,
+                         sd_plan** out) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require(out != nullptr, "out is null");
+        require(n_groups == 0 || groups != nullptr, "null group array");
+        auto p = std::make_unique<sd_plan>();
+        p->state = h;
+        if (opts) p->opts = *opts;
+        else sd_plan_options_default(&p->opts);
+        for (size_t i = 0; i < n_groups; ++i) {
+            sdb::GroupSpec g = spec_of(groups[i]);
+            auto chk = [&](int q) { check_qubit(s, q); };
+            for (int q : g.h_pre) chk(q);
+            for (int q : g.h_post) chk(q);
+            for (int q : g.s_layer) chk(q);
+            for (auto [a, b] : g.cnots) { chk(a); chk(b); }
+            for (auto [a, b] : g.czs) { chk(a); chk(b); }
+            for (uint64_t m : g.z_masks) {
+                if (s.n < 64 && (m >> s.n)) throw std::invalid_argument("diagonal exp: mask exceeds register");
+            }
+            p->groups.push_back(std::move(g));
+        }
+        if (!p->opts.fuse) require_unsharded(s);
+        plan_build(*p);
+        *out = p.release();
+    });
+}
+
+void sd_plan_destroy(sd_plan* p) {
+    if (!p) return;
+    cudaSetDevice(p->state->impl.device);
+    for (auto& e : p->ev_pool) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+    if (p->graph) cudaGraphExecDestroy(p->graph);
+    if (p->dev_block) cudaFree(p->dev_block);
+    delete p;
+}
+
+sd_status sd_plan_get_info(const sd_plan* p, sd_plan_info* o) {
+    return guard([&] {
+        require(p != nullptr && o != nullptr, "null argument");
+        const sdb::StateImpl& s = p->state->impl;
+        std::memset(o, 0, sizeof(*o));
+        o->n_ref_sweeps_per_step = p->n_ref_sweeps;
+        o->n_group_applications = static_cast<int>(p->opts.order == 2 && p->groups.size() > 1
+                                                        ? 2 * p->groups.size() - 1
+                                                        : p->groups.size());
+        if (p->opts.fuse) {
+            o->n_passes_per_step = static_cast<int>(p->host_passes.size());
+            o->tile_qubits = p->step.tile_qubits;
+            o->n_kernels_per_step = o->n_passes_per_step;
+            o->bytes_per_step = 2.0 * 16.0 * double(s.amps_count()) * o->n_passes_per_step;
+        } else {
+            o->n_passes_per_step = p->n_ref_sweeps;
+            o->n_kernels_per_step = 0;
+            o->bytes_per_step = 2.0 * 16.0 * double(s.amps_count()) * p->n_ref_sweeps;
+        }
+        o->n_exchanges_per_step = 0;
+    });
+}
+
+sd_status sd_plan_describe(const sd_plan* p, char* buf, size_t cap, size_t* len) {
+    return guard([&] {
+        require(p != nullptr, "null plan");
+        sdb::write_text_out(p->opts.fuse ? sdb::describe(p->step) : std::string("unfused reference schedule\n"),
+                            buf, cap, len);
+    });
+}
+
+sd_status sd_evolve(sd_plan* p, double dt, int n_steps) {
+    return guard([&] {
+        require(p != nullptr, "null plan");
+        evolve(*p, dt, n_steps, true);
+    });
+}
+
+sd_status sd_evolve_async(sd_plan* p, double dt, int n_steps) {
+    return guard([&] {
+        require(p != nullptr, "null plan");
+        evolve(*p, dt, n_steps, false);
+    });
+}
+
+sd_status sd_plan_set_profiling(sd_plan* p, int enable) {
+    return guard([&] {
+        require(p != nullptr, "null plan");
+        harvest(*p);
+        p->profiling = enable != 0;
+        for (int c = 0; c < 4; ++c) {
+            p->ms[c] = 0.0;
+            p->launches[c] = 0;
+            p->bytes[c] = 0.0;
+        }
+    });
+}
+
+sd_status sd_plan_kernel_times(sd_plan* p, double* ms, uint64_t* launches, double* bytes, int n_classes) {
+    return guard([&] {
+        require(p != nullptr, "null plan");
+        harvest(*p);
+        for (int c = 0; c < n_classes && c < 4; ++c) {
+            if (ms) ms[c] = p->ms[c];
+            if (launches) launches[c] = p->launches[c];
+            if (bytes) bytes[c] = p->bytes[c];
+        }
+    });
+}
+
+sd_status sd_comm_unique_id(unsigned char id[128]) {
+    return guard([&] {
+        (void)id;
+        throw std::runtime_error("NCCL exchange not built in this version");
+    });
+}
+
+sd_status sd_state_attach_comm(sd_state* h, const unsigned char id[128]) {
+    return guard([&] {
+        (void)h;
+        (void)id;
+        throw std::runtime_error("NCCL exchange not built in this version");
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,325 @@
+// Single-sweep state kernels for sm_100a: initialisation, reductions and the
+// reference's unfused gate sweeps (the StateVector methods of reference
+// proj/src/statevector.cpp). These back the sd_apply_* entry points and the
+// `fuse = 0` schedule; the Trotter hot path uses pass_kernel.cu.
+//
+// Memory layout: 2^n_local interleaved (re, im) doubles = double2 per
+// amplitude; every kernel is a grid-stride stream over amplitudes or
+// amplitude pairs with 16-byte vector loads.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <vector>
+
+#include "../internal.hpp"
+
+namespace sdb {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned grid_for(uint64_t work) {
+    uint64_t blocks = (work + kThreads - 1) / kThreads;
+    const uint64_t cap = 148ull * 16;  // 16 resident waves of 256-thread CTAs
+    if (blocks > cap) blocks = cap;
+    if (blocks == 0) blocks = 1;
+    return static_cast<unsigned>(blocks);
+}
+
+__device__ __forceinline__ uint64_t insert_zero(uint64_t v, int p) {
+    const uint64_t low = (1ull << p) - 1ull;
+    return ((v & ~low) << 1) | (v & low);
+}
+
+// --- counter RNG, identical integer stream to reference rng.hpp:15-49
+__device__ __forceinline__ uint64_t mix64(uint64_t v) {
+    v += 0x9e3779b97f4a7c15ull;
+    v = (v ^ (v >> 30)) * 0xbf58476d1ce4e5b9ull;
+    v = (v ^ (v >> 27)) * 0x94d049bb133111ebull;
+    return v ^ (v >> 31);
+}
+__device__ __forceinline__ uint64_t key_hash(uint64_t seed, uint64_t tag, uint64_t a, uint64_t b) {
+    uint64_t h = mix64(seed ^ 0x243f6a8885a308d3ull);
+    h = mix64(h ^ tag);
+    h = mix64(h ^ a);
+    h = mix64(h ^ b);
+    h = mix64(h ^ 0ull);
+    h = mix64(h ^ 0ull);
+    return h;
+}
+__device__ __forceinline__ double unit53(uint64_t w) { return double(w >> 11) * 0x1.0p-53; }
+__device__ __forceinline__ double normal_draw(uint64_t w) {
+    const double u1 = unit53(mix64(w ^ 0x5bf0a8dcull));
+    const double u2 = unit53(mix64(w ^ 0x94d0ca12ull));
+    // Same argument rounding as the reference (2*pi*u2 in double).
+    return sqrt(-2.0 * log1p(-u1)) * cos(2.0 * 3.141592653589793 * u2);
+}
+
+__global__ void k_fill(double2* __restrict__ a, uint64_t n, double re, double im) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        a[i] = make_double2(re, im);
+}
+
+__global__ void k_set_one(double2* a, uint64_t idx) { a[idx] = make_double2(1.0, 0.0); }
+
+__global__ void k_random(double2* __restrict__ a, uint64_t n, uint64_t seed, uint64_t first) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t g = first + i;
+        a[i] = make_double2(normal_draw(key_hash(seed, 0x57a7eull, g, 0)),
+                            normal_draw(key_hash(seed, 0x57a7eull, g, 1)));
+    }
+}
+
+__global__ void k_scale(double2* __restrict__ a, uint64_t n, double f) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        double2 v = a[i];
+        a[i] = make_double2(v.x * f, v.y * f);
+    }
+}
+
+// Deterministic two-level reduction: block b sums a fixed strided subset in
+// a fixed order, then a tree inside the block; the host-side second level
+// adds the block partials in index order.
+template <bool kInner>
+__global__ void k_reduce(const double2* __restrict__ a, const double2* __restrict__ b, uint64_t n,
+                         double2* __restrict__ partial) {
+    __shared__ double2 red[kThreads];
+    double sr = 0.0, si = 0.0;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const double2 x = a[i];
+        if (kInner) {
+            const double2 y = b[i];
+            sr += x.x * y.x + x.y * y.y;  // conj(x) * y
+            si += x.x * y.y - x.y * y.x;
+        } else {
+            sr += x.x * x.x + x.y * x.y;
+        }
+    }
+    red[threadIdx.x] = make_double2(sr, si);
+    __syncthreads();
+    for (int w = kThreads / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            red[threadIdx.x].x += red[threadIdx.x + w].x;
+            red[threadIdx.x].y += red[threadIdx.x + w].y;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+// apply_hadamard (reference statevector.cpp:156-174): one sweep over pairs,
+// scaled by fl(1/sqrt2) per gate exactly as the reference does.
+__global__ void k_hadamard(double2* __restrict__ a, uint64_t pairs, int t) {
+    const double c = 0.7071067811865475244;
+    const uint64_t tb = 1ull << t;
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < pairs;
+         p += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i0 = insert_zero(p, t), i1 = i0 | tb;
+        const double2 x = a[i0], y = a[i1];
+        a[i0] = make_double2((x.x + y.x) * c, (x.y + y.y) * c);
+        a[i1] = make_double2((x.x - y.x) * c, (x.y - y.y) * c);
+    }
+}
+
+// apply_batched_cnot (statevector.cpp:176-203): swap amp[i] <-> amp[i^T] for
+// the representative with control 1 and lowest target 0.
+__global__ void k_batched_cnot(double2* __restrict__ a, uint64_t quads, int lo, int hi,
+                               uint64_t cbit, uint64_t targets) {
+    for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < quads;
+         q += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = insert_zero(insert_zero(q, lo), hi) | cbit;
+        const uint64_t j = i ^ targets;
+        const double2 x = a[i];
+        a[i] = a[j];
+        a[j] = x;
+    }
+}
+
+// apply_phase_layer (statevector.cpp:205-245): multiply by i^quarter, exact.
+__global__ void k_phase_layer(double2* __restrict__ a, uint64_t n, uint64_t s_mask,
+                              const uint64_t* __restrict__ pairs, int n_pairs, int dagger) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        unsigned q = __popcll(i & s_mask) & 3u;
+        if (dagger) q = (4u - q) & 3u;
+        unsigned cz = 0;
+        for (int k = 0; k < n_pairs; ++k) {
+            const uint64_t pm = __ldg(pairs + k);
+            cz ^= ((i & pm) == pm) ? 1u : 0u;
+        }
+        q = (q + 2u * cz) & 3u;
+        if (q == 0) continue;
+        const double2 v = a[i];
+        a[i] = q == 1 ? make_double2(-v.y, v.x) : q == 2 ? make_double2(-v.x, -v.y)
+                                                         : make_double2(v.y, -v.x);
+    }
+}
+
+// apply_diagonal_exp (statevector.cpp:247-286): angle summed in term order
+// with the sign-bit flip, phi = -dt*angle, multiply by (cos phi, sin phi).
+__global__ void k_diag_exp(double2* __restrict__ a, uint64_t n, const uint64_t* __restrict__ zm,
+                           const double* __restrict__ cf, int m, double dt) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        double ang = 0.0;
+        for (int k = 0; k < m; ++k) {
+            const uint64_t par = __popcll(i & __ldg(zm + k)) & 1ull;
+            ang += __longlong_as_double(__double_as_longlong(__ldg(cf + k)) ^ (long long)(par << 63));
+        }
+        double sn, cs;
+        sincos(-dt * ang, &sn, &cs);
+        const double2 v = a[i];
+        a[i] = make_double2(v.x * cs - v.y * sn, v.x * sn + v.y * cs);
+    }
+}
+
+// Physical bit permutation dst[pi(i)] = src[i] with bit j of i moved to
+// bit new_pos[j] (used to restore logical order on download).
+__global__ void k_permute_bits(const double2* __restrict__ src, double2* __restrict__ dst,
+                               uint64_t n, const int* __restrict__ new_pos, int n_bits) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t j = 0;
+        for (int b = 0; b < n_bits; ++b) j |= ((i >> b) & 1ull) << __ldg(new_pos + b);
+        dst[j] = src[i];
+    }
+}
+
+double2* d2(StateImpl& s) { return reinterpret_cast<double2*>(s.amps); }
+
+template <typename T>
+T* upload_scratch(const std::vector<T>& v, cudaStream_t st) {
+    T* d = nullptr;
+    if (v.empty()) return nullptr;
+    SDB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), v.size() * sizeof(T), st));
+    SDB_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    return d;
+}
+
+}  // namespace
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        throw OomError(std::string("CUDA out of memory: ") + what);
+    }
+    throw CudaError(std::string(cudaGetErrorString(e)) + " at " + what);
+}
+
+void launch_fill(StateImpl& s, double re, double im) {
+    const uint64_t n = s.amps_count();
+    k_fill<<<grid_for(n), kThreads, 0, s.stream>>>(d2(s), n, re, im);
+    SDB_CUDA(cudaGetLastError());
+}
+
+void launch_set_basis(StateImpl& s, uint64_t local_index) {
+    launch_fill(s, 0.0, 0.0);
+    if (local_index < s.amps_count()) {
+        k_set_one<<<1, 1, 0, s.stream>>>(d2(s), local_index);
+        SDB_CUDA(cudaGetLastError());
+    }
+}
+
+void launch_random(StateImpl& s, uint64_t seed) {
+    const uint64_t n = s.amps_count();
+    k_random<<<grid_for(n), kThreads, 0, s.stream>>>(d2(s), n, seed, uint64_t(s.rank) << s.n_local);
+    SDB_CUDA(cudaGetLastError());
+}
+
+void launch_scale(StateImpl& s, double f) {
+    const uint64_t n = s.amps_count();
+    k_scale<<<grid_for(n), kThreads, 0, s.stream>>>(d2(s), n, f);
+    SDB_CUDA(cudaGetLastError());
+}
+
+static void reduce_impl(StateImpl& a, StateImpl* b, double* re, double* im) {
+    const uint64_t n = a.amps_count();
+    const unsigned blocks = grid_for(n);
+    if (!a.reduce_buf) SDB_CUDA(cudaMalloc(reinterpret_cast<void**>(&a.reduce_buf), 148 * 16 * sizeof(double2)));
+    double2* part = reinterpret_cast<double2*>(a.reduce_buf);
+    if (b)
+        k_reduce<true><<<blocks, kThreads, 0, a.stream>>>(d2(a), d2(*b), n, part);
+    else
+        k_reduce<false><<<blocks, kThreads, 0, a.stream>>>(d2(a), nullptr, n, part);
+    SDB_CUDA(cudaGetLastError());
+    std::vector<double2> h(blocks);
+    SDB_CUDA(cudaMemcpyAsync(h.data(), part, blocks * sizeof(double2), cudaMemcpyDeviceToHost, a.stream));
+    SDB_CUDA(cudaStreamSynchronize(a.stream));
+    // Pairwise sum of the block partials (fixed order).
+    while (h.size() > 1) {
+        std::vector<double2> nx((h.size() + 1) / 2);
+        for (size_t i = 0; i < nx.size(); ++i) {
+            nx[i] = h[2 * i];
+            if (2 * i + 1 < h.size()) {
+                nx[i].x += h[2 * i + 1].x;
+                nx[i].y += h[2 * i + 1].y;
+            }
+        }
+        h.swap(nx);
+    }
+    *re = h[0].x;
+    if (im) *im = h[0].y;
+}
+
+double device_norm_sq(StateImpl& s) {
+    double r = 0.0;
+    reduce_impl(s, nullptr, &r, nullptr);
+    return r;
+}
+
+void device_inner(StateImpl& a, StateImpl& b, double* re, double* im) { reduce_impl(a, &b, re, im); }
+
+void launch_hadamard(StateImpl& s, int t) {
+    const uint64_t pairs = s.amps_count() >> 1;
+    k_hadamard<<<grid_for(pairs), kThreads, 0, s.stream>>>(d2(s), pairs, t);
+    SDB_CUDA(cudaGetLastError());
+}
+
+void launch_batched_cnot(StateImpl& s, int control, uint64_t targets) {
+    const int t0 = __builtin_ctzll(targets);
+    const int lo = control < t0 ? control : t0, hi = control < t0 ? t0 : control;
+    const uint64_t quads = s.amps_count() >> 2;
+    k_batched_cnot<<<grid_for(quads), kThreads, 0, s.stream>>>(d2(s), quads, lo, hi, 1ull << control,
+                                                              targets);
+    SDB_CUDA(cudaGetLastError());
+}
+
+void launch_phase_layer(StateImpl& s, uint64_t s_mask, const std::vector<uint64_t>& pair_masks,
+                        bool dagger) {
+    uint64_t* dp = upload_scratch(pair_masks, s.stream);
+    const uint64_t n = s.amps_count();
+    k_phase_layer<<<grid_for(n), kThreads, 0, s.stream>>>(d2(s), n, s_mask, dp,
+                                                         static_cast<int>(pair_masks.size()), dagger ? 1 : 0);
+    SDB_CUDA(cudaGetLastError());
+    if (dp) SDB_CUDA(cudaFreeAsync(dp, s.stream));
+}
+
+void launch_diag_exp(StateImpl& s, const std::vector<uint64_t>& masks,
+                     const std::vector<double>& coeffs, double dt) {
+    uint64_t* dm = upload_scratch(masks, s.stream);
+    double* dc = upload_scratch(coeffs, s.stream);
+    const uint64_t n = s.amps_count();
+    k_diag_exp<<<grid_for(n), kThreads, 0, s.stream>>>(d2(s), n, dm, dc, static_cast<int>(masks.size()), dt);
+    SDB_CUDA(cudaGetLastError());
+    if (dm) SDB_CUDA(cudaFreeAsync(dm, s.stream));
+    if (dc) SDB_CUDA(cudaFreeAsync(dc, s.stream));
+}
+
+void launch_permute_bits(StateImpl& s, const double* src, double* dst, const int* new_pos_host,
+                         int n_bits) {
+    std::vector<int> pos(new_pos_host, new_pos_host + n_bits);
+    int* dpos = upload_scratch(pos, s.stream);
+    const uint64_t n = uint64_t(1) << n_bits;
+    k_permute_bits<<<grid_for(n), kThreads, 0, s.stream>>>(reinterpret_cast<const double2*>(src),
+                                                          reinterpret_cast<double2*>(dst), n, dpos, n_bits);
+    SDB_CUDA(cudaGetLastError());
+    SDB_CUDA(cudaFreeAsync(dpos, s.stream));
+}
+
+}  // namespace sdb

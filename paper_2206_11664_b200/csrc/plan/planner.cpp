@@ -1,0 +1,338 @@
+// Pass planner (host). See planner.hpp and DESIGN.md §3.
+//
+// The reference applies every layer of every C_j / C_j^dagger as its own
+// full-state sweep (proj/src/statevector.cpp:339-381, one sweep per H gate).
+// Here a step's gates are list-scheduled into tile passes: a pass may run
+// any ops whose "need" qubits (H targets, CNOT targets) lie in its <= k
+// local qubits, in any order consistent with the gates' commutation
+// relations; diagonal ops (phase layers, exp(-i dt Lambda)) need nothing and
+// ride along for free.
+#include "planner.hpp"
+
+#include <algorithm>
+#include <bit>
+#include <sstream>
+#include <stdexcept>
+
+namespace sdb {
+
+namespace {
+
+inline uint64_t bitq(int q) { return 1ull << q; }
+
+bool is_diag(const Op& o) { return o.kind == Op::PH || o.kind == Op::DG; }
+
+bool commute(const Op& a, const Op& b) {
+    if (is_diag(a) && is_diag(b)) return true;
+    if (a.kind == Op::H && b.kind == Op::H) return a.q != b.q;
+    if (a.kind == Op::H) return (bitq(a.q) & b.support) == 0;
+    if (b.kind == Op::H) return (bitq(b.q) & a.support) == 0;
+    if (a.kind == Op::CX && b.kind == Op::CX) {
+        return (bitq(a.q) & b.targets) == 0 && (bitq(b.q) & a.targets) == 0;
+    }
+    const Op& cx = a.kind == Op::CX ? a : b;
+    const Op& dg = a.kind == Op::CX ? b : a;
+    return (cx.targets & dg.support) == 0;
+}
+
+void emit_group(std::vector<Op>& out, const GroupSpec& g, int gi, double dt_scale) {
+    auto h = [&](int q) {
+        Op o;
+        o.kind = Op::H;
+        o.q = q;
+        o.support = o.need = bitq(q);
+        out.push_back(std::move(o));
+    };
+    // CNOT runs with one control, in application order (statevector.cpp:341-349).
+    std::vector<std::pair<int, uint64_t>> runs;
+    for (size_t k = 0; k < g.cnots.size();) {
+        const int c = g.cnots[k].first;
+        uint64_t t = 0;
+        while (k < g.cnots.size() && g.cnots[k].first == c) t |= bitq(g.cnots[k++].second);
+        runs.emplace_back(c, t);
+    }
+    auto cx = [&](int c, uint64_t t) {
+        Op o;
+        o.kind = Op::CX;
+        o.q = c;
+        o.targets = t;
+        o.support = t | bitq(c);
+        o.need = t;
+        out.push_back(std::move(o));
+    };
+    const bool has_phase = !g.czs.empty() || !g.s_layer.empty();
+    auto ph = [&](bool dagger) {
+        Op o;
+        o.kind = Op::PH;
+        o.dagger = dagger;
+        for (int q : g.s_layer) o.s_mask |= bitq(q);
+        o.czs = g.czs;
+        o.support = o.s_mask;
+        for (auto [a, b] : g.czs) o.support |= bitq(a) | bitq(b);
+        out.push_back(std::move(o));
+    };
+    for (int q : g.h_pre) h(q);
+    for (auto [c, t] : runs) cx(c, t);
+    if (has_phase) ph(false);
+    for (int q : g.h_post) h(q);
+    {
+        Op o;
+        o.kind = Op::DG;
+        o.group = gi;
+        o.dt_scale = dt_scale;
+        for (uint64_t m : g.z_masks) o.support |= m;
+        out.push_back(std::move(o));
+    }
+    for (int q : g.h_post) h(q);
+    if (has_phase) ph(true);
+    for (auto it = runs.rbegin(); it != runs.rend(); ++it) cx(it->first, it->second);
+    for (int q : g.h_pre) h(q);
+}
+
+uint64_t to_phys(uint64_t logical, const std::vector<int>& phys_of) {
+    uint64_t p = 0;
+    while (logical) {
+        const int q = std::countr_zero(logical);
+        logical &= logical - 1;
+        p |= bitq(phys_of[q]);
+    }
+    return p;
+}
+
+}  // namespace
+
+std::vector<Op> step_ops(const std::vector<GroupSpec>& groups, int /*n_qubits*/, int order) {
+    std::vector<Op> ops;
+    const int G = static_cast<int>(groups.size());
+    if (order == 1 || G <= 1) {
+        for (int g = 0; g < G; ++g) emit_group(ops, groups[g], g, 1.0);
+    } else if (order == 2) {
+        // Symmetric Suzuki S2 with the middle group merged.
+        for (int g = 0; g < G - 1; ++g) emit_group(ops, groups[g], g, 0.5);
+        emit_group(ops, groups[G - 1], G - 1, 1.0);
+        for (int g = G - 2; g >= 0; --g) emit_group(ops, groups[g], g, 0.5);
+    } else {
+        throw std::invalid_argument("trotter order must be 1 or 2");
+    }
+    return ops;
+}
+
+double reference_sweeps(const std::vector<GroupSpec>& groups, int order) {
+    // KernelStats sweeps of one reference group application
+    // (statevector.cpp:156-286): H = 1, batched CNOT = 1/2, phase layer = 1,
+    // diagonal = 1.
+    double per_step = 0.0;
+    for (const GroupSpec& g : groups) {
+        int runs = 0;
+        for (size_t k = 0; k < g.cnots.size(); ++k) {
+            if (k == 0 || g.cnots[k].first != g.cnots[k - 1].first) ++runs;
+        }
+        const bool ph = !g.czs.empty() || !g.s_layer.empty();
+        per_step += 2.0 * (double(g.h_pre.size() + g.h_post.size()) + 0.5 * runs + (ph ? 1 : 0)) + 1.0;
+    }
+    return order == 2 ? 2.0 * per_step : per_step;
+}
+
+StepPlan plan_step(const std::vector<Op>& ops, const std::vector<GroupSpec>& groups, int n_local,
+                   int k, int n_fixed, const std::vector<int>& phys_of) {
+    if (k > n_local) k = n_local;
+    if (n_fixed > k) n_fixed = k;
+    StepPlan plan;
+    plan.tile_qubits = k;
+    const size_t N = ops.size();
+    const int n_logical = static_cast<int>(phys_of.size());
+
+    // logical qubits currently stored at physical positions 0..n_fixed-1
+    uint64_t fixed_logical = 0;
+    std::vector<int> logical_of(64, -1);
+    for (int q = 0; q < n_logical; ++q) logical_of[phys_of[q]] = q;
+    for (int p = 0; p < n_fixed; ++p) {
+        if (logical_of[p] >= 0) fixed_logical |= bitq(logical_of[p]);
+    }
+    // Qubits stored on other ranks (physical >= n_local) can never be local.
+    uint64_t global_logical = 0;
+    for (int q = 0; q < n_logical; ++q) {
+        if (phys_of[q] >= n_local) global_logical |= bitq(q);
+    }
+    for (const Op& o : ops) {
+        if (o.need & global_logical) {
+            throw std::logic_error("plan_step: op needs a rank-global qubit (remap required)");
+        }
+    }
+
+    // --- list scheduling with a sliding window and blocker counts
+    constexpr size_t W = 768;
+    std::vector<char> done(N, 0);
+    std::vector<int> blockers(N, 0);
+    size_t first = 0, hi = 0;
+    auto extend = [&]() {
+        const size_t want = std::min(N, first + W);
+        for (; hi < want; ++hi) {
+            int b = 0;
+            for (size_t i = first; i < hi; ++i) {
+                if (!done[i] && !commute(ops[i], ops[hi])) ++b;
+            }
+            blockers[hi] = b;
+        }
+    };
+    std::vector<std::vector<int>> pass_ops;
+    std::vector<uint64_t> pass_local;
+    while (first < N) {
+        uint64_t L = fixed_logical;
+        std::vector<int> sched;
+        extend();
+        for (;;) {
+            long pick = -1;
+            for (size_t j = first; j < hi; ++j) {
+                if (!done[j] && blockers[j] == 0 && (ops[j].need & ~L) == 0) {
+                    pick = static_cast<long>(j);
+                    break;
+                }
+            }
+            if (pick < 0) {
+                for (size_t j = first; j < hi; ++j) {
+                    if (!done[j] && blockers[j] == 0 && std::popcount(L | ops[j].need) <= k) {
+                        pick = static_cast<long>(j);
+                        break;
+                    }
+                }
+                if (pick < 0) break;
+                L |= ops[pick].need;
+            }
+            done[pick] = 1;
+            sched.push_back(static_cast<int>(pick));
+            for (size_t j = pick + 1; j < hi; ++j) {
+                if (!done[j] && !commute(ops[pick], ops[j])) --blockers[j];
+            }
+            while (first < N && done[first]) ++first;
+            extend();
+        }
+        if (sched.empty()) throw std::logic_error("plan_step: no schedulable op (tile too small?)");
+        pass_ops.push_back(std::move(sched));
+        pass_local.push_back(L);
+    }
+
+    // --- lower each pass to physical stages
+    int cum = 0;
+    for (size_t p = 0; p < pass_ops.size(); ++p) {
+        PassPlan pp;
+        uint64_t Lphys = to_phys(pass_local[p], phys_of);
+        // pad with the lowest free physical bits (keeps accesses contiguous)
+        for (int b = 0; b < n_local && std::popcount(Lphys) < k; ++b) Lphys |= bitq(b);
+        for (int b = 0; b < n_local; ++b) {
+            if (Lphys & bitq(b)) pp.lpos.push_back(b);
+        }
+        std::vector<int> coord(64, -1);
+        for (size_t j = 0; j < pp.lpos.size(); ++j) coord[pp.lpos[j]] = static_cast<int>(j);
+        auto local_mask = [&](uint64_t logical) {
+            uint32_t m = 0;
+            while (logical) {
+                const int q = std::countr_zero(logical);
+                logical &= logical - 1;
+                const int c = coord[phys_of[q]];
+                if (c < 0) throw std::logic_error("plan_step: needed qubit not local");
+                m |= 1u << c;
+            }
+            return m;
+        };
+        std::vector<int> s_count(64, 0);
+        auto flush_point = [&]() {
+            if (pp.stages.empty() || pp.stages.back().kind != PassStage::POINT) return;
+            PointSpec& ps = pp.points[pp.stages.back().point];
+            for (int b = 0; b < 64; ++b) {
+                const int c = s_count[b] & 3;
+                if (c & 1) ps.s1 |= bitq(b);
+                if (c & 2) ps.s2 |= bitq(b);
+                s_count[b] = 0;
+            }
+        };
+        for (int id : pass_ops[p]) {
+            const Op& o = ops[id];
+            pp.op_ids.push_back(id);
+            if (o.kind == Op::H) {
+                flush_point();
+                const uint32_t m = local_mask(bitq(o.q));
+                if (!pp.stages.empty() && pp.stages.back().kind == PassStage::WHT) {
+                    pp.stages.back().mask ^= m;
+                } else {
+                    PassStage st{PassStage::WHT};
+                    st.mask = m;
+                    pp.stages.push_back(st);
+                }
+            } else if (o.kind == Op::CX) {
+                flush_point();
+                PassStage st{PassStage::CX};
+                st.mask = local_mask(o.targets);
+                const int pc = phys_of[o.q];
+                if (coord[pc] >= 0) st.ctrl_local = coord[pc];
+                else st.ctrl_phys = pc;
+                pp.stages.push_back(st);
+            } else {
+                if (pp.stages.empty() || pp.stages.back().kind != PassStage::POINT) {
+                    PassStage st{PassStage::POINT};
+                    st.point = static_cast<int>(pp.points.size());
+                    pp.points.emplace_back();
+                    pp.stages.push_back(st);
+                }
+                PointSpec& ps = pp.points[pp.stages.back().point];
+                if (o.kind == Op::PH) {
+                    uint64_t s = o.s_mask;
+                    while (s) {
+                        const int q = std::countr_zero(s);
+                        s &= s - 1;
+                        s_count[phys_of[q]] += o.dagger ? 3 : 1;
+                    }
+                    for (auto [a, b] : o.czs) ps.cz_masks.push_back(bitq(phys_of[a]) | bitq(phys_of[b]));
+                } else {
+                    const GroupSpec& g = groups[o.group];
+                    for (size_t t = 0; t < g.z_masks.size(); ++t) {
+                        ps.terms.push_back({to_phys(g.z_masks[t], phys_of), g.coeffs[t], o.dt_scale});
+                    }
+                }
+            }
+        }
+        flush_point();
+        // drop WHT stages that cancelled to nothing
+        std::vector<PassStage> kept;
+        for (const PassStage& st : pp.stages) {
+            if (st.kind == PassStage::WHT && st.mask == 0) continue;
+            kept.push_back(st);
+        }
+        pp.stages = std::move(kept);
+        int levels = 0;
+        for (const PassStage& st : pp.stages) {
+            if (st.kind == PassStage::WHT) levels += std::popcount(st.mask);
+        }
+        pp.butterflies = levels;
+        pp.scale_exp = (cum + levels) / 2 - cum / 2;
+        cum += levels;
+        plan.passes.push_back(std::move(pp));
+    }
+    if (cum & 1) throw std::logic_error("plan_step: odd number of Hadamards in a step");
+    plan.ref_sweeps = 0.0;
+    return plan;
+}
+
+std::string describe(const StepPlan& p) {
+    std::ostringstream os;
+    os << "tile_qubits=" << p.tile_qubits << " passes=" << p.passes.size()
+       << " ref_sweeps=" << p.ref_sweeps << "\n";
+    for (size_t i = 0; i < p.passes.size(); ++i) {
+        const PassPlan& pp = p.passes[i];
+        os << "pass " << i << " local{";
+        for (size_t j = 0; j < pp.lpos.size(); ++j) os << (j ? "," : "") << pp.lpos[j];
+        os << "} ops=" << pp.op_ids.size() << " scale=2^-" << pp.scale_exp << " :";
+        for (const PassStage& st : pp.stages) {
+            if (st.kind == PassStage::WHT) os << " H[" << std::popcount(st.mask) << "]";
+            else if (st.kind == PassStage::CX) os << " CX";
+            else {
+                const PointSpec& ps = pp.points[st.point];
+                os << " P[cz" << ps.cz_masks.size() << ",t" << ps.terms.size() << "]";
+            }
+        }
+        os << "\n";
+    }
+    return os.str();
+}
+
+}  // namespace sdb

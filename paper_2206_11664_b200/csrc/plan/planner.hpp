@@ -1,0 +1,85 @@
+// Pass planner: turns one Trotter step (a sequence of C_j, D_j, C_j^dagger
+// sandwiches, reference proj/src/evolve.cpp:47-58) into a short list of
+// shared-memory tile passes over the state.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace sdb {
+
+// One group as the planner sees it (a flattened DiagonalGroup).
+struct GroupSpec {
+    std::vector<int> h_pre, s_layer, h_post;
+    std::vector<std::pair<int, int>> cnots, czs;
+    std::vector<uint64_t> z_masks;
+    std::vector<double> coeffs;
+};
+
+// Gate-level operation in logical qubits.
+struct Op {
+    enum Kind { H, CX, PH, DG } kind = H;
+    int q = -1;              // H target, CX control
+    uint64_t targets = 0;    // CX target mask
+    uint64_t s_mask = 0;     // PH
+    bool dagger = false;     // PH
+    std::vector<std::pair<int, int>> czs;  // PH
+    int group = -1;          // DG: index into groups
+    double dt_scale = 1.0;   // DG: multiplier of dt
+    uint64_t support = 0;    // qubits acted on (commutation checks)
+    uint64_t need = 0;       // qubits that must be tile-local
+};
+
+// Builds the op sequence of one Trotter step (order 1 or 2).
+std::vector<Op> step_ops(const std::vector<GroupSpec>& groups, int n_qubits, int order);
+
+// A pass in physical bit positions.
+struct PassStage {
+    enum Kind { WHT, CX, POINT } kind;
+    uint32_t mask = 0;       // WHT local mask / CX local target mask
+    int ctrl_local = -1;     // CX
+    int ctrl_phys = -1;      // CX (outer control)
+    int point = -1;          // POINT: index into PassPlan::points
+};
+
+struct PointTerm {
+    uint64_t mask;   // physical
+    double coeff;    // signed coefficient c
+    double dt_scale; // weight = -dt * dt_scale * coeff
+};
+
+struct PointSpec {
+    uint64_t s1 = 0, s2 = 0;  // physical: quarter += popc(i&s1) + 2 popc(i&s2)
+    std::vector<uint64_t> cz_masks;        // physical, 2 bits each (one per pair)
+    std::vector<PointTerm> terms;
+};
+
+struct PassPlan {
+    std::vector<int> lpos;      // physical positions of local coordinates (ascending)
+    std::vector<PassStage> stages;
+    std::vector<PointSpec> points;
+    int butterflies = 0;        // WHT levels applied in this pass
+    int scale_exp = 0;          // store scale = 2^-scale_exp
+    std::vector<int> op_ids;    // ops scheduled here (debug)
+};
+
+struct StepPlan {
+    std::vector<PassPlan> passes;
+    int tile_qubits = 0;
+    double ref_sweeps = 0.0;     // reference KernelStats sweeps per step
+    int group_applications = 0;
+};
+
+// Greedy list scheduling of `ops` into tile passes of <= k local qubits, of
+// which the lowest `n_fixed` physical bits are always local (coalescing).
+// phys_of maps logical qubit -> physical bit (identity for one device).
+StepPlan plan_step(const std::vector<Op>& ops, const std::vector<GroupSpec>& groups, int n_local,
+                   int k, int n_fixed, const std::vector<int>& phys_of);
+
+double reference_sweeps(const std::vector<GroupSpec>& groups, int order);
+
+std::string describe(const StepPlan& p);
+
+}  // namespace sdb

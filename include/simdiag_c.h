@@ -207,6 +207,13 @@ sd_status sd_plan_get_info(const sd_plan* p, sd_plan_info* out);
  * sd_hamiltonian_save_text. */
 sd_status sd_plan_describe(const sd_plan* p, char* buf, size_t cap, size_t* len);
 
+/* Host-only: run the planner for a (sharded) state shape without touching a
+ * device; fills *info (may be NULL) and writes the schedule as JSON
+ * (passes -> local bit positions, stages, exact scale exponents). */
+sd_status sd_plan_preview(int n_qubits, int world, const sd_group_desc* groups, size_t n_groups,
+                          const sd_plan_options* opts, sd_plan_info* info, char* json, size_t cap,
+                          size_t* len);
+
 /* EvolutionPlan{total_time = dt*n_steps, n_steps} then evolve_grouped:
  * n_steps Trotter steps of size dt. n_steps == 0 is a no-op (evolve.cpp:13).
  * Blocks until complete. */

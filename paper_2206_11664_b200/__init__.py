@@ -24,6 +24,7 @@ from .simdiag import (  # noqa: F401
     greedy_partition,
     norm,
     partition_and_diagonalize,
+    plan_preview,
 )
 from . import models  # noqa: F401
 

@@ -130,6 +130,11 @@ sd_plan_create = _sig("sd_plan_create", [P, C.POINTER(GroupDesc), sz, C.POINTER(
 sd_plan_destroy = _sig("sd_plan_destroy", [P], None)
 sd_plan_get_info = _sig("sd_plan_get_info", [P, C.POINTER(PlanInfo)])
 sd_plan_describe = _sig("sd_plan_describe", [P, C.c_char_p, sz, C.POINTER(sz)])
+sd_plan_preview = _sig(
+    "sd_plan_preview",
+    [C.c_int, C.c_int, C.POINTER(GroupDesc), sz, C.POINTER(PlanOptions), C.POINTER(PlanInfo), C.c_char_p, sz,
+     C.POINTER(sz)],
+)
 sd_evolve = _sig("sd_evolve", [P, dbl, C.c_int])
 sd_evolve_async = _sig("sd_evolve_async", [P, dbl, C.c_int])
 sd_plan_set_profiling = _sig("sd_plan_set_profiling", [P, C.c_int])
@@ -152,7 +157,7 @@ EXPORTED = [
     "sd_apply_hadamard", "sd_apply_batched_cnot", "sd_apply_phase_layer", "sd_apply_diagonal_exp",
     "sd_apply_clifford", "sd_apply_clifford_inverse",
     "sd_plan_options_default", "sd_plan_create", "sd_plan_destroy", "sd_plan_get_info",
-    "sd_plan_describe", "sd_evolve", "sd_evolve_async", "sd_plan_set_profiling",
+    "sd_plan_describe", "sd_plan_preview", "sd_evolve", "sd_evolve_async", "sd_plan_set_profiling",
     "sd_plan_kernel_times", "sd_comm_unique_id", "sd_state_attach_comm",
 ]
 

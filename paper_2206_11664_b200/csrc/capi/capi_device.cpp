@@ -5,10 +5,12 @@
 #include <algorithm>
 #include <bit>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
 
+#include "../plan/lower.hpp"
 #include "../plan/planner.hpp"
 #include "guard.hpp"
 
@@ -39,6 +41,7 @@ struct sd_plan {
     cudaGraphExec_t graph = nullptr;
     double graph_dt = 0.0;
     int n_ref_sweeps = 0;
+    std::string program;
 };
 
 namespace {
@@ -161,127 +164,52 @@ constexpr int kTableThreshold = 8;  // terms per POINT stage above which the WHT
 
 void build_device_plan(sd_plan& p) {
     sdb::StateImpl& s = p.state->impl;
-    std::vector<sdb::PassDev> passes;
-    std::vector<sdb::StageDev> stages;
-    std::vector<sdb::PointDev> points;
-    std::vector<sdb::SegDev> segs;
-    std::vector<uint64_t> czm, tmask;
-    std::vector<double> tcoef;
-    p.pass_class.clear();
-    for (const sdb::PassPlan& pp : p.step.passes) {
-        sdb::PassDev pd{};
-        pd.k = static_cast<int>(pp.lpos.size());
-        uint64_t Lphys = 0;
-        for (size_t j = 0; j < pp.lpos.size(); ++j) {
-            pd.lpos[j] = pp.lpos[j];
-            Lphys |= 1ull << pp.lpos[j];
-        }
-        int no = 0;
-        for (int b = 0; b < s.n_local; ++b) {
-            if (!(Lphys & (1ull << b))) pd.opos[no++] = b;
-        }
-        pd.n_outer = no;
-        pd.stage_off = static_cast<int>(stages.size());
-        pd.n_stages = static_cast<int>(pp.stages.size());
-        pd.scale = std::ldexp(1.0, -pp.scale_exp);
-        pd.flags = 0;
-        bool only_point = true;
-        for (const sdb::PassStage& ps : pp.stages) {
-            sdb::StageDev sd{};
-            sd.kind = ps.kind == sdb::PassStage::WHT ? sdb::kStageWht
-                      : ps.kind == sdb::PassStage::CX ? sdb::kStageCx
-                                                      : sdb::kStagePoint;
-            sd.mask = ps.mask;
-            sd.ctrl_local = ps.ctrl_local;
-            sd.ctrl_phys = ps.ctrl_phys;
-            sd.point = -1;
-            if (ps.kind != sdb::PassStage::POINT) only_point = false;
-            if (ps.kind == sdb::PassStage::POINT) {
-                const sdb::PointSpec& spec = pp.points[ps.point];
-                sdb::PointDev pt{};
-                pt.s1 = spec.s1;
-                pt.s2 = spec.s2;
-                pt.cz_off = static_cast<int>(czm.size());
-                pt.n_cz = static_cast<int>(spec.cz_masks.size());
-                czm.insert(czm.end(), spec.cz_masks.begin(), spec.cz_masks.end());
-                pt.term_off = static_cast<int>(tmask.size());
-                pt.n_terms = static_cast<int>(spec.terms.size());
-                if (pt.n_terms > kTableThreshold) {
-                    // group terms by local part (stable: keeps term order inside a segment)
-                    struct T {
-                        uint32_t u;
-                        uint64_t zh;
-                        double c;
-                    };
-                    std::vector<T> ts;
-                    for (const sdb::PointTerm& t : spec.terms) {
-                        uint32_t u = 0;
-                        for (size_t j = 0; j < pp.lpos.size(); ++j) {
-                            if (t.mask & (1ull << pp.lpos[j])) u |= 1u << j;
-                        }
-                        ts.push_back({u, t.mask & ~Lphys, t.coeff * t.dt_scale});
-                    }
-                    std::stable_sort(ts.begin(), ts.end(), [](const T& a, const T& b) { return a.u < b.u; });
-                    pt.seg_off = static_cast<int>(segs.size());
-                    uint32_t tm = 0;
-                    for (size_t i = 0; i < ts.size();) {
-                        size_t j = i;
-                        while (j < ts.size() && ts[j].u == ts[i].u) ++j;
-                        segs.push_back({ts[i].u, static_cast<int>(i), static_cast<int>(j), 0});
-                        tm |= ts[i].u;
-                        i = j;
-                    }
-                    pt.n_seg = static_cast<int>(segs.size()) - pt.seg_off;
-                    pt.table_mask = tm;
-                    for (const T& t : ts) {
-                        tmask.push_back(t.zh);
-                        tcoef.push_back(t.c);
-                    }
-                    pd.flags |= sdb::kPassNeedsTable;
-                } else {
-                    for (const sdb::PointTerm& t : spec.terms) {
-                        tmask.push_back(t.mask);
-                        tcoef.push_back(t.coeff * t.dt_scale);
-                    }
-                }
-                sd.point = static_cast<int>(points.size());
-                points.push_back(pt);
-            }
-            stages.push_back(sd);
-        }
-        passes.push_back(pd);
-        p.pass_class.push_back(only_point ? 1 : 0);
-    }
-    // one device block, 16-byte aligned sub-arrays
+    int rbits = 4;
+    if (const char* e = std::getenv("SDB_RBITS")) rbits = std::atoi(e) == 3 ? 3 : 4;
+    sdb::HostPlanArrays A = sdb::lower_plan(p.step, s.n_local, kTableThreshold, rbits);
+    p.pass_class = A.pass_class;
+    p.program = sdb::describe_program(A);
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-    const size_t b_pass = al(passes.size() * sizeof(sdb::PassDev));
-    const size_t b_stage = al(std::max<size_t>(1, stages.size()) * sizeof(sdb::StageDev));
-    const size_t b_point = al(std::max<size_t>(1, points.size()) * sizeof(sdb::PointDev));
-    const size_t b_seg = al(std::max<size_t>(1, segs.size()) * sizeof(sdb::SegDev));
-    const size_t b_cz = al(std::max<size_t>(1, czm.size()) * 8);
-    const size_t b_tm = al(std::max<size_t>(1, tmask.size()) * 8);
-    const size_t b_tc = al(std::max<size_t>(1, tcoef.size()) * 8);
-    const size_t total = b_pass + b_stage + b_point + b_seg + b_cz + b_tm + b_tc;
+    const size_t sizes[] = {
+        al(std::max<size_t>(1, A.passes.size()) * sizeof(sdb::PassDev)),
+        al(std::max<size_t>(1, A.ops.size()) * sizeof(sdb::MicroOpDev)),
+        al(std::max<size_t>(1, A.perms.size()) * sizeof(sdb::PermDev)),
+        al(std::max<size_t>(1, A.points.size()) * sizeof(sdb::PointDev)),
+        al(std::max<size_t>(1, A.segs.size()) * sizeof(sdb::SegDev)),
+        al(std::max<size_t>(1, A.lo_pairs.size()) * sizeof(uint32_t)),
+        al(std::max<size_t>(1, A.oo_pairs.size()) * 8),
+        al(std::max<size_t>(1, A.qt_words.size()) * 8),
+        al(std::max<size_t>(1, A.cfg_tb.size()) * sizeof(sdb::CfgThreadDev)),
+        al(std::max<size_t>(1, A.term_masks.size()) * 8),
+        al(std::max<size_t>(1, A.term_coeffs.size()) * 8),
+    };
+    size_t total = 0;
+    for (size_t v : sizes) total += v;
     SDB_CUDA(cudaSetDevice(s.device));
     if (p.dev_block) SDB_CUDA(cudaFree(p.dev_block));
     SDB_CUDA(cudaMalloc(&p.dev_block, total));
     std::vector<unsigned char> host(total, 0);
     size_t off = 0;
-    auto put = [&](const void* src, size_t bytes, size_t span) {
+    int slot = 0;
+    auto put = [&](const void* src, size_t bytes) {
         if (bytes) std::memcpy(host.data() + off, src, bytes);
         void* dptr = static_cast<unsigned char*>(p.dev_block) + off;
-        off += span;
+        off += sizes[slot++];
         return dptr;
     };
-    p.dev.passes = static_cast<const sdb::PassDev*>(put(passes.data(), passes.size() * sizeof(sdb::PassDev), b_pass));
-    p.dev.stages = static_cast<const sdb::StageDev*>(put(stages.data(), stages.size() * sizeof(sdb::StageDev), b_stage));
-    p.dev.points = static_cast<const sdb::PointDev*>(put(points.data(), points.size() * sizeof(sdb::PointDev), b_point));
-    p.dev.segs = static_cast<const sdb::SegDev*>(put(segs.data(), segs.size() * sizeof(sdb::SegDev), b_seg));
-    p.dev.cz_masks = static_cast<const uint64_t*>(put(czm.data(), czm.size() * 8, b_cz));
-    p.dev.term_masks = static_cast<const uint64_t*>(put(tmask.data(), tmask.size() * 8, b_tm));
-    p.dev.term_coeffs = static_cast<const double*>(put(tcoef.data(), tcoef.size() * 8, b_tc));
+    p.dev.passes = static_cast<const sdb::PassDev*>(put(A.passes.data(), A.passes.size() * sizeof(sdb::PassDev)));
+    p.dev.ops = static_cast<const sdb::MicroOpDev*>(put(A.ops.data(), A.ops.size() * sizeof(sdb::MicroOpDev)));
+    p.dev.perms = static_cast<const sdb::PermDev*>(put(A.perms.data(), A.perms.size() * sizeof(sdb::PermDev)));
+    p.dev.points = static_cast<const sdb::PointDev*>(put(A.points.data(), A.points.size() * sizeof(sdb::PointDev)));
+    p.dev.segs = static_cast<const sdb::SegDev*>(put(A.segs.data(), A.segs.size() * sizeof(sdb::SegDev)));
+    p.dev.lo_pairs = static_cast<const uint32_t*>(put(A.lo_pairs.data(), A.lo_pairs.size() * sizeof(uint32_t)));
+    p.dev.oo_pairs = static_cast<const uint64_t*>(put(A.oo_pairs.data(), A.oo_pairs.size() * 8));
+    p.dev.qt_words = static_cast<const uint64_t*>(put(A.qt_words.data(), A.qt_words.size() * 8));
+    p.dev.cfg_tb = static_cast<const sdb::CfgThreadDev*>(put(A.cfg_tb.data(), A.cfg_tb.size() * sizeof(sdb::CfgThreadDev)));
+    p.dev.term_masks = static_cast<const uint64_t*>(put(A.term_masks.data(), A.term_masks.size() * 8));
+    p.dev.term_coeffs = static_cast<const double*>(put(A.term_coeffs.data(), A.term_coeffs.size() * 8));
     SDB_CUDA(cudaMemcpy(p.dev_block, host.data(), total, cudaMemcpyHostToDevice));
-    p.host_passes = std::move(passes);
+    p.host_passes = std::move(A.passes);
 }
 
 void plan_build(sd_plan& p) {
@@ -292,7 +220,7 @@ void plan_build(sd_plan& p) {
     if (!p.opts.fuse) return;
     int k = p.opts.tile_qubits > 0 ? p.opts.tile_qubits : 12;
     k = std::min({k, sdb::max_tile_qubits(), s.n_local});
-    const auto ops = sdb::step_ops(p.groups, s.n, order);
+    const auto ops = sdb::step_ops(p.groups, s.n, order, std::max(1, k - 3));
     p.step = sdb::plan_step(ops, p.groups, s.n_local, k, 3, s.phys_of);
     p.step.ref_sweeps = sdb::reference_sweeps(p.groups, order);
     build_device_plan(p);
@@ -712,8 +640,40 @@ sd_status sd_plan_get_info(const sd_plan* p, sd_plan_info* o) {
 sd_status sd_plan_describe(const sd_plan* p, char* buf, size_t cap, size_t* len) {
     return guard([&] {
         require(p != nullptr, "null plan");
-        sdb::write_text_out(p->opts.fuse ? sdb::describe(p->step) : std::string("unfused reference schedule\n"),
+        sdb::write_text_out(p->opts.fuse ? sdb::describe(p->step) + p->program : std::string("unfused reference schedule\n"),
                             buf, cap, len);
+    });
+}
+
+sd_status sd_plan_preview(int n, int world, const sd_group_desc* groups, size_t n_groups, const sd_plan_options* opts,
+                          sd_plan_info* info, char* json, size_t cap, size_t* len) {
+    return guard([&] {
+        require(n_groups == 0 || groups != nullptr, "null group array");
+        require(world >= 1 && (world & (world - 1)) == 0, "world size must be a power of two");
+        sd_plan_options o{};
+        if (opts) o = *opts;
+        else sd_plan_options_default(&o);
+        require(o.order == 1 || o.order == 2, "trotter order must be 1 or 2");
+        const int n_local = n - std::countr_zero(static_cast<unsigned>(world));
+        std::vector<sdb::GroupSpec> gs;
+        for (size_t i = 0; i < n_groups; ++i) gs.push_back(spec_of(groups[i]));
+        std::vector<int> phys(n);
+        std::iota(phys.begin(), phys.end(), 0);
+        int k = o.tile_qubits > 0 ? o.tile_qubits : 12;
+        k = std::min({k, sdb::max_tile_qubits(), n_local});
+        const auto ops = sdb::step_ops(gs, n, o.order, std::max(1, k - 3));
+        sdb::StepPlan sp = sdb::plan_step(ops, gs, n_local, k, 3, phys);
+        if (info) {
+            std::memset(info, 0, sizeof(*info));
+            info->n_passes_per_step = static_cast<int>(sp.passes.size());
+            info->n_ref_sweeps_per_step = static_cast<int>(std::lround(sdb::reference_sweeps(gs, o.order)));
+            info->n_group_applications =
+                static_cast<int>(o.order == 2 && gs.size() > 1 ? 2 * gs.size() - 1 : gs.size());
+            info->tile_qubits = sp.tile_qubits;
+            info->n_kernels_per_step = info->n_passes_per_step;
+            info->bytes_per_step = 2.0 * 16.0 * std::ldexp(1.0, n_local) * info->n_passes_per_step;
+        }
+        sdb::write_text_out(sdb::describe_json(sp), json, cap, len);
     });
 }
 

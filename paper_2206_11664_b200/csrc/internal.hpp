@@ -28,68 +28,122 @@ void cuda_check(cudaError_t e, const char* what);
 #define SDB_CUDA(call) ::sdb::cuda_check((call), #call)
 
 // ------------------------------------------------------- device-side plan
-// A tile pass: every CTA loads 2^k amplitudes whose index bits outside
-// `lpos` are fixed (the tile's outer bits), runs the stage list on them in
-// shared memory and stores them back in place. One pass = one full-state
-// HBM read + write.
-enum StageKind : int {
-    kStageWht = 0,    // unnormalised butterflies on local coords in `mask`
-    kStageCx = 1,     // l -> l ^ targets when the control bit is set
-    kStagePoint = 2,  // pointwise i^q(i) * exp(i*phi(i)), see PointDev
-};
+// A tile pass: a persistent CTA walks tiles of 2^k amplitudes whose index
+// bits outside the pass's local set are fixed (the tile's "outer" bits).
+// Tiles are prefetched into shared memory with cp.async (double-buffered);
+// each thread then holds 16 amplitudes in registers (a "register config":
+// 4 local coordinates vary across a thread's registers, the other k-4
+// across threads) and runs the pass's host-compiled micro-program:
+//   CFG   - shared-memory transpose into a new register config; an optional
+//           affine GF(2) index map (pending CNOT runs) is applied on the
+//           write side for free;
+//   BFLY  - unnormalised Hadamard butterflies on register coordinates;
+//   POINT - pointwise S/CZ quarter-turns and exp(-i dt Lambda) (PointDev);
+//   STORE - write back to HBM (direct from registers when the register
+//           coordinates avoid local coordinates 0..2, else via shared memory).
+// One pass = one full-state HBM read + write.
+//
+// Shared-memory slot of local index l (16-byte amplitudes): swz(l) XORs the
+// low 3 bits with bits 3-5, 6-8 and 9-11. It is GF(2)-linear, which the
+// kernel and the lowering both exploit.
+inline uint32_t host_swz(uint32_t l) { return l ^ ((l >> 3) & 7u) ^ ((l >> 6) & 7u) ^ ((l >> 9) & 7u); }
 
-struct StageDev {
+enum MicroKind : int { kOpCfg = 0, kOpBfly = 1, kOpPoint = 2, kOpStore = 3 };
+
+struct MicroOpDev {
     int kind;
-    uint32_t mask;    // WHT: local coordinate mask; CX: local target mask
-    int ctrl_local;   // CX: local coordinate of the control, or -1
-    int ctrl_phys;    // CX: physical bit of an outer control, or -1
-    int point;        // POINT: index into PointDev array
+    uint32_t mask;  // CFG: register coordinates (4 bits among k); BFLY: register slots (bits 0..3);
+                    // POINT: bit 0 = apply the pass scale here (folded into the phase factor);
+                    // STORE: bit 0 = direct from registers, bit 1 = apply the pass scale
+    int perm;       // CFG: PermDev index applied on the write side, or -1
+    int arg;        // CFG: index of this config among the pass's configs; POINT: PointDev index
+    uint32_t swc01; // CFG: swizzled slot offsets of register coordinates 0,1 (16 bits each)
+    uint32_t swc23; //      ... and 2,3
+    uint32_t cidx;  // CFG: local coordinate index of register coordinate j in byte j
     int pad;
+    uint64_t c_off[4];  // CFG: physical offsets of the register coordinates
 };
 
-// Pointwise factor on physical index i (of the whole state: the shard's rank
-// bits are OR-ed in by the kernel):
-//   q(i)   = popc(i & s1) + 2*popc(i & s2) + 2*parity(#CZ pairs fully set in i)
-//   phi(i) = -dt * sum_t  c_t * (-1)^{popc(i & zmask_t)}
+// Per-thread constant of one register config (host-computed): the local
+// index of the thread's register-0 amplitude (low 16 bits) and its swizzled
+// shared-memory slot (high 16 bits).
+using CfgThreadDev = uint32_t;
+
+// Affine map on local coordinates: l' = lo[l & 63] ^ hi[l >> 6] ^ b(h),
+// b(h) = XOR of flip[j] over the outer control bits set in the tile index.
+// lo/hi hold swizzled slots (the swizzle is GF(2)-linear, so it commutes
+// with the XOR composition); flip[] holds swizzled slots too.
+struct PermDev {
+    uint16_t lo[64];
+    uint16_t hi[64];
+    int n_ctrl;
+    int pad;
+    int ctrl_phys[16];
+    uint32_t flip[16];
+};
+
+// Pointwise factor on the full physical index i (rank bits included):
+//   q(i)   = popc(i & s1) + 2 popc(i & s2) + 2 [QT(l) ^ parity(l & M(h)) ^ C(h)]
+//            QT: local-local CZ pairs as a 2^k-bit table; M(h): local ends
+//            of local-outer pairs whose outer end is set; C(h): outer-outer
+//   phi(i) = -dt * sum_t c_t (-1)^{popc(i & zmask_t)}
 //   a     <- a * i^q * exp(i*phi)
-// Direct mode (n_seg == 0): loop over the terms' full masks.
-// Table mode  (n_seg > 0): terms are grouped by their local part u (a mask
-// over tile coordinates); per tile the kernel forms
-//   A[u] = sum_{t in seg(u)} c_t (-1)^{popc(outer_bits & zh_t)}
-// and a Walsh-Hadamard transform over `table_mask` turns A into phi/(-dt)
-// for all 2^k amplitudes of the tile (SURVEY §7 "Diagonal").
+// Direct mode (n_seg == 0) loops over full term masks. Table mode groups the
+// terms by local part u; per tile A[u] = sum c_t (-1)^{popc(h & zh_t)} and a
+// Walsh-Hadamard transform over `table_mask` in shared memory gives
+// phi(l)/(-dt) for all 2^k amplitudes of the tile (SURVEY §7 "Diagonal").
 struct PointDev {
     uint64_t s1;
     uint64_t s2;
-    int n_cz;
-    int cz_off;    // into cz pair masks (uint64 with 2 bits set)
+    int n_lo;      // local-outer CZ pairs, packed (coord << 8) | phys
+    int lo_off;
+    int n_oo;      // outer-outer CZ pairs (2-bit physical masks)
+    int oo_off;
+    int qt_off;    // offset (uint64 words) of the 2^k-bit QT table, -1 if none
     int n_terms;
     int term_off;  // into term masks / coefficients
     int n_seg;
     int seg_off;   // into SegDev
     uint32_t table_mask;
-    int pad;
 };
 
 struct SegDev {
-    uint32_t u;    // local part of the terms' masks (tile coordinates)
-    int begin;     // terms [begin, end) relative to PointDev::term_off
+    uint32_t u;  // local part of the terms' masks (tile coordinates)
+    int begin;   // terms [begin, end) relative to PointDev::term_off
     int end;
     int pad;
 };
 
 struct PassDev {
-    int k;                 // local qubit count (tile = 2^k amplitudes)
-    int n_outer;           // outer bit count (= n_local - k)
-    int n_stages;
-    int stage_off;
-    int lpos[16];          // physical bit position of local coordinate j
-    int opos[64];          // physical bit position of outer coordinate j
-    double scale;          // applied on store (exact power of two)
-    int flags;             // kPassNeedsTable: some POINT stage uses the angle table
+    int k;        // local qubit count (tile = 2^k amplitudes)
+    int n_outer;  // outer bit count (= n_local - k)
+    int n_ops;
+    int op_off;
+    int lpos[16];  // physical bit position of local coordinate j
+    int opos[64];  // physical bit position of outer coordinate j
+    double scale;  // exact power of two (applied once, see MicroOpDev)
+    int flags;     // kPassNeedsTable
+    int table_point;  // PointDev whose angle table is built at tile start, -1 if none
+    int n_cfg;        // register configs in the program
+    int cfg_off;      // offset of config 0's per-thread table in PlanDev::cfg_tb
+    int rbits;        // R: register coordinates per config (the kernel variant)
     int pad;
 };
 constexpr int kPassNeedsTable = 1;
+
+struct PlanDev {
+    const PassDev* passes;
+    const MicroOpDev* ops;
+    const PermDev* perms;
+    const PointDev* points;
+    const SegDev* segs;
+    const uint32_t* lo_pairs;
+    const uint64_t* oo_pairs;
+    const uint64_t* qt_words;
+    const CfgThreadDev* cfg_tb; // per-CFG per-thread bases (MicroOpDev::arg)
+    const uint64_t* term_masks;
+    const double* term_coeffs;  // c_t * dt_scale; the kernel multiplies by -dt
+};
 
 // --------------------------------------------------------------- handles
 struct StateImpl {
@@ -103,10 +157,11 @@ struct StateImpl {
     // Physical layout: phys_of[q] = physical index bit holding logical q.
     // Bits >= n_local select the rank. Identity unless a plan relabelled.
     std::vector<int> phys_of;
-    void* nccl = nullptr;        // ncclComm_t when attached
-    double* xbuf = nullptr;      // exchange receive buffer (lazily allocated)
+    void* nccl = nullptr;    // ncclComm_t when attached
+    double* xbuf = nullptr;  // exchange receive buffer (lazily allocated)
     uint64_t xbuf_amps = 0;
     double* reduce_buf = nullptr;
+    int sm_count = 0;
     uint64_t amps_count() const { return uint64_t(1) << n_local; }
 };
 
@@ -126,17 +181,7 @@ void launch_diag_exp(StateImpl& s, const std::vector<uint64_t>& masks,
 void launch_permute_bits(StateImpl& s, const double* src, double* dst, const int* new_pos,
                          int n_bits);
 
-// Fused pass launcher (pass_kernel.cu). `dev_*` are device arrays owned by
-// the plan; `pass_host` is the host copy of the descriptor (for k).
-struct PlanDev {
-    const PassDev* passes;
-    const StageDev* stages;
-    const PointDev* points;
-    const SegDev* segs;
-    const uint64_t* cz_masks;
-    const uint64_t* term_masks;
-    const double* term_coeffs;  // c_t * dt_scale; the kernel multiplies by -dt
-};
+// Fused pass launcher (pass_kernel.cu).
 void launch_tile_pass(StateImpl& s, const PassDev& pass_host, int pass_index, const PlanDev& plan,
                       double dt, uint64_t rank_bits);
 int max_tile_qubits();

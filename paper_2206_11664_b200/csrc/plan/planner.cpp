@@ -35,7 +35,7 @@ bool commute(const Op& a, const Op& b) {
     return (cx.targets & dg.support) == 0;
 }
 
-void emit_group(std::vector<Op>& out, const GroupSpec& g, int gi, double dt_scale) {
+void emit_group(std::vector<Op>& out, const GroupSpec& g, int gi, double dt_scale, int max_targets) {
     auto h = [&](int q) {
         Op o;
         o.kind = Op::H;
@@ -49,6 +49,17 @@ void emit_group(std::vector<Op>& out, const GroupSpec& g, int gi, double dt_scal
         const int c = g.cnots[k].first;
         uint64_t t = 0;
         while (k < g.cnots.size() && g.cnots[k].first == c) t |= bitq(g.cnots[k++].second);
+        // Same-control CNOTs commute, so a run wider than a tile can hold is
+        // split into sub-runs of at most max_targets targets.
+        while (std::popcount(t) > max_targets) {
+            uint64_t part = 0;
+            for (int j = 0; j < max_targets; ++j) {
+                const uint64_t lo = t & (~t + 1);
+                part |= lo;
+                t ^= lo;
+            }
+            runs.emplace_back(c, part);
+        }
         runs.emplace_back(c, t);
     }
     auto cx = [&](int c, uint64_t t) {
@@ -101,16 +112,16 @@ uint64_t to_phys(uint64_t logical, const std::vector<int>& phys_of) {
 
 }  // namespace
 
-std::vector<Op> step_ops(const std::vector<GroupSpec>& groups, int /*n_qubits*/, int order) {
+std::vector<Op> step_ops(const std::vector<GroupSpec>& groups, int /*n_qubits*/, int order, int max_targets) {
     std::vector<Op> ops;
     const int G = static_cast<int>(groups.size());
     if (order == 1 || G <= 1) {
-        for (int g = 0; g < G; ++g) emit_group(ops, groups[g], g, 1.0);
+        for (int g = 0; g < G; ++g) emit_group(ops, groups[g], g, 1.0, max_targets);
     } else if (order == 2) {
         // Symmetric Suzuki S2 with the middle group merged.
-        for (int g = 0; g < G - 1; ++g) emit_group(ops, groups[g], g, 0.5);
-        emit_group(ops, groups[G - 1], G - 1, 1.0);
-        for (int g = G - 2; g >= 0; --g) emit_group(ops, groups[g], g, 0.5);
+        for (int g = 0; g < G - 1; ++g) emit_group(ops, groups[g], g, 0.5, max_targets);
+        emit_group(ops, groups[G - 1], G - 1, 1.0, max_targets);
+        for (int g = G - 2; g >= 0; --g) emit_group(ops, groups[g], g, 0.5, max_targets);
     } else {
         throw std::invalid_argument("trotter order must be 1 or 2");
     }
@@ -304,11 +315,31 @@ StepPlan plan_step(const std::vector<Op>& ops, const std::vector<GroupSpec>& gro
             if (st.kind == PassStage::WHT) levels += std::popcount(st.mask);
         }
         pp.butterflies = levels;
-        pp.scale_exp = (cum + levels) / 2 - cum / 2;
         cum += levels;
         plan.passes.push_back(std::move(pp));
     }
     if (cum & 1) throw std::logic_error("plan_step: odd number of Hadamards in a step");
+    // Deferred exact normalisation: butterflies are unnormalised, and
+    // multiplying by 2^-e is exact in floating point, so the pending factor
+    // is applied only in passes that already multiply every amplitude by a
+    // phase (free), when it exceeds 2^48, or at the end of the step.
+    int pending = 0;
+    for (size_t p = 0; p < plan.passes.size(); ++p) {
+        PassPlan& pp = plan.passes[p];
+        pending += pp.butterflies;
+        bool has_phase = false;
+        for (const PassStage& st : pp.stages) {
+            if (st.kind == PassStage::POINT && !pp.points[st.point].terms.empty()) has_phase = true;
+        }
+        const bool last = p + 1 == plan.passes.size();
+        if (last || has_phase || pending >= 96) {
+            pp.scale_exp = pending / 2;
+            pending -= 2 * pp.scale_exp;
+        } else {
+            pp.scale_exp = 0;
+        }
+    }
+    if (pending != 0) throw std::logic_error("plan_step: normalisation did not close");
     plan.ref_sweeps = 0.0;
     return plan;
 }
@@ -332,6 +363,41 @@ std::string describe(const StepPlan& p) {
         }
         os << "\n";
     }
+    return os.str();
+}
+
+std::string describe_json(const StepPlan& p) {
+    std::ostringstream os;
+    os.precision(17);
+    os << "{\"tile_qubits\":" << p.tile_qubits << ",\"passes\":[";
+    for (size_t i = 0; i < p.passes.size(); ++i) {
+        const PassPlan& pp = p.passes[i];
+        os << (i ? "," : "") << "{\"lpos\":[";
+        for (size_t j = 0; j < pp.lpos.size(); ++j) os << (j ? "," : "") << pp.lpos[j];
+        os << "],\"scale_exp\":" << pp.scale_exp << ",\"stages\":[";
+        for (size_t j = 0; j < pp.stages.size(); ++j) {
+            const PassStage& st = pp.stages[j];
+            os << (j ? "," : "");
+            if (st.kind == PassStage::WHT) {
+                os << "{\"kind\":\"wht\",\"mask\":" << st.mask << "}";
+            } else if (st.kind == PassStage::CX) {
+                os << "{\"kind\":\"cx\",\"mask\":" << st.mask << ",\"ctrl_local\":" << st.ctrl_local
+                   << ",\"ctrl_phys\":" << st.ctrl_phys << "}";
+            } else {
+                const PointSpec& ps = pp.points[st.point];
+                os << "{\"kind\":\"point\",\"s1\":" << ps.s1 << ",\"s2\":" << ps.s2 << ",\"cz\":[";
+                for (size_t k = 0; k < ps.cz_masks.size(); ++k) os << (k ? "," : "") << ps.cz_masks[k];
+                os << "],\"terms\":[";
+                for (size_t k = 0; k < ps.terms.size(); ++k) {
+                    os << (k ? "," : "") << "[" << ps.terms[k].mask << "," << ps.terms[k].coeff << ","
+                       << ps.terms[k].dt_scale << "]";
+                }
+                os << "]}";
+            }
+        }
+        os << "]}";
+    }
+    os << "]}";
     return os.str();
 }
 

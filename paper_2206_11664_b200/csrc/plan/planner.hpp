@@ -33,7 +33,8 @@ struct Op {
 };
 
 // Builds the op sequence of one Trotter step (order 1 or 2).
-std::vector<Op> step_ops(const std::vector<GroupSpec>& groups, int n_qubits, int order);
+// CNOT runs wider than max_targets are split (same-control CNOTs commute).
+std::vector<Op> step_ops(const std::vector<GroupSpec>& groups, int n_qubits, int order, int max_targets);
 
 // A pass in physical bit positions.
 struct PassStage {
@@ -81,5 +82,7 @@ StepPlan plan_step(const std::vector<Op>& ops, const std::vector<GroupSpec>& gro
 double reference_sweeps(const std::vector<GroupSpec>& groups, int order);
 
 std::string describe(const StepPlan& p);
+// Machine-readable schedule (tests emulate it on the CPU).
+std::string describe_json(const StepPlan& p);
 
 }  // namespace sdb

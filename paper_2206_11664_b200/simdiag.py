@@ -504,6 +504,29 @@ class TrotterPlan:
         return {names[c]: {"ms": ms[c], "launches": ln[c], "bytes": by[c]} for c in range(4)}
 
 
+def plan_preview(n_qubits: int, groups: Sequence[DiagonalGroup], order: int = 1, tile_qubits: int = 0,
+                 world: int = 1) -> Tuple[dict, dict]:
+    """Host-only planner run: (info, schedule-as-dict). No device needed."""
+    import json
+
+    opts = A.PlanOptions()
+    check(A.sd_plan_options_default(C.byref(opts)))
+    opts.order = order
+    opts.tile_qubits = tile_qubits
+    descs = (A.GroupDesc * max(1, len(groups)))()
+    keep = []
+    for i, g in enumerate(groups):
+        d, k = g._desc()
+        descs[i] = d
+        keep.append(k)
+    info = A.PlanInfo()
+    n = C.c_size_t(0)
+    check(A.sd_plan_preview(n_qubits, world, descs, len(groups), C.byref(opts), C.byref(info), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    check(A.sd_plan_preview(n_qubits, world, descs, len(groups), C.byref(opts), None, buf, n.value + 1, C.byref(n)))
+    return {f: getattr(info, f) for f, _ in A.PlanInfo._fields_}, json.loads(buf.value.decode())
+
+
 def evolve_grouped(groups: Sequence[DiagonalGroup], psi: StateVector, plan: EvolutionPlan, **options) -> None:
     """evolve_grouped (evolve.cpp:47-58): per step and group, C_j, exp(-i dt
     Lambda_j), C_j^dagger -- executed as fused tile passes on the GPU."""

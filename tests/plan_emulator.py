@@ -1,0 +1,61 @@
+"""Numpy emulation of a fused schedule (sd_plan_preview JSON) -- test only.
+
+Applies each pass's stages to the whole state exactly as the sm_100a tile
+kernel applies them per tile (every stage is tile-local, so applying it
+globally is equivalent). Used to check the planner's reordering and
+lowering against the oracle without a GPU.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def _popcount(a: np.ndarray) -> np.ndarray:
+    a = a.copy()
+    c = np.zeros_like(a)
+    while np.any(a):
+        c += a & np.uint64(1)
+        a >>= np.uint64(1)
+    return c
+
+
+def run_schedule(psi: np.ndarray, n: int, sched: dict, dt: float, steps: int = 1) -> np.ndarray:
+    a = np.array(psi, dtype=np.complex128, copy=True)
+    idx = np.arange(1 << n, dtype=np.uint64)
+    for _ in range(steps):
+        for p in sched["passes"]:
+            lpos = p["lpos"]
+            for st in p["stages"]:
+                if st["kind"] == "wht":
+                    for j in range(len(lpos)):
+                        if (st["mask"] >> j) & 1:
+                            b = 1 << lpos[j]
+                            lo = (idx & np.uint64(b)) == 0
+                            i0 = idx[lo]
+                            i1 = i0 | np.uint64(b)
+                            x, y = a[i0].copy(), a[i1].copy()
+                            a[i0], a[i1] = x + y, x - y
+                elif st["kind"] == "cx":
+                    T = 0
+                    for j in range(len(lpos)):
+                        if (st["mask"] >> j) & 1:
+                            T |= 1 << lpos[j]
+                    cb = lpos[st["ctrl_local"]] if st["ctrl_local"] >= 0 else st["ctrl_phys"]
+                    on = ((idx >> np.uint64(cb)) & np.uint64(1)) == 1
+                    src = np.where(on, idx ^ np.uint64(T), idx)
+                    a = a[src]
+                else:
+                    q = _popcount(idx & np.uint64(st["s1"])) + 2 * _popcount(idx & np.uint64(st["s2"]))
+                    cz = np.zeros_like(idx)
+                    for m in st["cz"]:
+                        cz ^= ((idx & np.uint64(m)) == np.uint64(m)).astype(np.uint64)
+                    q = (q + 2 * cz) & np.uint64(3)
+                    a = a * (1j ** q.astype(np.int64))
+                    if st["terms"]:
+                        ang = np.zeros(1 << n)
+                        for mask, c, s in st["terms"]:
+                            par = _popcount(idx & np.uint64(mask)) & np.uint64(1)
+                            ang += np.where(par == 1, -c * s, c * s)
+                        a = a * np.exp(1j * (-dt) * ang)
+            a = a * (2.0 ** -p["scale_exp"])
+    return a

@@ -164,10 +164,9 @@ constexpr int kTableThreshold = 8;  // terms per POINT stage above which the WHT
 
 void build_device_plan(sd_plan& p) {
     sdb::StateImpl& s = p.state->impl;
-    int rbits = 4;
-    if (const char* e = std::getenv("SDB_RBITS")) rbits = std::atoi(e) == 3 ? 3 : 4;
-    sdb::HostPlanArrays A = sdb::lower_plan(p.step, s.n_local, kTableThreshold, rbits);
+    sdb::HostPlanArrays A = sdb::lower_plan(p.step, s.n_local, kTableThreshold, 4);
     p.pass_class = A.pass_class;
+
     p.program = sdb::describe_program(A);
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t sizes[] = {
@@ -180,7 +179,8 @@ void build_device_plan(sd_plan& p) {
         al(std::max<size_t>(1, A.oo_pairs.size()) * 8),
         al(std::max<size_t>(1, A.qt_words.size()) * 8),
         al(std::max<size_t>(1, A.cfg_tb.size()) * sizeof(sdb::CfgThreadDev)),
-        al(std::max<size_t>(1, A.term_masks.size()) * 8),
+        al(std::max<size_t>(1, A.term_hmask.size()) * 8),
+        al(std::max<size_t>(1, A.term_lmask.size()) * 4),
         al(std::max<size_t>(1, A.term_coeffs.size()) * 8),
     };
     size_t total = 0;
@@ -206,7 +206,8 @@ void build_device_plan(sd_plan& p) {
     p.dev.oo_pairs = static_cast<const uint64_t*>(put(A.oo_pairs.data(), A.oo_pairs.size() * 8));
     p.dev.qt_words = static_cast<const uint64_t*>(put(A.qt_words.data(), A.qt_words.size() * 8));
     p.dev.cfg_tb = static_cast<const sdb::CfgThreadDev*>(put(A.cfg_tb.data(), A.cfg_tb.size() * sizeof(sdb::CfgThreadDev)));
-    p.dev.term_masks = static_cast<const uint64_t*>(put(A.term_masks.data(), A.term_masks.size() * 8));
+    p.dev.term_hmask = static_cast<const uint64_t*>(put(A.term_hmask.data(), A.term_hmask.size() * 8));
+    p.dev.term_lmask = static_cast<const uint32_t*>(put(A.term_lmask.data(), A.term_lmask.size() * 4));
     p.dev.term_coeffs = static_cast<const double*>(put(A.term_coeffs.data(), A.term_coeffs.size() * 8));
     SDB_CUDA(cudaMemcpy(p.dev_block, host.data(), total, cudaMemcpyHostToDevice));
     p.host_passes = std::move(A.passes);

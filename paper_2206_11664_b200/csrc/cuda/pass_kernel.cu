@@ -1,17 +1,15 @@
 // Fused Clifford/diagonal tile pass for sm_100a (north star (a) + (b)).
 //
-// Persistent CTAs (one per SM) walk the tiles of a pass. Tile t+stride is
-// prefetched with cp.async into the second shared-memory buffer while tile t
-// is processed, so HBM streaming overlaps the in-tile work. Each thread keeps
-// 2^R amplitudes of the tile in registers and executes the pass's host-
-// compiled micro-program (internal.hpp): register butterflies for Hadamard
-// layers, shared-memory transposes between register configs (pending CNOT
-// index maps applied on the write side), pointwise quarter-turn phases and
-// exp(-i dt Lambda) with a per-tile Walsh-Hadamard angle table, and a store
-// that goes straight from registers to HBM when a warp's lanes cover whole
-// 128-byte lines. The program (ops + per-thread config bases) is staged in
-// shared memory once per launch; the angle table is built at the start of
-// each tile, before any amplitude occupies registers.
+// Two persistent CTAs per SM walk the tiles of a pass. A tile of 2^k
+// amplitudes is loaded from HBM straight into registers (16 amplitudes per
+// thread, 128-byte coalesced lines), transformed by the pass's host-compiled
+// micro-program (internal.hpp) and stored straight back. While one CTA is in
+// its compute phase (register butterflies for Hadamard layers, shared-memory
+// transposes between register configs with pending CNOT index maps applied
+// on the write side, pointwise quarter-turn phases and exp(-i dt Lambda)
+// with a per-tile Walsh-Hadamard angle table) the other CTA's loads and
+// stores keep HBM busy; the CTA-level double buffering costs no extra
+// shared-memory staging of the loaded tile.
 //
 // Reference semantics per op: proj/src/statevector.cpp:156-286
 // (apply_hadamard, apply_batched_cnot, apply_phase_layer, apply_diagonal_exp).
@@ -23,34 +21,69 @@ namespace sdb {
 
 namespace {
 
-// 16-byte amplitude slots: XOR the low 3 slot bits with bits 3-5, 6-8, 9-11
-// so the 8 lanes of a quarter-warp hit distinct 16-byte bank groups for any
-// three consecutive thread coordinates. GF(2)-linear (host_swz twin).
+// 16-byte amplitude slots (host_swz twin, see internal.hpp).
 __host__ __device__ constexpr uint32_t swz(uint32_t l) {
     return l ^ ((l >> 3) & 7u) ^ ((l >> 6) & 7u) ^ ((l >> 9) & 7u);
 }
-// 8-byte angle-table slots: same idea over 16-element rows.
+// 8-byte angle-table slots: XOR the low 4 bits with bits 4-7 and 8-11 so the
+// radix-16 table butterflies (lanes 16 entries apart) spread over the banks.
 __device__ __forceinline__ uint32_t tsw(uint32_t u) { return u ^ ((u >> 4) & 15u) ^ ((u >> 8) & 15u); }
 
-// scatter the low bits of v into the set bits of mask (ascending)
-__device__ __forceinline__ uint32_t pdep32(uint32_t v, uint32_t mask) {
-    uint32_t out = 0;
-    for (uint32_t m = mask; m; m &= m - 1) {
-        if (v & 1u) out |= m & (~m + 1u);
-        v >>= 1;
+// gather the bits of v selected by mask into the low bits (ascending)
+__device__ __forceinline__ uint32_t pext32(uint32_t v, uint32_t mask) {
+    uint32_t out = 0, bit = 1;
+    for (uint32_t m = mask; m; m &= m - 1, bit <<= 1) {
+        if (v & m & (~m + 1u)) out |= bit;
     }
     return out;
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+
+// sin/cos of a phase. Cody-Waite reduction by pi/2 and the fdlibm kernels on
+// [-pi/4, pi/4] (errors < 1 ulp); arguments beyond 2^20 take CUDA's sincos.
+__device__ __forceinline__ void phase_sincos(double x, double* s, double* c) {
+    if (fabs(x) > 1048576.0) {
+        sincos(x, s, c);
+        return;
+    }
+    const double q = rint(x * 0.63661977236758134308);
+    double r = fma(-q, 1.57079632673412561417e+00, x);
+    r = fma(-q, 6.07710050650619224932e-11, r);
+    r = fma(-q, 2.02226624879595063154e-21, r);
+    const double z = r * r;
+    const double ps = fma(z, fma(z, fma(z, fma(z, fma(z, 1.58969099521155010221e-10, -2.50507602534068634195e-08),
+                                                2.75573137070700676789e-06),
+                                        -1.98412698298579493134e-04),
+                                8.33333333332248946124e-03),
+                          -1.66666666666666324348e-01);
+    const double sn = fma(r * z, ps, r);
+    const double pc = z * fma(z, fma(z, fma(z, fma(z, fma(z, -1.13596475577881948265e-11, 2.08757232129817482790e-09),
+                                                   -2.75573143513906633035e-07),
+                                           2.48015872894767294178e-05),
+                                   -1.38888888888741095749e-03),
+                             4.16666666666666019037e-02);
+    const double hz = 0.5 * z;
+    const double w = 1.0 - hz;
+    const double cs = w + (((1.0 - w) - hz) + z * pc);
+    const int quad = static_cast<int>(static_cast<long long>(q) & 3);
+    double so = sn, co = cs;
+    if (quad & 1) {
+        so = cs;
+        co = -sn;
+    }
+    if (quad & 2) {
+        so = -so;
+        co = -co;
+    }
+    *s = so;
+    *c = co;
+}
 
 // Butterflies on the register coordinates selected by the compile-time mask M.
 template <int R, int M>
@@ -82,82 +115,114 @@ __device__ __forceinline__ void bfly_dispatch(double2 (&v)[1 << R], uint32_t mas
     }
 }
 
-// Angle table for one tile: A[u] from the term segments, then a real WHT
-// over `tmask` (up to RT coordinates per shared-memory round trip).
-template <int K, int NT>
-__device__ void build_angle_table(double* __restrict__ tab, const PlanDev& plan, const PointDev& pt, uint64_t full) {
-    constexpr int N = 1 << K;
-    constexpr int RT = K < 4 ? K : 4;
+// One radix-2^RB round of the in-place table WHT over compact coordinates
+// LO..LO+RB-1 (the swizzle is linear: slot(base | s << LO) = tsw(base) ^ tsw(s << LO)).
+template <int NT, int LO, int RB>
+__device__ __forceinline__ void wht_round(double* __restrict__ tab, int size) {
+    constexpr int M = 1 << RB;
+    const int groups = size >> RB;
+    constexpr uint32_t lowm = (1u << LO) - 1u;
+    for (int gi = threadIdx.x; gi < groups; gi += NT) {
+        const uint32_t g = static_cast<uint32_t>(gi);
+        const uint32_t b = tsw(((g >> LO) << (LO + RB)) | (g & lowm));
+        double w[M];
+#pragma unroll
+        for (int s = 0; s < M; ++s) w[s] = tab[b ^ tsw(static_cast<uint32_t>(s) << LO)];
+#pragma unroll
+        for (int j = 0; j < RB; ++j)
+#pragma unroll
+            for (int s = 0; s < M; ++s) {
+                if ((s >> j) & 1) continue;
+                const double a = w[s], d = w[s | (1 << j)];
+                w[s] = a + d;
+                w[s | (1 << j)] = a - d;
+            }
+#pragma unroll
+        for (int s = 0; s < M; ++s) tab[b ^ tsw(static_cast<uint32_t>(s) << LO)] = w[s];
+    }
+}
+
+template <int NT, int BITS>
+__device__ __forceinline__ void wht_fixed(double* __restrict__ tab) {
+    constexpr int size = 1 << BITS;
+    if constexpr (BITS >= 4) {
+        wht_round<NT, 0, 4>(tab, size);
+        __syncthreads();
+    }
+    if constexpr (BITS >= 8) {
+        wht_round<NT, 4, 4>(tab, size);
+        __syncthreads();
+    }
+    if constexpr (BITS >= 12) {
+        wht_round<NT, 8, 4>(tab, size);
+        __syncthreads();
+    }
+    constexpr int done = BITS >= 12 ? 12 : (BITS >= 8 ? 8 : (BITS >= 4 ? 4 : 0));
+    if constexpr (BITS > done) {
+        wht_round<NT, done, BITS - done>(tab, size);
+        __syncthreads();
+    }
+}
+
+// In-place WHT of a 2^bits table (tsw-swizzled); ends with a barrier.
+template <int NT>
+__device__ void wht_table(double* __restrict__ tab, int bits) {
+    switch (bits) {
+#define SDB_W(BB) \
+    case BB: wht_fixed<NT, BB>(tab); break;
+        SDB_W(1) SDB_W(2) SDB_W(3) SDB_W(4) SDB_W(5) SDB_W(6) SDB_W(7) SDB_W(8) SDB_W(9) SDB_W(10) SDB_W(11)
+        SDB_W(12)
+#undef SDB_W
+        default: break;
+    }
+}
+
+// Per-tile tables of the pass's table point, built before any amplitude of
+// the tile is loaded. Full mode: angle table A[u] from the term segments,
+// WHT over the table_bits compact coordinates (phi/(-dt) per local index).
+// Factor mode: one angle table per factor, WHT each, then complex tables
+// E_f = exp(-i dt theta_f) (E_0 carries table_scale).
+template <int NT>
+__device__ void build_tables(double* __restrict__ tab, const PlanDev& plan, const PointDev& pt, uint64_t full,
+                             double neg_dt, double tscale) {
     const int tid = threadIdx.x;
-    for (int u = tid; u < N; u += NT) tab[tsw(static_cast<uint32_t>(u))] = 0.0;
+    const bool fac = pt.n_fac > 0;
+    __syncthreads();  // previous tile's readers are done with tab
+    if (fac) {
+        for (int f = 0; f < pt.n_fac; ++f)
+            for (int u = tid; u < (1 << pt.fac_bits[f]); u += NT) tab[pt.fac_doff[f] + u] = 0.0;
+    } else {
+        for (int u = tid; u < (1 << pt.table_bits); u += NT) tab[u] = 0.0;
+    }
     __syncthreads();
-    const uint64_t* zm = plan.term_masks + pt.term_off;
+    const uint64_t* zh = plan.term_hmask + pt.term_off;
     const double* cf = plan.term_coeffs + pt.term_off;
     for (int s = tid; s < pt.n_seg; s += NT) {
         const SegDev sg = plan.segs[pt.seg_off + s];
         double acc = 0.0;
         for (int q = sg.begin; q < sg.end; ++q) {
-            const uint64_t par = __popcll(full & __ldg(zm + q)) & 1ull;
+            const uint64_t par = __popcll(full & __ldg(zh + q)) & 1ull;
             acc += __longlong_as_double(__double_as_longlong(__ldg(cf + q)) ^ static_cast<long long>(par << 63));
         }
-        tab[tsw(sg.u)] = acc;
+        tab[(fac ? pt.fac_doff[sg.fac] : 0) + tsw(sg.u)] = acc;
     }
     __syncthreads();
-    uint32_t rem = pt.table_mask;
-    while (rem) {
-        uint32_t cb4[RT];
-        int r = 0;
-#pragma unroll
-        for (int j = 0; j < RT; ++j) {
-            cb4[j] = rem & (~rem + 1u);
-            rem &= rem - 1u;
-            if (cb4[j]) ++r;
-        }
-        uint32_t cm = 0;
-#pragma unroll
-        for (int j = 0; j < RT; ++j) cm |= cb4[j];
-        const uint32_t others = (static_cast<uint32_t>(N) - 1u) & ~cm;
-        const int groups = N >> r;
-        for (int gi = tid; gi < groups; gi += NT) {
-            const uint32_t b = pdep32(static_cast<uint32_t>(gi), others);
-            double w[1 << RT];
-            uint32_t idx[1 << RT];
-#pragma unroll
-            for (int s = 0; s < (1 << RT); ++s) {
-                uint32_t x = b;
-                bool valid = true;
-#pragma unroll
-                for (int j = 0; j < RT; ++j) {
-                    if ((s >> j) & 1) {
-                        if (!cb4[j]) valid = false;
-                        x |= cb4[j];
-                    }
-                }
-                idx[s] = tsw(x);
-                w[s] = valid ? tab[idx[s]] : 0.0;
-            }
-#pragma unroll
-            for (int j = 0; j < RT; ++j) {
-                if (!cb4[j]) continue;
-#pragma unroll
-                for (int s = 0; s < (1 << RT); ++s) {
-                    if ((s >> j) & 1) continue;
-                    const double a = w[s], d = w[s | (1 << j)];
-                    w[s] = a + d;
-                    w[s | (1 << j)] = a - d;
-                }
-            }
-#pragma unroll
-            for (int s = 0; s < (1 << RT); ++s) {
-                bool valid = true;
-#pragma unroll
-                for (int j = 0; j < RT; ++j)
-                    if (((s >> j) & 1) && !cb4[j]) valid = false;
-                if (valid) tab[idx[s]] = w[s];
-            }
-        }
-        __syncthreads();
+    if (!fac) {
+        wht_table<NT>(tab, pt.table_bits);
+        return;
     }
+    for (int f = 0; f < pt.n_fac; ++f) wht_table<NT>(tab + pt.fac_doff[f], pt.fac_bits[f]);
+    for (int f = 0; f < pt.n_fac; ++f) {
+        const double sc = f == 0 ? tscale : 1.0;
+        double2* const E = reinterpret_cast<double2*>(tab + pt.fac_coff[f]);
+        const double* const th = tab + pt.fac_doff[f];
+        for (int x = tid; x < (1 << pt.fac_bits[f]); x += NT) {
+            double sn, cs;
+            phase_sincos(neg_dt * th[tsw(static_cast<uint32_t>(x))], &sn, &cs);
+            E[swz(static_cast<uint32_t>(x))] = make_double2(cs * sc, sn * sc);
+        }
+    }
+    __syncthreads();
 }
 
 template <int K, int RB>
@@ -168,15 +233,17 @@ struct Cfg {
     static constexpr int N = 1 << K;
     static constexpr int LO = K < 6 ? K : 6;
     static constexpr int HI = K - LO;
+    static constexpr int MINB = K >= 12 ? 2 : 1;  // resident CTAs per SM the register budget is cut for
 };
 
+constexpr int kTbaseChunks = 4;  // outer bits covered by the tile-base tables: 4 x 7
+
 template <int K, int RB>
-__global__ void __launch_bounds__(Cfg<K, RB>::NT)
+__global__ void __launch_bounds__(Cfg<K, RB>::NT, Cfg<K, RB>::MINB)
 k_tile_pass(double2* __restrict__ psi, PlanDev plan, int pass_index, double neg_dt, uint64_t rank_bits,
             uint64_t n_tiles) {
     using C = Cfg<K, RB>;
     constexpr int R = C::R, NR = C::NR, NT = C::NT, N = C::N, LO = C::LO, HI = C::HI;
-    constexpr int TB = K - R;  // thread bits
     const PassDev& P = plan.passes[pass_index];
     const int tid = threadIdx.x;
     const int n_outer = P.n_outer;
@@ -185,14 +252,16 @@ k_tile_pass(double2* __restrict__ psi, PlanDev plan, int pass_index, double neg_
     const bool has_table = P.table_point >= 0;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2* const ring = reinterpret_cast<double2*>(smem_raw);  // 2 tile buffers
-    double* const tab = reinterpret_cast<double*>(ring + 2 * N);  // angle table (if any)
-    MicroOpDev* const s_ops = reinterpret_cast<MicroOpDev*>(tab + (has_table ? N : 0));
-    uint32_t* const s_cfg = reinterpret_cast<uint32_t*>(s_ops + n_ops);  // n_cfg x NT
+    double2* const buf = reinterpret_cast<double2*>(smem_raw);            // transpose buffer
+    double* const tab = reinterpret_cast<double*>(buf + N);               // angle table (if any)
+    const int tab_words = P.tab_words;
+    MicroOpDev* const s_ops = reinterpret_cast<MicroOpDev*>(tab + tab_words);
+    uint32_t* const s_cfg = reinterpret_cast<uint32_t*>(s_ops + n_ops);   // n_cfg x NT
+    uint32_t* const s_qt = s_cfg + n_cfg * NT;                            // QT bit tables
     __shared__ uint64_t off_lo[1 << LO];
     __shared__ uint64_t off_hi[1 << HI];
-    __shared__ uint64_t s_tbase[3][128];  // tile index (7 bits per chunk) -> outer offset
-    __shared__ uint64_t s_offj[NR];       // offset of local index j << TB
+    __shared__ uint64_t s_tbase[kTbaseChunks][128];  // tile index (7 bits per chunk) -> outer offset
+    __shared__ uint32_t s_pl[3][64], s_ph[3][64];    // local index (low / high 6 bits) -> compact table index
 
     // ---- stage the program and the index tables (once per launch)
     {
@@ -201,6 +270,8 @@ k_tile_pass(double2* __restrict__ psi, PlanDev plan, int pass_index, double neg_
         const int words = n_ops * static_cast<int>(sizeof(MicroOpDev) / sizeof(int4));
         for (int i = tid; i < words; i += NT) dst[i] = __ldg(src + i);
         for (int i = tid; i < n_cfg * NT; i += NT) s_cfg[i] = __ldg(plan.cfg_tb + P.cfg_off + i);
+        const uint32_t* q32 = reinterpret_cast<const uint32_t*>(plan.qt_words + P.qt_off);
+        for (int i = tid; i < 2 * P.n_qt_words; i += NT) s_qt[i] = __ldg(q32 + i);
     }
     for (int i = tid; i < (1 << LO); i += NT) {
         uint64_t o = 0;
@@ -214,7 +285,7 @@ k_tile_pass(double2* __restrict__ psi, PlanDev plan, int pass_index, double neg_
             if ((i >> j) & 1) o |= 1ull << P.lpos[LO + j];
         off_hi[i] = o;
     }
-    for (int i = tid; i < 3 * 128; i += NT) {
+    for (int i = tid; i < kTbaseChunks * 128; i += NT) {
         const int c = i >> 7, v = i & 127;
         uint64_t o = 0;
         for (int j = 0; j < 7; ++j) {
@@ -223,210 +294,102 @@ k_tile_pass(double2* __restrict__ psi, PlanDev plan, int pass_index, double neg_
         }
         s_tbase[c][v] = o;
     }
-    for (int j = tid; j < NR; j += NT) {
-        uint64_t o = 0;
-        for (int b = 0; b < R; ++b)
-            if ((j >> b) & 1) o |= 1ull << P.lpos[TB + b];
-        s_offj[j] = o;
+    if (has_table) {
+        const PointDev& tp = plan.points[P.table_point];
+        const int nf = tp.n_fac > 0 ? tp.n_fac : 1;
+        for (int f = 0; f < nf; ++f) {
+            const uint32_t tm = tp.n_fac > 0 ? tp.fac_mask[f] : tp.table_mask;
+            const int nlo = __popc(tm & 63u);
+            for (int i = tid; i < 64; i += NT) {
+                const uint32_t lo = pext32(static_cast<uint32_t>(i), tm & 63u);
+                const uint32_t hi = pext32(static_cast<uint32_t>(i), tm >> 6) << nlo;
+                // factor tables hold complex entries in amplitude-swizzled slots
+                s_pl[f][i] = tp.n_fac > 0 ? swz(lo) : tsw(lo);
+                s_ph[f][i] = tp.n_fac > 0 ? swz(hi) : tsw(hi);
+            }
+        }
     }
     const double scale = P.scale;  // exact power of two
-    const PointDev* const tpt = has_table ? plan.points + P.table_point : nullptr;
     __syncthreads();
 
     auto tile_base = [&](uint64_t t) {
-        return s_tbase[0][t & 127] | s_tbase[1][(t >> 7) & 127] | s_tbase[2][(t >> 14) & 127];
+        uint64_t b = 0;
+#pragma unroll
+        for (int c = 0; c < kTbaseChunks; ++c) b |= s_tbase[c][(t >> (7 * c)) & 127];
+        return b;
     };
     auto off_of = [&](uint32_t l) -> uint64_t { return off_lo[l & ((1u << LO) - 1u)] | off_hi[l >> LO]; };
-    // prefetch: this thread copies local indices tid + j*NT (= tid | j << TB)
-    const uint32_t pf_sw = swz(static_cast<uint32_t>(tid));
-    const uint64_t pf_off = off_of(static_cast<uint32_t>(tid));
-    auto prefetch = [&](uint64_t t, double2* dst) {
-        const double2* g = psi + (tile_base(t) | pf_off);
-#pragma unroll
-        for (int j = 0; j < NR; ++j) {
-            const uint32_t sj = swz(static_cast<uint32_t>(j) << TB);  // compile-time
-            cp_async16(dst + (pf_sw ^ sj), g + s_offj[j]);
-        }
-        cp_async_commit();
-    };
 
     const uint64_t stride = gridDim.x;
-    uint64_t t = blockIdx.x;
-    if (t < n_tiles) prefetch(t, ring);
-    for (int it = 0; t < n_tiles; t += stride, ++it) {
-        double2* const cb = ring + (it & 1) * N;
-        cp_async_wait_all();
-        __syncthreads();  // tile t resident in cb; everyone is done with the other buffer
-        if (t + stride < n_tiles) prefetch(t + stride, ring + ((it + 1) & 1) * N);
-
+    for (uint64_t t = blockIdx.x; t < n_tiles; t += stride) {
         const uint64_t base = tile_base(t);
         const uint64_t full = rank_bits | base;
         double2* const g = psi + base;
-        if (has_table) build_angle_table<K, NT>(tab, plan, *tpt, full);
+        if (has_table) build_tables<NT>(tab, plan, plan.points[P.table_point], full, neg_dt, P.table_scale);
 
         double2 v[NR];
-        bool in_regs = false;
         uint32_t tb = 0, swt = 0;  // local index / slot of this thread's register 0
         uint32_t cidx = 0;         // local coordinate index of register coordinate j (byte j)
-        uint32_t swc[R];           // slot offset of register coordinate j
+        uint32_t swc[4] = {0, 0, 0, 0};
+        uint64_t coff[4] = {0, 0, 0, 0};
+        bool smem_busy = true;     // smem may still be read by other threads (sync before writing)
+
+        auto set_cfg = [&](const MicroOpDev& op) {
+            const uint32_t w = s_cfg[op.arg * NT + tid];
+            tb = w & 0xffffu;
+            swt = w >> 16;
+            cidx = op.cidx;
+            swc[0] = op.swc01 & 0xffffu;
+            swc[1] = op.swc01 >> 16;
+            swc[2] = op.swc23 & 0xffffu;
+            swc[3] = op.swc23 >> 16;
 #pragma unroll
-        for (int j = 0; j < R; ++j) swc[j] = 0;
+            for (int j = 0; j < 4; ++j) coff[j] = op.c_off[j];
+        };
+        auto phys_offsets = [&](uint64_t (&o)[NR]) {
+            o[0] = off_of(tb);
+#pragma unroll
+            for (int j = 0; j < R; ++j)
+#pragma unroll
+                for (int s = 0; s < (1 << j); ++s) o[s + (1 << j)] = o[s] | coff[j];
+        };
 
         for (int oi = 0; oi < n_ops; ++oi) {
-            const int4 hdr = reinterpret_cast<const int4*>(s_ops + oi)[0];
-            const int kind = hdr.x;
-            const uint32_t mask = static_cast<uint32_t>(hdr.y);
-            const int perm = hdr.z;
-            const int arg = hdr.w;
-            if (kind == kOpCfg) {
-                if (in_regs || perm >= 0) {
-                    uint32_t sb = 0;
-                    const PermDev* pm = perm >= 0 ? plan.perms + perm : nullptr;
-                    if (pm) {
-                        for (int j = 0; j < pm->n_ctrl; ++j)
-                            if ((full >> pm->ctrl_phys[j]) & 1ull) sb ^= pm->flip[j];
-                    }
-                    if (!in_regs) {
-                        // permutation straight out of the load buffer: identity config
+            const MicroOpDev& op = s_ops[oi];
+            const int kind = op.kind;
+            if (kind == kOpLoad) {
+                set_cfg(op);
+                uint64_t o[NR];
+                phys_offsets(o);
 #pragma unroll
-                        for (int j = 0; j < NR; ++j) v[j] = cb[pf_sw ^ swz(static_cast<uint32_t>(j) << TB)];
-                        tb = static_cast<uint32_t>(tid);
-                        cidx = 0;
+                for (int s = 0; s < NR; ++s) v[s] = __ldcs(g + o[s]);
+                // Pull this CTA's next tile into L2 while the current one is
+                // transformed: HBM keeps streaming through the compute phase
+                // without holding registers or shared memory.
+                if (t + stride < n_tiles) {
+                    const double2* gn = psi + tile_base(t + stride);
 #pragma unroll
-                        for (int j = 0; j < R; ++j) cidx |= static_cast<uint32_t>(TB + j) << (8 * j);
-                        __syncthreads();
-                    }
-                    if (pm) {
-                        uint32_t l[NR];
-                        l[0] = tb;
-#pragma unroll
-                        for (int j = 0; j < R; ++j)
-#pragma unroll
-                            for (int s = 0; s < (1 << j); ++s)
-                                l[s + (1 << j)] = l[s] | (1u << ((cidx >> (8 * j)) & 255u));
-#pragma unroll
-                        for (int s = 0; s < NR; ++s) {
-                            const uint32_t m = static_cast<uint32_t>(pm->lo[l[s] & 63u]) ^
-                                               static_cast<uint32_t>(pm->hi[l[s] >> 6]) ^ sb;
-                            cb[m] = v[s];
-                        }
-                    } else {
-                        uint32_t a[NR];
-                        a[0] = swt;
-#pragma unroll
-                        for (int j = 0; j < R; ++j)
-#pragma unroll
-                            for (int s = 0; s < (1 << j); ++s) a[s + (1 << j)] = a[s] ^ swc[j];
-#pragma unroll
-                        for (int s = 0; s < NR; ++s) cb[a[s]] = v[s];
-                    }
-                    __syncthreads();
+                    for (int s = 0; s < NR; ++s) prefetch_l2(gn + o[s]);
                 }
-                const int4 ext = reinterpret_cast<const int4*>(s_ops + oi)[1];
-                const uint32_t w = s_cfg[arg * NT + tid];
-                tb = w & 0xffffu;
-                swt = w >> 16;
-                cidx = static_cast<uint32_t>(ext.z);
-                swc[0] = static_cast<uint32_t>(ext.x) & 0xffffu;
-                if (R > 1) swc[1 % R] = static_cast<uint32_t>(ext.x) >> 16;
-                if (R > 2) swc[2 % R] = static_cast<uint32_t>(ext.y) & 0xffffu;
-                if (R > 3) swc[3 % R] = static_cast<uint32_t>(ext.y) >> 16;
-                {
-                    uint32_t a[NR];
-                    a[0] = swt;
+            } else if (kind == kOpCfg) {
+                if (smem_busy) __syncthreads();
+                if (op.perm >= 0) {
+                    const PermDev* pm = plan.perms + op.perm;
+                    uint32_t sb = 0;
+                    for (int j = 0; j < pm->n_ctrl; ++j)
+                        if ((full >> pm->ctrl_phys[j]) & 1ull) sb ^= pm->flip[j];
+                    uint32_t l[NR];
+                    l[0] = tb;
 #pragma unroll
                     for (int j = 0; j < R; ++j)
 #pragma unroll
-                        for (int s = 0; s < (1 << j); ++s) a[s + (1 << j)] = a[s] ^ swc[j];
+                        for (int s = 0; s < (1 << j); ++s)
+                            l[s + (1 << j)] = l[s] | (1u << ((cidx >> (8 * j)) & 255u));
 #pragma unroll
-                    for (int s = 0; s < NR; ++s) v[s] = cb[a[s]];
-                }
-                in_regs = true;
-                __syncthreads();
-            } else if (kind == kOpBfly) {
-                bfly_dispatch<R>(v, mask);
-            } else if (kind == kOpPoint) {
-                const PointDev& pt = plan.points[arg];
-                const bool table = arg == P.table_point;
-                const bool scale_here = (mask & 1u) != 0;
-                const int n_terms = pt.n_terms;
-                const uint64_t s1 = pt.s1, s2 = pt.s2;
-                // per-tile CZ pieces: local ends of local-outer pairs, outer-outer parity
-                uint32_t mh = 0, cc = 0;
-                for (int j = 0; j < pt.n_lo; ++j) {
-                    const uint32_t wl = __ldg(plan.lo_pairs + pt.lo_off + j);
-                    if ((full >> (wl & 0xffu)) & 1ull) mh ^= 1u << (wl >> 8);
-                }
-                for (int j = 0; j < pt.n_oo; ++j) {
-                    const uint64_t m = __ldg(plan.oo_pairs + pt.oo_off + j);
-                    cc ^= ((full & m) == m) ? 1u : 0u;
-                }
-                const uint32_t tmask = pt.table_mask;
-                const uint64_t* zm = plan.term_masks + pt.term_off;
-                const double* cf = plan.term_coeffs + pt.term_off;
-                const uint64_t* qt = pt.qt_off >= 0 ? plan.qt_words + pt.qt_off : nullptr;
-                uint32_t l[NR];
-                uint64_t o[NR];
-                l[0] = tb;
-                o[0] = off_of(tb);
-#pragma unroll
-                for (int j = 0; j < R; ++j) {
-                    const uint32_t cbit = 1u << ((cidx >> (8 * j)) & 255u);
-                    const uint64_t coff = off_of(cbit);
-#pragma unroll
-                    for (int s = 0; s < (1 << j); ++s) {
-                        l[s + (1 << j)] = l[s] | cbit;
-                        o[s + (1 << j)] = o[s] | coff;
-                    }
-                }
-#pragma unroll
-                for (int s = 0; s < NR; ++s) {
-                    const uint64_t i = full | o[s];
-                    uint32_t czp = cc ^ (__popc(l[s] & mh) & 1u);
-                    if (qt) czp ^= static_cast<uint32_t>((__ldg(qt + (l[s] >> 6)) >> (l[s] & 63u)) & 1ull);
-                    const unsigned q = (__popcll(i & s1) + 2u * __popcll(i & s2) + 2u * czp) & 3u;
-                    double2 a = v[s];
-                    if (q & 2u) a = make_double2(-a.x, -a.y);
-                    if (q & 1u) a = make_double2(-a.y, a.x);
-                    if (n_terms > 0) {
-                        double ang;
-                        if (table) {
-                            ang = tab[tsw(l[s] & tmask)];
-                        } else {
-                            ang = 0.0;
-                            for (int q2 = 0; q2 < n_terms; ++q2) {
-                                const uint64_t par = __popcll(i & __ldg(zm + q2)) & 1ull;
-                                ang += __longlong_as_double(__double_as_longlong(__ldg(cf + q2)) ^
-                                                            static_cast<long long>(par << 63));
-                            }
-                        }
-                        double sn, cs;
-                        sincos(neg_dt * ang, &sn, &cs);
-                        if (scale_here) {
-                            sn *= scale;
-                            cs *= scale;
-                        }
-                        a = make_double2(a.x * cs - a.y * sn, a.x * sn + a.y * cs);
-                    }
-                    v[s] = a;
-                }
-            } else {  // kOpStore
-                const double sc = (mask & 2u) ? scale : 1.0;
-                if (mask & 1u) {
-                    uint64_t o[NR];
-                    o[0] = off_of(tb);
-#pragma unroll
-                    for (int j = 0; j < R; ++j) {
-                        const uint64_t coff = off_of(1u << ((cidx >> (8 * j)) & 255u));
-#pragma unroll
-                        for (int s = 0; s < (1 << j); ++s) o[s + (1 << j)] = o[s] | coff;
-                    }
-                    if (mask & 2u) {
-#pragma unroll
-                        for (int s = 0; s < NR; ++s) __stcs(g + o[s], make_double2(v[s].x * sc, v[s].y * sc));
-                    } else {
-#pragma unroll
-                        for (int s = 0; s < NR; ++s) __stcs(g + o[s], v[s]);
+                    for (int s = 0; s < NR; ++s) {
+                        const uint32_t m = static_cast<uint32_t>(__ldg(&pm->lo[l[s] & 63u])) ^
+                                           static_cast<uint32_t>(__ldg(&pm->hi[l[s] >> 6])) ^ sb;
+                        buf[m] = v[s];
                     }
                 } else {
                     uint32_t a[NR];
@@ -436,27 +399,179 @@ k_tile_pass(double2* __restrict__ psi, PlanDev plan, int pass_index, double neg_
 #pragma unroll
                         for (int s = 0; s < (1 << j); ++s) a[s + (1 << j)] = a[s] ^ swc[j];
 #pragma unroll
-                    for (int s = 0; s < NR; ++s) cb[a[s]] = v[s];
-                    __syncthreads();
-                    double2* gp = g + pf_off;
+                    for (int s = 0; s < NR; ++s) buf[a[s]] = v[s];
+                }
+                __syncthreads();
+                set_cfg(op);
+                {
+                    uint32_t a[NR];
+                    a[0] = swt;
 #pragma unroll
-                    for (int j = 0; j < NR; ++j) {
-                        const double2 x = cb[pf_sw ^ swz(static_cast<uint32_t>(j) << TB)];
-                        __stcs(gp + s_offj[j], make_double2(x.x * sc, x.y * sc));
+                    for (int j = 0; j < R; ++j)
+#pragma unroll
+                        for (int s = 0; s < (1 << j); ++s) a[s + (1 << j)] = a[s] ^ swc[j];
+#pragma unroll
+                    for (int s = 0; s < NR; ++s) v[s] = buf[a[s]];
+                }
+                smem_busy = true;
+            } else if (kind == kOpBfly) {
+                bfly_dispatch<R>(v, op.mask);
+            } else if (kind == kOpPoint) {
+                const PointDev& pt = plan.points[op.arg];
+                const bool table = op.arg == P.table_point;
+                const bool scale_here = (op.mask & 1u) != 0;
+                const int n_terms = pt.n_terms;
+                uint32_t cb[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) cb[j] = 1u << ((cidx >> (8 * j)) & 255u);
+                // ---- quarter turns: q(tb ^ r_s) = q0 + sum_{j in s} dq_j + 2 QT(r_s)  (mod 4)
+                // (QT is a quadratic form: QT(a^b) = QT(a) + QT(b) + B(a,b), B bilinear)
+                uint32_t m2 = pt.s2L;
+                unsigned q0 = __popcll(full & pt.s1H) + 2u * __popcll(full & pt.s2H);
+                for (int j = 0; j < pt.n_lo; ++j) {
+                    const uint32_t wl = __ldg(plan.lo_pairs + pt.lo_off + j);
+                    if ((full >> (wl & 0xffu)) & 1ull) m2 ^= 1u << (wl >> 8);
+                }
+                for (int j = 0; j < pt.n_oo; ++j) {
+                    const uint64_t m = __ldg(plan.oo_pairs + pt.oo_off + j);
+                    if ((full & m) == m) q0 += 2u;
+                }
+                const uint32_t* qt = pt.qt_word >= 0 ? s_qt + 2 * pt.qt_word : nullptr;
+                auto qtb = [&](uint32_t l) -> unsigned { return qt ? (qt[l >> 5] >> (l & 31u)) & 1u : 0u; };
+                const unsigned qt_tb = qtb(tb);
+                q0 += __popc(tb & pt.s1L) + 2u * (__popc(tb & m2) + qt_tb);
+                unsigned dq[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const unsigned bil = qt ? (qtb(tb ^ cb[j]) ^ qt_tb ^ qtb(cb[j])) : 0u;
+                    dq[j] = __popc(cb[j] & pt.s1L) + 2u * (__popc(cb[j] & m2) + bil);
+                }
+                const uint32_t qr = op.pad;  // bit s: QT(r_s), host-computed for this config
+                // ---- angle-table slots of this thread's registers (compact index, swizzle linear)
+                const int n_fac = table ? pt.n_fac : 0;
+                uint32_t ts0 = 0, tc[4] = {0, 0, 0, 0};
+                uint32_t fb[3] = {0, 0, 0};
+                if (table && n_fac == 0) {
+                    ts0 = s_pl[0][tb & 63u] ^ s_ph[0][tb >> 6];
+                    tc[0] = tsw(op.swc01 & 0xffffu);
+                    tc[1] = tsw(op.swc01 >> 16);
+                    tc[2] = tsw(op.swc23 & 0xffffu);
+                    tc[3] = tsw(op.swc23 >> 16);
+                }
+#pragma unroll
+                for (int f = 0; f < 3; ++f)
+                    if (f < n_fac) fb[f] = s_pl[f][tb & 63u] ^ s_ph[f][tb >> 6];
+                // ---- direct-mode terms (few) with the tile's outer sign folded in
+                const bool direct = !table && n_terms > 0 && n_terms <= 8;
+                double dc[8];
+                uint32_t dz[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    dc[q] = 0.0;
+                    dz[q] = 0u;
+                }
+                if (direct) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        if (q < n_terms) {
+                            const uint64_t par = __popcll(full & __ldg(plan.term_hmask + pt.term_off + q)) & 1ull;
+                            dc[q] = __longlong_as_double(__double_as_longlong(__ldg(plan.term_coeffs + pt.term_off + q)) ^
+                                                         static_cast<long long>(par << 63));
+                            dz[q] = __ldg(plan.term_lmask + pt.term_off + q);
+                        }
                     }
+                }
+#pragma unroll
+                for (int s2 = 0; s2 < NR; ++s2) {
+                    unsigned q = q0 + 2u * ((qr >> s2) & 1u);
+#pragma unroll
+                    for (int j = 0; j < R; ++j)
+                        if ((s2 >> j) & 1) q += dq[j];
+                    q &= 3u;
+                    double2 a = v[s2];
+                    if (q & 2u) a = make_double2(-a.x, -a.y);
+                    if (q & 1u) a = make_double2(-a.y, a.x);
+                    if (n_fac > 0) {
+                        double2 e = make_double2(1.0, 0.0);
+#pragma unroll
+                        for (int f = 0; f < 3; ++f) {
+                            if (f < n_fac) {
+                                uint32_t x = fb[f];
+#pragma unroll
+                                for (int j = 0; j < R; ++j)
+                                    if ((s2 >> j) & 1) x ^= static_cast<uint32_t>(op.c_off[f] >> (16 * j)) & 0xffffu;
+                                const double2 t = reinterpret_cast<const double2*>(tab + pt.fac_coff[f])[x];
+                                e = f == 0 ? t : make_double2(e.x * t.x - e.y * t.y, e.x * t.y + e.y * t.x);
+                            }
+                        }
+                        a = make_double2(a.x * e.x - a.y * e.y, a.x * e.y + a.y * e.x);
+                    } else if (n_terms > 0) {
+                        double ang = 0.0;
+                        if (table) {
+                            uint32_t ti = ts0;
+#pragma unroll
+                            for (int j = 0; j < R; ++j)
+                                if ((s2 >> j) & 1) ti ^= tc[j];
+                            ang = tab[ti];
+                        } else if (direct) {
+                            uint32_t l = tb;
+#pragma unroll
+                            for (int j = 0; j < R; ++j)
+                                if ((s2 >> j) & 1) l |= cb[j];
+#pragma unroll
+                            for (int q2 = 0; q2 < 8; ++q2) {
+                                const long long sg = static_cast<long long>(__popc(l & dz[q2]) & 1u) << 63;
+                                ang += __longlong_as_double(__double_as_longlong(dc[q2]) ^ sg);
+                            }
+                        } else {
+                            uint32_t l = tb;
+#pragma unroll
+                            for (int j = 0; j < R; ++j)
+                                if ((s2 >> j) & 1) l |= cb[j];
+                            for (int q2 = 0; q2 < n_terms; ++q2) {
+                                const uint64_t zm = __ldg(plan.term_hmask + pt.term_off + q2);
+                                const uint32_t zl = __ldg(plan.term_lmask + pt.term_off + q2);
+                                const long long sg =
+                                    static_cast<long long>((__popcll(full & zm) + __popc(l & zl)) & 1u) << 63;
+                                ang += __longlong_as_double(__double_as_longlong(__ldg(plan.term_coeffs + pt.term_off + q2)) ^ sg);
+                            }
+                        }
+                        double sn, cs;
+                        phase_sincos(neg_dt * ang, &sn, &cs);
+                        if (scale_here) {
+                            sn *= scale;
+                            cs *= scale;
+                        }
+                        a = make_double2(a.x * cs - a.y * sn, a.x * sn + a.y * cs);
+                    }
+                    v[s2] = a;
+                }
+            } else {  // kOpStore
+                uint64_t o[NR];
+                phys_offsets(o);
+                if (op.mask & 2u) {
+#pragma unroll
+                    for (int s = 0; s < NR; ++s) __stcs(g + o[s], make_double2(v[s].x * scale, v[s].y * scale));
+                } else {
+#pragma unroll
+                    for (int s = 0; s < NR; ++s) __stcs(g + o[s], v[s]);
                 }
             }
         }
     }
-    cp_async_wait_all();
+}
+
+template <int K, int RB>
+size_t smem_bytes(const PassDev& ph) {
+    using C = Cfg<K, RB>;
+    return sizeof(double2) * C::N + sizeof(double) * ph.tab_words + sizeof(MicroOpDev) * ph.n_ops +
+           sizeof(uint32_t) * ph.n_cfg * C::NT + sizeof(uint64_t) * ph.n_qt_words;
 }
 
 template <int K, int RB>
 void launch_kr(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& plan, double dt, uint64_t rank_bits) {
     using C = Cfg<K, RB>;
-    const bool need_table = ph.table_point >= 0;
-    const size_t smem = sizeof(double2) * 2 * C::N + (need_table ? sizeof(double) * C::N : 0) +
-                        sizeof(MicroOpDev) * ph.n_ops + sizeof(uint32_t) * ph.n_cfg * C::NT;
+    const size_t smem = smem_bytes<K, RB>(ph);
     static size_t configured = 0;
     if (smem > configured) {
         SDB_CUDA(cudaFuncSetAttribute(k_tile_pass<K, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -477,8 +592,10 @@ void launch_kr(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& p
 
 template <int K>
 void launch_k(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& plan, double dt, uint64_t rank_bits) {
-    if (ph.rbits == 3) launch_kr<K, 3>(s, ph, pass_index, plan, dt, rank_bits);
-    else launch_kr<K, 4>(s, ph, pass_index, plan, dt, rank_bits);
+    // R = 4 register coordinates (16 amplitudes per thread). R = 3 with twice the
+    // threads spills at the 2-CTA/SM register budget (measured).
+    if (ph.rbits != 4 && K >= 4) throw std::invalid_argument("tile pass: unsupported register config");
+    launch_kr<K, 4>(s, ph, pass_index, plan, dt, rank_bits);
 }
 
 }  // namespace
@@ -487,6 +604,7 @@ int max_tile_qubits() { return 12; }
 
 void launch_tile_pass(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& plan, double dt,
                       uint64_t rank_bits) {
+    if (ph.n_outer > 7 * kTbaseChunks) throw std::invalid_argument("tile pass: too many outer bits");
     switch (ph.k) {
 #define SDB_K(KK) \
     case KK: launch_k<KK>(s, ph, pass_index, plan, dt, rank_bits); break;

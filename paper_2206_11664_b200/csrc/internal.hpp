@@ -28,40 +28,47 @@ void cuda_check(cudaError_t e, const char* what);
 #define SDB_CUDA(call) ::sdb::cuda_check((call), #call)
 
 // ------------------------------------------------------- device-side plan
-// A tile pass: a persistent CTA walks tiles of 2^k amplitudes whose index
-// bits outside the pass's local set are fixed (the tile's "outer" bits).
-// Tiles are prefetched into shared memory with cp.async (double-buffered);
-// each thread then holds 16 amplitudes in registers (a "register config":
-// 4 local coordinates vary across a thread's registers, the other k-4
-// across threads) and runs the pass's host-compiled micro-program:
+// A tile pass: persistent CTAs (two per SM) walk tiles of 2^k amplitudes
+// whose index bits outside the pass's local set are fixed (the tile's
+// "outer" bits). Each thread holds 2^R amplitudes in registers (a "register
+// config": R local coordinates vary across a thread's registers, the other
+// k-R across threads) and runs the pass's host-compiled micro-program:
+//   LOAD  - read the tile from HBM straight into registers (config `arg`);
 //   CFG   - shared-memory transpose into a new register config; an optional
 //           affine GF(2) index map (pending CNOT runs) is applied on the
 //           write side for free;
 //   BFLY  - unnormalised Hadamard butterflies on register coordinates;
 //   POINT - pointwise S/CZ quarter-turns and exp(-i dt Lambda) (PointDev);
-//   STORE - write back to HBM (direct from registers when the register
-//           coordinates avoid local coordinates 0..2, else via shared memory).
-// One pass = one full-state HBM read + write.
+//   STORE - write the registers back to HBM.
+// One pass = one full-state HBM read + write. Loads/stores are coalesced
+// when a config's threads cover local coordinates 0..2 in lanes 0..2 (8
+// lanes x 16 B = one 128-byte line); the lowering arranges that for the
+// LOAD and STORE configs.
 //
 // Shared-memory slot of local index l (16-byte amplitudes): swz(l) XORs the
-// low 3 bits with bits 3-5, 6-8 and 9-11. It is GF(2)-linear, which the
-// kernel and the lowering both exploit.
+// low 3 bits with bits 3-5, 6-8 and 9-11, so coordinate c lands in slot bit
+// (c mod 3); lanes 0..2 of every config get coordinates with distinct
+// residues, which makes each quarter-warp of a 128-bit access conflict-free.
+// swz is GF(2)-linear, which the kernel and the lowering both exploit.
 inline uint32_t host_swz(uint32_t l) { return l ^ ((l >> 3) & 7u) ^ ((l >> 6) & 7u) ^ ((l >> 9) & 7u); }
 
-enum MicroKind : int { kOpCfg = 0, kOpBfly = 1, kOpPoint = 2, kOpStore = 3 };
+enum MicroKind : int { kOpLoad = 0, kOpCfg = 1, kOpBfly = 2, kOpPoint = 3, kOpStore = 4 };
 
 struct MicroOpDev {
     int kind;
-    uint32_t mask;  // CFG: register coordinates (4 bits among k); BFLY: register slots (bits 0..3);
+    uint32_t mask;  // LOAD/CFG: register coordinates (R bits among k); BFLY: register slots (bits 0..3);
                     // POINT: bit 0 = apply the pass scale here (folded into the phase factor);
-                    // STORE: bit 0 = direct from registers, bit 1 = apply the pass scale
+                    // STORE: bit 1 = apply the pass scale
     int perm;       // CFG: PermDev index applied on the write side, or -1
-    int arg;        // CFG: index of this config among the pass's configs; POINT: PointDev index
-    uint32_t swc01; // CFG: swizzled slot offsets of register coordinates 0,1 (16 bits each)
-    uint32_t swc23; //      ... and 2,3
-    uint32_t cidx;  // CFG: local coordinate index of register coordinate j in byte j
-    int pad;
-    uint64_t c_off[4];  // CFG: physical offsets of the register coordinates
+    int arg;        // LOAD/CFG: index of this config among the pass's configs; POINT: PointDev index
+    uint32_t swc01; // LOAD/CFG: swizzled slot offsets of register coordinates 0,1 (16 bits each);
+                    // POINT: compact angle-table index of register coordinates 0,1
+    uint32_t swc23; //           ... and 2,3
+    uint32_t cidx;  // LOAD/CFG: local coordinate index of register coordinate j in byte j
+    int pad;        // POINT: bit s = QT(r_s) for the register combination s of the current config
+    uint64_t c_off[4];  // LOAD/CFG: physical offsets of the register coordinates;
+                        // POINT (factor mode): c_off[f] packs the swizzled compact
+                        // slot offset of register coordinate j in bits 16j..16j+15
 };
 
 // Per-thread constant of one register config (host-computed): the local
@@ -82,36 +89,53 @@ struct PermDev {
     uint32_t flip[16];
 };
 
-// Pointwise factor on the full physical index i (rank bits included):
-//   q(i)   = popc(i & s1) + 2 popc(i & s2) + 2 [QT(l) ^ parity(l & M(h)) ^ C(h)]
-//            QT: local-local CZ pairs as a 2^k-bit table; M(h): local ends
-//            of local-outer pairs whose outer end is set; C(h): outer-outer
+// Pointwise factor on the full physical index i = outer(h) | local(l):
+//   q(i)   = popc(i & s1) + 2 popc(i & s2) + 2 [QT(l) ^ parity(l & M(h)) ^ C(h)]   (mod 4)
+//            s1/s2 split into local-coordinate masks (s1L, s2L) and outer
+//            physical masks (s1H, s2H); QT: local-local CZ pairs as a
+//            2^k-bit table; M(h): local ends of local-outer pairs whose outer
+//            end is set; C(h): parity of outer-outer pairs
 //   phi(i) = -dt * sum_t c_t (-1)^{popc(i & zmask_t)}
 //   a     <- a * i^q * exp(i*phi)
-// Direct mode (n_seg == 0) loops over full term masks. Table mode groups the
-// terms by local part u; per tile A[u] = sum c_t (-1)^{popc(h & zh_t)} and a
-// Walsh-Hadamard transform over `table_mask` in shared memory gives
-// phi(l)/(-dt) for all 2^k amplitudes of the tile (SURVEY §7 "Diagonal").
+// Direct mode (n_seg == 0, few terms): per amplitude, sum over the terms
+// with the outer sign folded per tile. Table mode groups the terms by their
+// local part u (compacted onto the table coordinates `table_mask`); per tile
+// A[u] = sum c_t (-1)^{popc(h & zh_t)}, and a Walsh-Hadamard transform over
+// the table_bits compact coordinates in shared memory gives phi/(-dt) for
+// every amplitude of the tile (SURVEY section 7 "Diagonal").
 struct PointDev {
-    uint64_t s1;
-    uint64_t s2;
+    uint64_t s1H;
+    uint64_t s2H;
+    uint32_t s1L;
+    uint32_t s2L;
     int n_lo;      // local-outer CZ pairs, packed (coord << 8) | phys
     int lo_off;
     int n_oo;      // outer-outer CZ pairs (2-bit physical masks)
     int oo_off;
-    int qt_off;    // offset (uint64 words) of the 2^k-bit QT table, -1 if none
+    int qt_word;   // word offset of the 2^k-bit QT table inside the pass's staged QT region, -1 if none
     int n_terms;
-    int term_off;  // into term masks / coefficients
+    int term_off;  // into term_hmask / term_lmask / term_coeffs
     int n_seg;
     int seg_off;   // into SegDev
-    uint32_t table_mask;
+    uint32_t table_mask;  // full mode: local coordinates spanned by the angle table
+    int table_bits;       // popcount(table_mask)
+    // Factor mode (n_fac > 0): the terms' local parts split into n_fac
+    // disjoint coordinate sets (no term spans two), so
+    //   exp(-i dt theta(l)) = prod_f E_f[pext(l, fac_mask[f])]
+    // with per-tile complex tables E_f of 2^fac_bits[f] entries (2^b sincos
+    // per tile instead of one per amplitude).
+    int n_fac;
+    uint32_t fac_mask[3];
+    int fac_bits[3];
+    int fac_doff[3];  // angle scratch of factor f: double offset in the table region
+    int fac_coff[3];  // complex table of factor f: double offset (even) in the table region
 };
 
 struct SegDev {
-    uint32_t u;  // local part of the terms' masks (tile coordinates)
+    uint32_t u;  // compact table index of the terms' local part
     int begin;   // terms [begin, end) relative to PointDev::term_off
     int end;
-    int pad;
+    int fac;     // factor table the segment belongs to (factor mode)
 };
 
 struct PassDev {
@@ -126,8 +150,11 @@ struct PassDev {
     int table_point;  // PointDev whose angle table is built at tile start, -1 if none
     int n_cfg;        // register configs in the program
     int cfg_off;      // offset of config 0's per-thread table in PlanDev::cfg_tb
-    int rbits;        // R: register coordinates per config (the kernel variant)
-    int pad;
+    int rbits;        // R: register coordinates per config
+    int qt_off;       // first QT word of this pass in PlanDev::qt_words
+    int n_qt_words;   // QT words staged into shared memory
+    int tab_words;    // 8-byte words of the per-tile table region (even; 0 if none)
+    double table_scale;  // factor mode: exact scale folded into E_0 (1 if applied elsewhere)
 };
 constexpr int kPassNeedsTable = 1;
 
@@ -140,8 +167,9 @@ struct PlanDev {
     const uint32_t* lo_pairs;
     const uint64_t* oo_pairs;
     const uint64_t* qt_words;
-    const CfgThreadDev* cfg_tb; // per-CFG per-thread bases (MicroOpDev::arg)
-    const uint64_t* term_masks;
+    const CfgThreadDev* cfg_tb; // per-config per-thread bases (MicroOpDev::arg)
+    const uint64_t* term_hmask; // outer (physical) part of each term's z-mask
+    const uint32_t* term_lmask; // local-coordinate part (direct mode)
     const double* term_coeffs;  // c_t * dt_scale; the kernel multiplies by -dt
 };
 

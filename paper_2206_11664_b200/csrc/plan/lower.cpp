@@ -1,11 +1,13 @@
 // Pass -> micro-program lowering (host). See internal.hpp for the device
-// semantics of CFG / BFLY / POINT / STORE.
+// semantics of LOAD / CFG / BFLY / POINT / STORE.
 //
 // Register configs: each thread holds R = min(4, k) local coordinates in
-// registers. A WHT stage's coordinates are covered in ascending chunks of
-// R (the lowest coordinates first, so the final config of a pass tends to
-// hold high coordinates and the store can go straight from registers to
-// HBM with coalesced lanes); coordinates already in the current config are
+// registers. The tile is loaded straight into registers, so the LOAD config
+// (and the config the STORE runs from) keeps local coordinates 0..2 on the
+// thread lanes 0..2: every 8 lanes then cover one 128-byte line. A WHT
+// stage's coordinates are covered in chunks of R; the chunk holding
+// coordinates 0..2 is scheduled in the middle of the pass so the first and
+// last configs stay coalesced. Coordinates already in the current config are
 // done in place. CNOT runs become a pending affine index map that the next
 // transpose applies on its write side (no extra shared-memory traffic).
 #include "lower.hpp"
@@ -61,6 +63,97 @@ uint32_t slot_mask(uint32_t coords, uint32_t cfg) {
     return out;
 }
 
+uint32_t pext_host(uint32_t v, uint32_t mask) {
+    uint32_t out = 0, bit = 1;
+    for (uint32_t m = mask; m; m &= m - 1, bit <<= 1) {
+        if (v & m & (~m + 1u)) out |= bit;
+    }
+    return out;
+}
+
+// Thread-coordinate order of a config: tid bit b <-> order[b]. Lanes 0..2
+// take coordinates 0..2 when they are thread coordinates (coalescing);
+// otherwise three coordinates with distinct residues mod 3 (conflict-free
+// 128-bit shared-memory access, see swz in internal.hpp); the rest ascend.
+std::vector<int> thread_order(uint32_t others) {
+    std::vector<int> order;
+    uint32_t rest = others;
+    if ((others & 7u) == 7u) {
+        order = {0, 1, 2};
+        rest &= ~7u;
+    } else {
+        bool used[3] = {false, false, false};
+        for (uint32_t m = others; m && order.size() < 3; m &= m - 1) {
+            const int c = std::countr_zero(m);
+            if (!used[c % 3]) {
+                used[c % 3] = true;
+                order.push_back(c);
+                rest &= ~(1u << c);
+            }
+        }
+    }
+    for (uint32_t m = rest; m; m &= m - 1) order.push_back(std::countr_zero(m));
+    return order;
+}
+
+// Factor cover of a table point: split the coordinates its terms touch into
+// at most three disjoint sets of <= kMaxFacBits coordinates such that no
+// term's local part spans two sets (connected components of the "appear in
+// one term" relation, first-fit-decreasing into bins). Empty result: no such
+// cover, use the full angle table with a sincos per amplitude.
+constexpr int kMaxFacBits = 9;
+std::vector<uint32_t> factor_cover(const std::vector<uint32_t>& us, uint32_t tm) {
+    std::vector<int> parent(32);
+    for (int i = 0; i < 32; ++i) parent[i] = i;
+    auto find = [&](int x) {
+        while (parent[x] != x) x = parent[x] = parent[parent[x]];
+        return x;
+    };
+    for (uint32_t u : us) {
+        if (!u) continue;
+        const int a = std::countr_zero(u);
+        for (uint32_t m = u & (u - 1); m; m &= m - 1) parent[find(std::countr_zero(m))] = find(a);
+    }
+    std::vector<uint32_t> comps;
+    for (uint32_t m = tm; m; m &= m - 1) {
+        const int c = std::countr_zero(m);
+        if (find(c) != c) continue;
+        uint32_t comp = 0;
+        for (uint32_t q = tm; q; q &= q - 1) {
+            if (find(std::countr_zero(q)) == c) comp |= q & (~q + 1u);
+        }
+        comps.push_back(comp);
+    }
+    std::stable_sort(comps.begin(), comps.end(),
+                     [](uint32_t a, uint32_t b) { return std::popcount(a) > std::popcount(b); });
+    // fewest bins first, then the most balanced (smallest total table size)
+    for (int nb = 1; nb <= 3; ++nb) {
+        const int cap = std::min(kMaxFacBits, (std::popcount(tm) + nb - 1) / nb + 2);
+        std::vector<uint32_t> bins(nb, 0);
+        bool ok = true;
+        for (uint32_t c : comps) {
+            int best = -1;
+            for (int b = 0; b < nb; ++b) {
+                if (std::popcount(bins[b] | c) > cap) continue;
+                if (best < 0 || std::popcount(bins[b]) < std::popcount(bins[best])) best = b;
+            }
+            if (best < 0) {
+                ok = false;
+                break;
+            }
+            bins[best] |= c;
+        }
+        if (!ok) continue;
+        std::vector<uint32_t> out;
+        for (uint32_t b : bins) {
+            if (b) out.push_back(b);
+        }
+        if (out.empty()) out.push_back(0);
+        return out;
+    }
+    return {};
+}
+
 }  // namespace
 
 HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, int rbits) {
@@ -69,7 +162,8 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
         const int K = static_cast<int>(pp.lpos.size());
         const int R = std::min(rbits, K);
         const uint32_t all = K >= 32 ? ~0u : ((1u << K) - 1u);
-        const uint32_t low3 = 7u & all;
+        const bool coalesce = K - R >= 3;
+        const uint32_t low3 = coalesce ? 7u : 0u;
         PassDev pd{};
         pd.k = K;
         uint64_t Lphys = 0;
@@ -90,13 +184,24 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
         pd.n_cfg = 0;
         pd.cfg_off = static_cast<int>(A.cfg_tb.size());
         pd.rbits = R;
+        pd.qt_off = static_cast<int>(A.qt_words.size());
+        pd.tab_words = 0;
+        pd.table_scale = 1.0;
+        auto local_of = [&](uint64_t phys) {
+            uint32_t m = 0;
+            for (int j = 0; j < K; ++j) {
+                if ((phys >> pp.lpos[j]) & 1) m |= 1u << j;
+            }
+            return m;
+        };
 
         // upcoming WHT coordinates (for filling partial configs)
         std::vector<uint32_t> wht_after(pp.stages.size() + 1, 0);
         for (int i = static_cast<int>(pp.stages.size()) - 1; i >= 0; --i) {
             wht_after[i] = wht_after[i + 1] | (pp.stages[i].kind == PassStage::WHT ? pp.stages[i].mask : 0u);
         }
-        uint32_t cur = 0;  // current config (0 = data still in the load buffer)
+        uint32_t cur = 0;
+        bool loaded = false;
         bool scale_placed = false;
         Affine P(K);
         int transposes = 0;
@@ -117,42 +222,40 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
             take(all, true);
             return cfg;
         };
-        auto emit_cfg = [&](uint32_t cfg) {
+        auto emit = [&](int kind, uint32_t cfg) {
             MicroOpDev op{};
-            op.kind = kOpCfg;
+            op.kind = kind;
             op.mask = cfg;
             op.perm = -1;
-            {
-                // per-thread base: thread bits scattered into the non-register coordinates
-                const int nt = 1 << (K - R);
-                const uint32_t others = all & ~cfg;
-                op.arg = pd.n_cfg++;
-                for (int tid = 0; tid < nt; ++tid) {
-                    uint32_t tb = 0, v = static_cast<uint32_t>(tid);
-                    for (uint32_t m = others; m; m &= m - 1, v >>= 1) {
-                        if (v & 1u) tb |= m & (~m + 1u);
-                    }
-                    A.cfg_tb.push_back(tb | (host_swz(tb) << 16));
+            op.arg = pd.n_cfg++;
+            const uint32_t others = all & ~cfg;
+            const std::vector<int> order = thread_order(others);
+            const int nt = 1 << (K - R);
+            for (int tid = 0; tid < nt; ++tid) {
+                uint32_t tb = 0;
+                for (size_t b = 0; b < order.size(); ++b) {
+                    if ((tid >> b) & 1) tb |= 1u << order[b];
                 }
-                uint32_t sw[4] = {0, 0, 0, 0};
-                int j = 0;
-                for (uint32_t m = cfg; m && j < 4; m &= m - 1, ++j) {
-                    const int c = std::countr_zero(m);
-                    sw[j] = host_swz(1u << c);
-                    op.cidx |= static_cast<uint32_t>(c) << (8 * j);
-                    op.c_off[j] = 1ull << pp.lpos[c];
-                }
-                op.swc01 = sw[0] | (sw[1] << 16);
-                op.swc23 = sw[2] | (sw[3] << 16);
+                A.cfg_tb.push_back(tb | (host_swz(tb) << 16));
             }
-            if (!P.identity) {
+            uint32_t sw[4] = {0, 0, 0, 0};
+            int j = 0;
+            for (uint32_t m = cfg; m && j < 4; m &= m - 1, ++j) {
+                const int c = std::countr_zero(m);
+                sw[j] = host_swz(1u << c);
+                op.cidx |= static_cast<uint32_t>(c) << (8 * j);
+                op.c_off[j] = 1ull << pp.lpos[c];
+            }
+            op.swc01 = sw[0] | (sw[1] << 16);
+            op.swc23 = sw[2] | (sw[3] << 16);
+            if (kind == kOpCfg && !P.identity) {
                 PermDev pm{};
                 for (int x = 0; x < 64; ++x) {
                     uint32_t lo = 0, hi = 0;
-                    for (int j = 0; j < 6; ++j) {
-                        if ((x >> j) & 1) {
-                            if (j < K) lo ^= P.col[j];
-                            if (j + 6 < K) hi ^= P.col[j + 6];
+                    for (int b = 0; b < 6; ++b) {
+                        if ((x >> b) & 1) {
+                            if (b < K) lo ^= P.col[b];
+                            if (b + 6 < K) hi ^= P.col[b + 6];
                         }
                     }
                     pm.lo[x] = static_cast<uint16_t>(host_swz(lo));
@@ -160,54 +263,73 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                 }
                 if (P.outer.size() > 16) throw std::logic_error("lower_plan: too many outer-controlled CNOT runs");
                 pm.n_ctrl = static_cast<int>(P.outer.size());
-                for (size_t j = 0; j < P.outer.size(); ++j) {
-                    pm.ctrl_phys[j] = P.outer[j].first;
-                    pm.flip[j] = host_swz(P.outer[j].second);
+                for (size_t b = 0; b < P.outer.size(); ++b) {
+                    pm.ctrl_phys[b] = P.outer[b].first;
+                    pm.flip[b] = host_swz(P.outer[b].second);
                 }
                 op.perm = static_cast<int>(A.perms.size());
                 A.perms.push_back(pm);
                 P = Affine(K);
                 only_point = false;
             }
-            if (cur != 0) ++transposes;
+            if (kind == kOpCfg) ++transposes;
             A.ops.push_back(op);
             cur = cfg;
         };
+        // LOAD (identity positions), then flush a pending CNOT map if any.
+        auto load = [&](uint32_t cfg) {
+            emit(kOpLoad, cfg);
+            loaded = true;
+            if (!P.identity) emit(kOpCfg, cfg);
+        };
         for (size_t si = 0; si < pp.stages.size(); ++si) {
             const PassStage& st = pp.stages[si];
+            const uint32_t after = wht_after[si + 1];
             if (st.kind == PassStage::WHT) {
                 only_point = false;
                 uint32_t bits = st.mask;
                 while (bits) {
-                    if (cur != 0 && P.identity && (bits & cur)) {
+                    if (loaded && P.identity && (bits & cur)) {
                         const uint32_t doing = bits & cur;
-                        {
-                            MicroOpDev b{};
-                            b.kind = kOpBfly;
-                            b.mask = slot_mask(doing, cur);
-                            b.perm = -1;
-                            A.ops.push_back(b);
-                        }
+                        MicroOpDev b{};
+                        b.kind = kOpBfly;
+                        b.mask = slot_mask(doing, cur);
+                        b.perm = -1;
+                        A.ops.push_back(b);
                         bits &= ~doing;
                         continue;
                     }
-                    const uint32_t chunk = lowest_bits(bits, R);
-                    emit_cfg(fill(chunk, (bits | wht_after[si + 1]) & ~chunk));
+                    if (!loaded) {
+                        const uint32_t chunk = lowest_bits(bits & ~low3, R);
+                        load(fill(chunk, (bits | after) & ~chunk));
+                        continue;
+                    }
+                    uint32_t chunk;
+                    if (bits & low3) {
+                        chunk = bits & low3;
+                        chunk |= lowest_bits(bits & ~low3, R - std::popcount(chunk));
+                    } else {
+                        chunk = lowest_bits(bits, R);
+                    }
+                    emit(kOpCfg, fill(chunk, (bits | after) & ~chunk));
                 }
             } else if (st.kind == PassStage::CX) {
                 only_point = false;
                 if (st.ctrl_local >= 0) P.compose_local(st.ctrl_local, st.mask);
                 else P.compose_outer(st.ctrl_phys, st.mask);
             } else {
-                if (cur == 0 || !P.identity) {
-                    const uint32_t next = wht_after[si + 1];
-                    emit_cfg(fill(lowest_bits(next & ~low3, R), next));
+                if (!loaded) {
+                    load(fill(lowest_bits(after & ~low3, R), after));
+                } else if (!P.identity) {
+                    emit(kOpCfg, fill(lowest_bits(after & ~low3, R), after));
                 }
                 const PointSpec& ps = pp.points[st.point];
                 PointDev pt{};
-                pt.s1 = ps.s1;
-                pt.s2 = ps.s2;
-                pt.qt_off = -1;
+                pt.s1L = local_of(ps.s1);
+                pt.s2L = local_of(ps.s2);
+                pt.s1H = ps.s1 & ~Lphys;
+                pt.s2H = ps.s2 & ~Lphys;
+                pt.qt_word = -1;
                 // CZ pairs by locality
                 std::vector<std::pair<int, int>> ll;
                 pt.lo_off = static_cast<int>(A.lo_pairs.size());
@@ -224,7 +346,7 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                 pt.n_lo = static_cast<int>(A.lo_pairs.size()) - pt.lo_off;
                 pt.n_oo = static_cast<int>(A.oo_pairs.size()) - pt.oo_off;
                 if (!ll.empty()) {
-                    pt.qt_off = static_cast<int>(A.qt_words.size());
+                    pt.qt_word = static_cast<int>(A.qt_words.size()) - pd.qt_off;
                     const uint32_t N = 1u << K;
                     std::vector<uint64_t> words((N + 63) / 64, 0);
                     for (uint32_t l = 0; l < N; ++l) {
@@ -234,7 +356,7 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                     }
                     A.qt_words.insert(A.qt_words.end(), words.begin(), words.end());
                 }
-                pt.term_off = static_cast<int>(A.term_masks.size());
+                pt.term_off = static_cast<int>(A.term_hmask.size());
                 pt.n_terms = static_cast<int>(ps.terms.size());
                 pt.seg_off = static_cast<int>(A.segs.size());
                 if (pt.n_terms > table_threshold && pd.table_point < 0) {
@@ -244,33 +366,71 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                         double c;
                     };
                     std::vector<T> ts;
+                    uint32_t tm = 0;
                     for (const PointTerm& t : ps.terms) {
-                        uint32_t u = 0;
-                        for (int j = 0; j < K; ++j) {
-                            if ((t.mask >> pp.lpos[j]) & 1) u |= 1u << j;
-                        }
+                        const uint32_t u = local_of(t.mask);
+                        tm |= u;
                         ts.push_back({u, t.mask & ~Lphys, t.coeff * t.dt_scale});
                     }
-                    std::stable_sort(ts.begin(), ts.end(), [](const T& a, const T& b) { return a.u < b.u; });
-                    uint32_t tm = 0;
-                    for (size_t i = 0; i < ts.size();) {
+                    std::vector<uint32_t> us;
+                    for (const T& t : ts) us.push_back(t.u);
+                    const std::vector<uint32_t> facs = factor_cover(us, tm);
+                    pt.table_mask = tm;
+                    pt.table_bits = std::popcount(tm);
+                    pt.n_fac = static_cast<int>(facs.size());
+                    std::vector<int> fac_of(ts.size(), 0);
+                    if (pt.n_fac > 0) {
+                        int off = 0;
+                        for (int f = 0; f < pt.n_fac; ++f) {
+                            pt.fac_mask[f] = facs[f];
+                            pt.fac_bits[f] = std::popcount(facs[f]);
+                            pt.fac_doff[f] = off;
+                            off += std::max(2, 1 << pt.fac_bits[f]);
+                        }
+                        for (int f = 0; f < pt.n_fac; ++f) {
+                            pt.fac_coff[f] = off;
+                            off += 2 * (1 << pt.fac_bits[f]);
+                        }
+                        pd.tab_words = off;
+                        for (size_t i = 0; i < ts.size(); ++i) {
+                            int f = 0;
+                            while (f + 1 < pt.n_fac && (ts[i].u & ~facs[f])) ++f;
+                            fac_of[i] = f;
+                            ts[i].u = pext_host(ts[i].u, facs[f]);
+                        }
+                    } else {
+                        pd.tab_words = std::max(2, 1 << pt.table_bits);
+                        for (T& t : ts) t.u = pext_host(t.u, tm);
+                    }
+                    std::vector<size_t> ord(ts.size());
+                    for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
+                    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+                        return fac_of[a] != fac_of[b] ? fac_of[a] < fac_of[b] : ts[a].u < ts[b].u;
+                    });
+                    std::vector<T> sorted;
+                    std::vector<int> sfac;
+                    for (size_t i : ord) {
+                        sorted.push_back(ts[i]);
+                        sfac.push_back(fac_of[i]);
+                    }
+                    for (size_t i = 0; i < sorted.size();) {
                         size_t j = i;
-                        while (j < ts.size() && ts[j].u == ts[i].u) ++j;
-                        A.segs.push_back({ts[i].u, static_cast<int>(i), static_cast<int>(j), 0});
-                        tm |= ts[i].u;
+                        while (j < sorted.size() && sorted[j].u == sorted[i].u && sfac[j] == sfac[i]) ++j;
+                        A.segs.push_back({sorted[i].u, static_cast<int>(i), static_cast<int>(j), sfac[i]});
                         i = j;
                     }
                     pt.n_seg = static_cast<int>(A.segs.size()) - pt.seg_off;
-                    pt.table_mask = tm;
-                    for (const T& t : ts) {
-                        A.term_masks.push_back(t.zh);
+                    for (const T& t : sorted) {
+                        A.term_hmask.push_back(t.zh);
+                        A.term_lmask.push_back(0);
                         A.term_coeffs.push_back(t.c);
                     }
                     pd.flags |= kPassNeedsTable;
                     pd.table_point = static_cast<int>(A.points.size());
                 } else {
                     for (const PointTerm& t : ps.terms) {
-                        A.term_masks.push_back(t.mask);
+                        A.term_hmask.push_back(t.mask & ~Lphys);
+                        A.term_lmask.push_back(local_of(t.mask));
                         A.term_coeffs.push_back(t.coeff * t.dt_scale);
                     }
                 }
@@ -279,25 +439,60 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                     po.kind = kOpPoint;
                     po.perm = -1;
                     po.arg = static_cast<int>(A.points.size());
+                    // per-config constants of this point: compact table index of each
+                    // register coordinate (swc01/swc23) and QT(r_s) for the 2^R
+                    // register combinations r_s (pad, bit s)
+                    std::vector<uint32_t> cbits;
+                    for (uint32_t m = cur; m; m &= m - 1) cbits.push_back(m & (~m + 1u));
+                    uint32_t tic[4] = {0, 0, 0, 0};
+                    if (pd.table_point == static_cast<int>(A.points.size())) {
+                        for (size_t j = 0; j < cbits.size() && j < 4; ++j) tic[j] = pext_host(cbits[j], pt.table_mask);
+                    }
+                    po.swc01 = tic[0] | (tic[1] << 16);
+                    po.swc23 = tic[2] | (tic[3] << 16);
+                    if (pd.table_point == static_cast<int>(A.points.size())) {
+                        for (int f = 0; f < pt.n_fac; ++f) {
+                            uint64_t packed = 0;
+                            for (size_t j = 0; j < cbits.size() && j < 4; ++j) {
+                                packed |= uint64_t(host_swz(pext_host(cbits[j], pt.fac_mask[f]))) << (16 * j);
+                            }
+                            po.c_off[f] = packed;
+                        }
+                    }
+                    uint32_t qr = 0;
+                    if (pt.qt_word >= 0) {
+                        const uint64_t* words = A.qt_words.data() + pd.qt_off + pt.qt_word;
+                        for (int sidx = 0; sidx < (1 << cbits.size()); ++sidx) {
+                            uint32_t r = 0;
+                            for (size_t j = 0; j < cbits.size(); ++j) {
+                                if ((sidx >> j) & 1) r |= cbits[j];
+                            }
+                            if ((words[r >> 6] >> (r & 63)) & 1ull) qr |= 1u << sidx;
+                        }
+                    }
+                    po.pad = static_cast<int>(qr);
                     if (pp.scale_exp > 0 && !scale_placed && pt.n_terms > 0) {
                         po.mask = 1u;
                         scale_placed = true;
+                        if (pd.table_point == static_cast<int>(A.points.size()) && pt.n_fac > 0) pd.table_scale = pd.scale;
                     }
                     A.ops.push_back(po);
                 }
                 A.points.push_back(pt);
             }
         }
-        if (cur == 0 || !P.identity) emit_cfg(fill(0, 0));
-        // direct store when the register coordinates avoid coordinates 0..2
+        if (!loaded) {
+            load(fill(0, 0));
+        } else if (!P.identity || (cur & low3)) {
+            emit(kOpCfg, fill(0, 0));
+        }
         MicroOpDev so{};
         so.kind = kOpStore;
-        so.mask = (cur & low3) == 0 ? 1u : 0u;
         so.perm = -1;
-        if (!(so.mask & 1u)) ++transposes;
         if (pp.scale_exp > 0 && !scale_placed) so.mask |= 2u;
         A.ops.push_back(so);
         pd.n_ops = static_cast<int>(A.ops.size()) - pd.op_off;
+        pd.n_qt_words = static_cast<int>(A.qt_words.size()) - pd.qt_off;
         A.passes.push_back(pd);
         A.pass_class.push_back(only_point ? 1 : 0);
         A.transposes.push_back(transposes);
@@ -312,13 +507,21 @@ std::string describe_program(const HostPlanArrays& a) {
         os << "pass " << p << " k=" << pd.k << " transposes=" << a.transposes[p] << " :";
         for (int i = 0; i < pd.n_ops; ++i) {
             const MicroOpDev& op = a.ops[pd.op_off + i];
-            if (op.kind == kOpCfg) os << " CFG{" << std::hex << op.mask << std::dec << (op.perm >= 0 ? ",perm" : "") << "}";
+            if (op.kind == kOpLoad) os << " LD{" << std::hex << op.mask << std::dec << "}";
+            else if (op.kind == kOpCfg) os << " CFG{" << std::hex << op.mask << std::dec << (op.perm >= 0 ? ",perm" : "") << "}";
             else if (op.kind == kOpBfly) os << " B" << std::popcount(op.mask);
             else if (op.kind == kOpPoint) {
                 const PointDev& pt = a.points[op.arg];
-                os << " P[t" << pt.n_terms << (pt.n_seg ? "T" : "") << ",lo" << pt.n_lo << ",oo" << pt.n_oo
-                   << (pt.qt_off >= 0 ? ",qt" : "") << "]";
-            } else os << ((op.mask & 1u) ? " ST" : " ST(smem)") << ((op.mask & 2u) ? "*s" : "");
+                std::string tdesc;
+                if (pt.n_seg && pt.n_fac) {
+                    tdesc = "F";
+                    for (int f = 0; f < pt.n_fac; ++f) tdesc += (f ? "+" : "") + std::to_string(pt.fac_bits[f]);
+                } else if (pt.n_seg) {
+                    tdesc = "T" + std::to_string(pt.table_bits);
+                }
+                os << " P[t" << pt.n_terms << tdesc << ",lo" << pt.n_lo
+                   << ",oo" << pt.n_oo << (pt.qt_word >= 0 ? ",qt" : "") << "]";
+            } else os << " ST" << ((op.mask & 2u) ? "*s" : "");
         }
         os << "\n";
     }

@@ -20,7 +20,8 @@ struct HostPlanArrays {
     std::vector<uint64_t> oo_pairs;
     std::vector<uint64_t> qt_words;
     std::vector<CfgThreadDev> cfg_tb;
-    std::vector<uint64_t> term_masks;
+    std::vector<uint64_t> term_hmask;
+    std::vector<uint32_t> term_lmask;
     std::vector<double> term_coeffs;
     std::vector<int> pass_class;   // 0 = transform pass, 1 = diagonal-only pass
     std::vector<int> transposes;   // shared-memory transposes per pass (CFG with a write side)

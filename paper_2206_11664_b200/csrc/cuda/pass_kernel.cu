@@ -142,26 +142,21 @@ __device__ __forceinline__ void wht_round(double* __restrict__ tab, int size) {
     }
 }
 
+// Radix-4 rounds (the tables are built while the tile's loads are in flight,
+// so the round keeps few registers live).
+template <int NT, int LO, int BITS>
+__device__ __forceinline__ void wht_rounds(double* __restrict__ tab) {
+    if constexpr (LO < BITS) {
+        constexpr int RB = BITS - LO >= 2 ? 2 : 1;
+        wht_round<NT, LO, RB>(tab, 1 << BITS);
+        __syncthreads();
+        wht_rounds<NT, LO + RB, BITS>(tab);
+    }
+}
+
 template <int NT, int BITS>
 __device__ __forceinline__ void wht_fixed(double* __restrict__ tab) {
-    constexpr int size = 1 << BITS;
-    if constexpr (BITS >= 4) {
-        wht_round<NT, 0, 4>(tab, size);
-        __syncthreads();
-    }
-    if constexpr (BITS >= 8) {
-        wht_round<NT, 4, 4>(tab, size);
-        __syncthreads();
-    }
-    if constexpr (BITS >= 12) {
-        wht_round<NT, 8, 4>(tab, size);
-        __syncthreads();
-    }
-    constexpr int done = BITS >= 12 ? 12 : (BITS >= 8 ? 8 : (BITS >= 4 ? 4 : 0));
-    if constexpr (BITS > done) {
-        wht_round<NT, done, BITS - done>(tab, size);
-        __syncthreads();
-    }
+    wht_rounds<NT, 0, BITS>(tab);
 }
 
 // In-place WHT of a 2^bits table (tsw-swizzled); ends with a barrier.
@@ -325,7 +320,6 @@ k_tile_pass(double2* __restrict__ psi, PlanDev plan, int pass_index, double neg_
         const uint64_t base = tile_base(t);
         const uint64_t full = rank_bits | base;
         double2* const g = psi + base;
-        if (has_table) build_tables<NT>(tab, plan, plan.points[P.table_point], full, neg_dt, P.table_scale);
 
         double2 v[NR];
         uint32_t tb = 0, swt = 0;  // local index / slot of this thread's register 0
@@ -371,6 +365,8 @@ k_tile_pass(double2* __restrict__ psi, PlanDev plan, int pass_index, double neg_
 #pragma unroll
                     for (int s = 0; s < NR; ++s) prefetch_l2(gn + o[s]);
                 }
+                // per-tile phase tables, built while the loads are in flight
+                if (has_table) build_tables<NT>(tab, plan, plan.points[P.table_point], full, neg_dt, P.table_scale);
             } else if (kind == kOpCfg) {
                 if (smem_busy) __syncthreads();
                 if (op.perm >= 0) {
@@ -458,9 +454,22 @@ k_tile_pass(double2* __restrict__ psi, PlanDev plan, int pass_index, double neg_
                     tc[2] = tsw(op.swc23 & 0xffffu);
                     tc[3] = tsw(op.swc23 >> 16);
                 }
+                const double2* E0 = nullptr;
+                const double2* E1 = nullptr;
+                const double2* E2 = nullptr;
+                uint32_t fo[3][4];
+                if (n_fac > 0) {
 #pragma unroll
-                for (int f = 0; f < 3; ++f)
-                    if (f < n_fac) fb[f] = s_pl[f][tb & 63u] ^ s_ph[f][tb >> 6];
+                    for (int f = 0; f < 3; ++f) {
+                        if (f < n_fac) fb[f] = s_pl[f][tb & 63u] ^ s_ph[f][tb >> 6];
+                        const uint64_t pk = f < n_fac ? op.c_off[f] : 0ull;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) fo[f][j] = static_cast<uint32_t>(pk >> (16 * j)) & 0xffffu;
+                    }
+                    E0 = reinterpret_cast<const double2*>(tab + pt.fac_coff[0]);
+                    if (n_fac > 1) E1 = reinterpret_cast<const double2*>(tab + pt.fac_coff[1]);
+                    if (n_fac > 2) E2 = reinterpret_cast<const double2*>(tab + pt.fac_coff[2]);
+                }
                 // ---- direct-mode terms (few) with the tile's outer sign folded in
                 const bool direct = !table && n_terms > 0 && n_terms <= 8;
                 double dc[8];
@@ -492,17 +501,23 @@ k_tile_pass(double2* __restrict__ psi, PlanDev plan, int pass_index, double neg_
                     if (q & 2u) a = make_double2(-a.x, -a.y);
                     if (q & 1u) a = make_double2(-a.y, a.x);
                     if (n_fac > 0) {
-                        double2 e = make_double2(1.0, 0.0);
+                        uint32_t x0 = fb[0], x1 = fb[1], x2 = fb[2];
 #pragma unroll
-                        for (int f = 0; f < 3; ++f) {
-                            if (f < n_fac) {
-                                uint32_t x = fb[f];
-#pragma unroll
-                                for (int j = 0; j < R; ++j)
-                                    if ((s2 >> j) & 1) x ^= static_cast<uint32_t>(op.c_off[f] >> (16 * j)) & 0xffffu;
-                                const double2 t = reinterpret_cast<const double2*>(tab + pt.fac_coff[f])[x];
-                                e = f == 0 ? t : make_double2(e.x * t.x - e.y * t.y, e.x * t.y + e.y * t.x);
+                        for (int j = 0; j < R; ++j) {
+                            if ((s2 >> j) & 1) {
+                                x0 ^= fo[0][j];
+                                x1 ^= fo[1][j];
+                                x2 ^= fo[2][j];
                             }
+                        }
+                        double2 e = E0[x0];
+                        if (E1) {
+                            const double2 t1 = E1[x1];
+                            e = make_double2(e.x * t1.x - e.y * t1.y, e.x * t1.y + e.y * t1.x);
+                        }
+                        if (E2) {
+                            const double2 t2 = E2[x2];
+                            e = make_double2(e.x * t2.x - e.y * t2.y, e.x * t2.y + e.y * t2.x);
                         }
                         a = make_double2(a.x * e.x - a.y * e.y, a.x * e.y + a.y * e.x);
                     } else if (n_terms > 0) {
@@ -593,7 +608,8 @@ void launch_kr(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& p
 template <int K>
 void launch_k(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& plan, double dt, uint64_t rank_bits) {
     // R = 4 register coordinates (16 amplitudes per thread). R = 3 with twice the
-    // threads spills at the 2-CTA/SM register budget (measured).
+    // threads spills at the 2-CTA/SM register budget and measured 1.5x slower
+    // per step (profiles/r1_notes.md).
     if (ph.rbits != 4 && K >= 4) throw std::invalid_argument("tile pass: unsupported register config");
     launch_kr<K, 4>(s, ph, pass_index, plan, dt, rank_bits);
 }

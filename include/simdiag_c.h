@@ -232,10 +232,31 @@ sd_status sd_plan_kernel_times(sd_plan* p, double* ms_by_class, uint64_t* launch
 /* Multi-rank exchange (NCCL over NVLink; one process per GPU)          */
 /* ------------------------------------------------------------------ */
 
+/* The state shards on the top log2(world) qubits (sd_state_create_shard).
+ * Diagonals, S/CZ layers and CNOTs with a global control run without
+ * communication; a Hadamard or CNOT target on a global qubit is handled by a
+ * qubit remap that the planner inserts between pass segments: the pass in
+ * front of it stores out of place through a local bit permutation, then the
+ * ranks swap chunks (no reference counterpart -- the reference has
+ * no distributed state). */
+
 /* 128-byte ncclUniqueId, produced on rank 0 and broadcast by the caller. */
 sd_status sd_comm_unique_id(unsigned char id[128]);
-/* Bind a shard state to an NCCL communicator over all `world` ranks. */
+/* Bind a shard state to an NCCL communicator over all `world` ranks
+ * (libnccl.so.2 is resolved at run time). sd_evolve then performs the remaps
+ * with grouped ncclSend/ncclRecv on the state's stream. */
 sd_status sd_state_attach_comm(sd_state* s, const unsigned char id[128]);
+/* Restore the canonical layout (logical qubit q at physical bit q) of a
+ * relabelled state; collective over the communicator for sharded states.
+ * sd_state_download does this implicitly. */
+sd_status sd_state_canonicalize(sd_state* s);
+
+/* Several shards driven by ONE process (devices[r] may repeat, e.g. virtual
+ * shards on one GPU): remaps are device copies between the shards' buffers,
+ * with exactly the NCCL path's routing. plans[r] must be created on shard r. */
+sd_status sd_state_create_local_shards(int n_qubits, int world, const int* devices, sd_state** out);
+sd_status sd_evolve_local(sd_plan* const* plans, int world, double dt, int n_steps);
+sd_status sd_local_canonicalize(sd_state* const* shards, int world);
 
 #ifdef __cplusplus
 }

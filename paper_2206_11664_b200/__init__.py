@@ -13,10 +13,12 @@ from .simdiag import (  # noqa: F401
     DiagonalGroup,
     EvolutionPlan,
     Hamiltonian,
+    LocalShards,
     PauliString,
     StateVector,
     TrotterPlan,
     WeightedTerm,
+    comm_unique_id,
     commutes,
     diagonalize_group,
     evolve_grouped,
@@ -32,4 +34,5 @@ __all__ = [
     "CliffordCircuit", "CommutingGroup", "DiagonalGroup", "EvolutionPlan", "Hamiltonian",
     "PauliString", "StateVector", "TrotterPlan", "WeightedTerm", "commutes", "diagonalize_group",
     "evolve_grouped", "fidelity", "greedy_partition", "norm", "partition_and_diagonalize", "models",
+    "LocalShards", "comm_unique_id", "plan_preview",
 ]

@@ -7,10 +7,12 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <numeric>
 
 #include "../plan/lower.hpp"
+#include "exchange.hpp"
 #include "../plan/planner.hpp"
 #include "guard.hpp"
 
@@ -22,15 +24,27 @@ struct sd_state {
     sdb::StateImpl impl;
 };
 
+// One planned Trotter step for a given starting layout (segments, remaps),
+// lowered and uploaded. Plans are cached per layout: the layout sequence of a
+// sharded evolution cycles after a few steps.
+struct StepExec {
+    sdb::ShardedStep ss;
+    std::vector<sdb::PassDev> host_passes;
+    std::vector<int> pass_class;  // 0 fused, 1 diagonal-only
+    std::vector<int> seg_first, seg_count;
+    sdb::PlanDev dev{};
+    void* dev_block = nullptr;
+    std::string program;
+};
+
 struct sd_plan {
     sd_state* state = nullptr;
     std::vector<sdb::GroupSpec> groups;
     sd_plan_options opts{};
-    sdb::StepPlan step;
-    std::vector<sdb::PassDev> host_passes;
-    std::vector<int> pass_class;  // 0 fused, 1 diagonal-only
-    sdb::PlanDev dev{};
-    void* dev_block = nullptr;    // one allocation backing every PlanDev array
+    std::vector<sdb::Op> ops;  // one Trotter step (gate level)
+    int k = 12;
+    std::map<std::vector<int>, std::unique_ptr<StepExec>> steps;
+    StepExec* first = nullptr;  // plan of the canonical (identity) layout
     bool profiling = false;
     double ms[4] = {0, 0, 0, 0};
     uint64_t launches[4] = {0, 0, 0, 0};
@@ -38,10 +52,7 @@ struct sd_plan {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
     std::vector<int> ev_class;
     size_t ev_used = 0;
-    cudaGraphExec_t graph = nullptr;
-    double graph_dt = 0.0;
     int n_ref_sweeps = 0;
-    std::string program;
 };
 
 namespace {
@@ -160,14 +171,13 @@ void clifford_unfused(sdb::StateImpl& s, const sdb::GroupSpec& g, bool inverse) 
 }
 
 // ---------------------------------------------------------------- plan build
-constexpr int kTableThreshold = 8;  // terms per POINT stage above which the WHT table is used
+constexpr int kTableThreshold = 8;  // terms per POINT stage above which a per-tile table is used
 
-void build_device_plan(sd_plan& p) {
+void upload_step(sd_plan& p, StepExec& E, const sdb::StepPlan& combined) {
     sdb::StateImpl& s = p.state->impl;
-    sdb::HostPlanArrays A = sdb::lower_plan(p.step, s.n_local, kTableThreshold, 4);
-    p.pass_class = A.pass_class;
-
-    p.program = sdb::describe_program(A);
+    sdb::HostPlanArrays A = sdb::lower_plan(combined, s.n_local, kTableThreshold, 4);
+    E.pass_class = A.pass_class;
+    E.program = sdb::describe_program(A);
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t sizes[] = {
         al(std::max<size_t>(1, A.passes.size()) * sizeof(sdb::PassDev)),
@@ -186,31 +196,58 @@ void build_device_plan(sd_plan& p) {
     size_t total = 0;
     for (size_t v : sizes) total += v;
     SDB_CUDA(cudaSetDevice(s.device));
-    if (p.dev_block) SDB_CUDA(cudaFree(p.dev_block));
-    SDB_CUDA(cudaMalloc(&p.dev_block, total));
+    SDB_CUDA(cudaMalloc(&E.dev_block, total));
     std::vector<unsigned char> host(total, 0);
     size_t off = 0;
     int slot = 0;
     auto put = [&](const void* src, size_t bytes) {
         if (bytes) std::memcpy(host.data() + off, src, bytes);
-        void* dptr = static_cast<unsigned char*>(p.dev_block) + off;
+        void* dptr = static_cast<unsigned char*>(E.dev_block) + off;
         off += sizes[slot++];
         return dptr;
     };
-    p.dev.passes = static_cast<const sdb::PassDev*>(put(A.passes.data(), A.passes.size() * sizeof(sdb::PassDev)));
-    p.dev.ops = static_cast<const sdb::MicroOpDev*>(put(A.ops.data(), A.ops.size() * sizeof(sdb::MicroOpDev)));
-    p.dev.perms = static_cast<const sdb::PermDev*>(put(A.perms.data(), A.perms.size() * sizeof(sdb::PermDev)));
-    p.dev.points = static_cast<const sdb::PointDev*>(put(A.points.data(), A.points.size() * sizeof(sdb::PointDev)));
-    p.dev.segs = static_cast<const sdb::SegDev*>(put(A.segs.data(), A.segs.size() * sizeof(sdb::SegDev)));
-    p.dev.lo_pairs = static_cast<const uint32_t*>(put(A.lo_pairs.data(), A.lo_pairs.size() * sizeof(uint32_t)));
-    p.dev.oo_pairs = static_cast<const uint64_t*>(put(A.oo_pairs.data(), A.oo_pairs.size() * 8));
-    p.dev.qt_words = static_cast<const uint64_t*>(put(A.qt_words.data(), A.qt_words.size() * 8));
-    p.dev.cfg_tb = static_cast<const sdb::CfgThreadDev*>(put(A.cfg_tb.data(), A.cfg_tb.size() * sizeof(sdb::CfgThreadDev)));
-    p.dev.term_hmask = static_cast<const uint64_t*>(put(A.term_hmask.data(), A.term_hmask.size() * 8));
-    p.dev.term_lmask = static_cast<const uint32_t*>(put(A.term_lmask.data(), A.term_lmask.size() * 4));
-    p.dev.term_coeffs = static_cast<const double*>(put(A.term_coeffs.data(), A.term_coeffs.size() * 8));
-    SDB_CUDA(cudaMemcpy(p.dev_block, host.data(), total, cudaMemcpyHostToDevice));
-    p.host_passes = std::move(A.passes);
+    E.dev.passes = static_cast<const sdb::PassDev*>(put(A.passes.data(), A.passes.size() * sizeof(sdb::PassDev)));
+    E.dev.ops = static_cast<const sdb::MicroOpDev*>(put(A.ops.data(), A.ops.size() * sizeof(sdb::MicroOpDev)));
+    E.dev.perms = static_cast<const sdb::PermDev*>(put(A.perms.data(), A.perms.size() * sizeof(sdb::PermDev)));
+    E.dev.points = static_cast<const sdb::PointDev*>(put(A.points.data(), A.points.size() * sizeof(sdb::PointDev)));
+    E.dev.segs = static_cast<const sdb::SegDev*>(put(A.segs.data(), A.segs.size() * sizeof(sdb::SegDev)));
+    E.dev.lo_pairs = static_cast<const uint32_t*>(put(A.lo_pairs.data(), A.lo_pairs.size() * sizeof(uint32_t)));
+    E.dev.oo_pairs = static_cast<const uint64_t*>(put(A.oo_pairs.data(), A.oo_pairs.size() * 8));
+    E.dev.qt_words = static_cast<const uint64_t*>(put(A.qt_words.data(), A.qt_words.size() * 8));
+    E.dev.cfg_tb = static_cast<const sdb::CfgThreadDev*>(put(A.cfg_tb.data(), A.cfg_tb.size() * sizeof(sdb::CfgThreadDev)));
+    E.dev.term_hmask = static_cast<const uint64_t*>(put(A.term_hmask.data(), A.term_hmask.size() * 8));
+    E.dev.term_lmask = static_cast<const uint32_t*>(put(A.term_lmask.data(), A.term_lmask.size() * 4));
+    E.dev.term_coeffs = static_cast<const double*>(put(A.term_coeffs.data(), A.term_coeffs.size() * 8));
+    SDB_CUDA(cudaMemcpy(E.dev_block, host.data(), total, cudaMemcpyHostToDevice));
+    E.host_passes = std::move(A.passes);
+}
+
+StepExec& step_for(sd_plan& p, const std::vector<int>& layout) {
+    auto it = p.steps.find(layout);
+    if (it != p.steps.end()) return *it->second;
+    sdb::StateImpl& s = p.state->impl;
+    auto E = std::make_unique<StepExec>();
+    E->ss = sdb::plan_sharded_step(p.ops, p.groups, s.n_local, p.k, 3, layout);
+    sdb::StepPlan combined;
+    combined.tile_qubits = p.k;
+    for (const sdb::Segment& sg : E->ss.segs) {
+        E->seg_first.push_back(static_cast<int>(combined.passes.size()));
+        E->seg_count.push_back(static_cast<int>(sg.plan.passes.size()));
+        for (const sdb::PassPlan& pp : sg.plan.passes) combined.passes.push_back(pp);
+    }
+    upload_step(p, *E, combined);
+    if (E->ss.n_exchanges > 0 && !s.xbuf) {
+        SDB_CUDA(cudaSetDevice(s.device));
+        cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&s.xbuf), 16 * s.amps_count());
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            throw sdb::OomError("cannot allocate the exchange buffer");
+        }
+        s.xbuf_amps = s.amps_count();
+    }
+    StepExec& ref = *E;
+    p.steps.emplace(layout, std::move(E));
+    return ref;
 }
 
 void plan_build(sd_plan& p) {
@@ -220,11 +257,11 @@ void plan_build(sd_plan& p) {
     p.n_ref_sweeps = static_cast<int>(std::lround(sdb::reference_sweeps(p.groups, order)));
     if (!p.opts.fuse) return;
     int k = p.opts.tile_qubits > 0 ? p.opts.tile_qubits : 12;
-    k = std::min({k, sdb::max_tile_qubits(), s.n_local});
-    const auto ops = sdb::step_ops(p.groups, s.n, order, std::max(1, k - 3));
-    p.step = sdb::plan_step(ops, p.groups, s.n_local, k, 3, s.phys_of);
-    p.step.ref_sweeps = sdb::reference_sweeps(p.groups, order);
-    build_device_plan(p);
+    p.k = std::min({k, sdb::max_tile_qubits(), s.n_local});
+    p.ops = sdb::step_ops(p.groups, s.n, order, std::max(1, p.k - 3));
+    std::vector<int> ident(s.n);
+    std::iota(ident.begin(), ident.end(), 0);
+    p.first = &step_for(p, ident);
 }
 
 void record_start(sd_plan& p, int cls) {
@@ -259,17 +296,36 @@ void harvest(sd_plan& p) {
     p.ev_used = 0;
 }
 
-void run_step_fused(sd_plan& p, double dt) {
+void run_segment(sd_plan& p, StepExec& E, size_t seg, double dt) {
     sdb::StateImpl& s = p.state->impl;
     const uint64_t rank_bits = uint64_t(s.rank) << s.n_local;
     const double bytes = 2.0 * 16.0 * double(s.amps_count());
-    for (size_t i = 0; i < p.host_passes.size(); ++i) {
-        record_start(p, p.pass_class[i]);
-        sdb::launch_tile_pass(s, p.host_passes[i], static_cast<int>(i), p.dev, dt, rank_bits);
+    const bool exch = E.ss.segs[seg].exchange_after;
+    const int first = E.seg_first[seg], count = E.seg_count[seg];
+    for (int i = first; i < first + count; ++i) {
+        const bool to_buf = exch && i == first + count - 1;
+        record_start(p, E.pass_class[i]);
+        sdb::launch_tile_pass(s, E.host_passes[i], i, E.dev, dt, rank_bits, to_buf ? s.xbuf : nullptr);
         record_end(p, bytes);
         bump(s, s.amps_count(), s.amps_count());
         if (p.profiling && p.ev_used >= 4096) harvest(p);
     }
+}
+
+void run_step_fused(sd_plan& p, double dt) {
+    sdb::StateImpl& s = p.state->impl;
+    StepExec& E = step_for(p, s.phys_of);
+    for (size_t seg = 0; seg < E.ss.segs.size(); ++seg) {
+        run_segment(p, E, seg, dt);
+        if (E.ss.segs[seg].exchange_after) {
+            const double xb = 2.0 * 16.0 * double(s.amps_count()) *
+                              (1.0 - std::ldexp(1.0, -static_cast<int>(E.ss.segs[seg].ex.swaps.size())));
+            record_start(p, 2);
+            sdb::exchange_nccl(s, E.ss.segs[seg].ex);
+            record_end(p, xb);
+        }
+    }
+    s.phys_of = E.ss.phys_out;
 }
 
 void run_step_unfused(sd_plan& p, double dt) {
@@ -300,6 +356,126 @@ void evolve(sd_plan& p, double dt, int n_steps, bool wait) {
     }
     if (wait) SDB_CUDA(cudaStreamSynchronize(s.stream));
     harvest(p);
+}
+
+// Exchanges that bring a relabelled sharded layout back to the identity
+// (logical qubit q at physical bit q): (1) fix the set of global qubits,
+// (2) if the global qubits sit in the wrong order, swap them all out and back
+// in order. The remaining local permutation is done by permute_local().
+std::vector<sdb::ExchangeSpec> canonical_exchanges(std::vector<int>& L, int n_local) {
+    const int n = static_cast<int>(L.size());
+    const int g = n - n_local;
+    std::vector<sdb::ExchangeSpec> out;
+    auto apply = [&](const std::vector<int>& to_top, const std::vector<int>& incoming) {
+        // to_top: local qubits that leave (placed on T by sigma); incoming: global qubits, paired in order
+        const int gp = static_cast<int>(incoming.size());
+        const int t0 = n_local - gp;
+        sdb::ExchangeSpec ex;
+        ex.sigma.resize(n_local);
+        std::iota(ex.sigma.begin(), ex.sigma.end(), 0);
+        std::vector<int> at(n_local, -1);
+        for (int q = 0; q < n; ++q) {
+            if (L[q] < n_local) at[L[q]] = q;
+        }
+        // target slot of each leaving qubit: t0 + i; move it there by a transposition
+        for (int i = 0; i < gp; ++i) {
+            const int e = to_top[i];
+            const int pe = L[e], pt = t0 + i;
+            if (pe == pt) continue;
+            const int other = at[pt];
+            // compose the transposition (pe pt) into sigma (sigma maps original bit -> new bit)
+            for (int b = 0; b < n_local; ++b) {
+                if (ex.sigma[b] == pe) ex.sigma[b] = pt;
+                else if (ex.sigma[b] == pt) ex.sigma[b] = pe;
+            }
+            L[e] = pt;
+            if (other >= 0) L[other] = pe;
+            at[pt] = e;
+            at[pe] = other;
+        }
+        for (int i = 0; i < gp; ++i) {
+            const int qi = incoming[i], qe = to_top[i];
+            ex.swaps.emplace_back(L[qi], t0 + i);
+            L[qe] = L[qi];
+            L[qi] = t0 + i;
+        }
+        out.push_back(std::move(ex));
+    };
+    std::vector<int> W, V;
+    for (int q = 0; q < n; ++q) {
+        if (q >= n_local && L[q] < n_local) W.push_back(q);
+        if (q < n_local && L[q] >= n_local) V.push_back(q);
+    }
+    if (!W.empty()) {
+        std::sort(V.begin(), V.end(), [&](int a, int b) { return L[a] < L[b]; });
+        apply(W, V);
+    }
+    bool ordered = true;
+    for (int q = n_local; q < n; ++q) ordered &= L[q] == q;
+    if (!ordered && g > 0) {
+        // swap every global bit out (its current holder comes local)...
+        std::vector<int> out_q, in_q;
+        std::vector<int> at(n, -1);
+        for (int q = 0; q < n; ++q) at[L[q]] = q;
+        for (int i = 0; i < g; ++i) {
+            in_q.push_back(at[n_local + i]);
+            out_q.push_back(at[n_local - g + i]);
+        }
+        apply(out_q, in_q);
+        // ...and bring logical n_local+i back to global bit n_local+i
+        std::fill(at.begin(), at.end(), -1);
+        for (int q = 0; q < n; ++q) at[L[q]] = q;
+        out_q.clear();
+        in_q.clear();
+        for (int i = 0; i < g; ++i) {
+            out_q.push_back(n_local + i);
+            in_q.push_back(at[n_local + i]);
+        }
+        apply(out_q, in_q);
+    }
+    return out;
+}
+
+// state <- the state with its local physical bits permuted (new_pos[b]), via xbuf
+void permute_into_xbuf(sdb::StateImpl& s, const std::vector<int>& new_pos) {
+    if (!s.xbuf) {
+        SDB_CUDA(cudaMalloc(reinterpret_cast<void**>(&s.xbuf), 16 * s.amps_count()));
+        s.xbuf_amps = s.amps_count();
+    }
+    sdb::launch_permute_bits(s, s.amps, s.xbuf, new_pos.data(), s.n_local);
+}
+
+void permute_local(sdb::StateImpl& s) {
+    std::vector<int> new_pos(s.n_local);
+    bool ident = true;
+    for (int q = 0; q < s.n_local; ++q) {
+        if (s.phys_of[q] >= s.n_local) throw std::logic_error("permute_local: global qubits not canonical");
+        new_pos[s.phys_of[q]] = q;
+        ident &= s.phys_of[q] == q;
+    }
+    if (ident) return;
+    permute_into_xbuf(s, new_pos);
+    std::swap(s.amps, s.xbuf);
+    for (int q = 0; q < s.n_local; ++q) s.phys_of[q] = q;
+}
+
+void canonicalize_nccl(sdb::StateImpl& s) {
+    std::vector<int> L = s.phys_of;
+    const auto exs = canonical_exchanges(L, s.n_local);
+    for (const sdb::ExchangeSpec& ex : exs) {
+        permute_into_xbuf(s, ex.sigma);
+        sdb::exchange_nccl(s, ex);
+    }
+    s.phys_of = L;
+    permute_local(s);
+    SDB_CUDA(cudaStreamSynchronize(s.stream));
+}
+
+bool is_identity(const std::vector<int>& L) {
+    for (size_t q = 0; q < L.size(); ++q) {
+        if (L[q] != static_cast<int>(q)) return false;
+    }
+    return true;
 }
 
 }  // namespace
@@ -346,6 +522,10 @@ void sd_state_destroy(sd_state* h) {
     sdb::StateImpl& s = h->impl;
     cudaSetDevice(s.device);
     if (s.stream) cudaStreamSynchronize(s.stream);
+    try {
+        sdb::nccl_detach(s);
+    } catch (...) {
+    }
     if (s.amps) cudaFree(s.amps);
     if (s.xbuf) cudaFree(s.xbuf);
     if (s.reduce_buf) cudaFree(s.reduce_buf);
@@ -439,7 +619,12 @@ sd_status sd_state_download(sd_state* h, double* re_im, uint64_t n_amps) {
         sdb::StateImpl& s = st(h);
         require(re_im != nullptr, "null host buffer");
         require(n_amps == s.amps_count(), "download size does not match the shard");
-        require_identity_layout(s);
+        if (!is_identity(s.phys_of)) {
+            SDB_CUDA(cudaSetDevice(s.device));
+            if (s.world == 1) permute_local(s);
+            else if (s.nccl) canonicalize_nccl(s);  // collective: every rank downloads
+            else throw std::runtime_error("sharded state is relabelled: call sd_local_canonicalize first");
+        }
         SDB_CUDA(cudaSetDevice(s.device));
         SDB_CUDA(cudaMemcpyAsync(re_im, s.amps, n_amps * 16, cudaMemcpyDeviceToHost, s.stream));
         SDB_CUDA(cudaStreamSynchronize(s.stream));
@@ -610,8 +795,9 @@ void sd_plan_destroy(sd_plan* p) {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
     }
-    if (p->graph) cudaGraphExecDestroy(p->graph);
-    if (p->dev_block) cudaFree(p->dev_block);
+    for (auto& kv : p->steps) {
+        if (kv.second->dev_block) cudaFree(kv.second->dev_block);
+    }
     delete p;
 }
 
@@ -625,8 +811,12 @@ sd_status sd_plan_get_info(const sd_plan* p, sd_plan_info* o) {
                                                         ? 2 * p->groups.size() - 1
                                                         : p->groups.size());
         if (p->opts.fuse) {
-            o->n_passes_per_step = static_cast<int>(p->host_passes.size());
-            o->tile_qubits = p->step.tile_qubits;
+            // steady state: the plan of the current layout (identity until the first exchange)
+            auto it = p->steps.find(s.phys_of);
+            const StepExec* E = it != p->steps.end() ? it->second.get() : p->first;
+            o->n_passes_per_step = E->ss.n_passes;
+            o->n_exchanges_per_step = E->ss.n_exchanges;
+            o->tile_qubits = p->k;
             o->n_kernels_per_step = o->n_passes_per_step;
             o->bytes_per_step = 2.0 * 16.0 * double(s.amps_count()) * o->n_passes_per_step;
         } else {
@@ -634,15 +824,27 @@ sd_status sd_plan_get_info(const sd_plan* p, sd_plan_info* o) {
             o->n_kernels_per_step = 0;
             o->bytes_per_step = 2.0 * 16.0 * double(s.amps_count()) * p->n_ref_sweeps;
         }
-        o->n_exchanges_per_step = 0;
     });
 }
 
 sd_status sd_plan_describe(const sd_plan* p, char* buf, size_t cap, size_t* len) {
     return guard([&] {
         require(p != nullptr, "null plan");
-        sdb::write_text_out(p->opts.fuse ? sdb::describe(p->step) + p->program : std::string("unfused reference schedule\n"),
-                            buf, cap, len);
+        std::string txt = "unfused reference schedule\n";
+        if (p->opts.fuse) {
+            txt.clear();
+            const StepExec& E = *p->first;
+            for (size_t i = 0; i < E.ss.segs.size(); ++i) {
+                txt += "segment " + std::to_string(i) + ": " + sdb::describe(E.ss.segs[i].plan);
+                if (E.ss.segs[i].exchange_after) {
+                    txt += "  exchange swaps";
+                    for (auto [gb, lb] : E.ss.segs[i].ex.swaps) txt += " (" + std::to_string(gb) + "," + std::to_string(lb) + ")";
+                    txt += "\n";
+                }
+            }
+            txt += E.program;
+        }
+        sdb::write_text_out(txt, buf, cap, len);
     });
 }
 
@@ -656,6 +858,7 @@ sd_status sd_plan_preview(int n, int world, const sd_group_desc* groups, size_t 
         else sd_plan_options_default(&o);
         require(o.order == 1 || o.order == 2, "trotter order must be 1 or 2");
         const int n_local = n - std::countr_zero(static_cast<unsigned>(world));
+        require(n_local >= 1, "too many ranks for this state");
         std::vector<sdb::GroupSpec> gs;
         for (size_t i = 0; i < n_groups; ++i) gs.push_back(spec_of(groups[i]));
         std::vector<int> phys(n);
@@ -663,18 +866,37 @@ sd_status sd_plan_preview(int n, int world, const sd_group_desc* groups, size_t 
         int k = o.tile_qubits > 0 ? o.tile_qubits : 12;
         k = std::min({k, sdb::max_tile_qubits(), n_local});
         const auto ops = sdb::step_ops(gs, n, o.order, std::max(1, k - 3));
-        sdb::StepPlan sp = sdb::plan_step(ops, gs, n_local, k, 3, phys);
+        // steps until the layout repeats (the executor caches one plan per layout)
+        std::vector<sdb::ShardedStep> steps;
+        std::vector<std::vector<int>> seen;
+        int cycle_start = 0;
+        for (int it = 0; it < 16; ++it) {
+            auto f = std::find(seen.begin(), seen.end(), phys);
+            if (f != seen.end()) {
+                cycle_start = static_cast<int>(f - seen.begin());
+                break;
+            }
+            seen.push_back(phys);
+            steps.push_back(sdb::plan_sharded_step(ops, gs, n_local, k, 3, phys));
+            phys = steps.back().phys_out;
+        }
         if (info) {
+            const sdb::ShardedStep& st = steps[static_cast<size_t>(cycle_start)];
             std::memset(info, 0, sizeof(*info));
-            info->n_passes_per_step = static_cast<int>(sp.passes.size());
+            info->n_passes_per_step = st.n_passes;
             info->n_ref_sweeps_per_step = static_cast<int>(std::lround(sdb::reference_sweeps(gs, o.order)));
             info->n_group_applications =
                 static_cast<int>(o.order == 2 && gs.size() > 1 ? 2 * gs.size() - 1 : gs.size());
-            info->tile_qubits = sp.tile_qubits;
-            info->n_kernels_per_step = info->n_passes_per_step;
-            info->bytes_per_step = 2.0 * 16.0 * std::ldexp(1.0, n_local) * info->n_passes_per_step;
+            info->tile_qubits = k;
+            info->n_kernels_per_step = st.n_passes;
+            info->n_exchanges_per_step = st.n_exchanges;
+            info->bytes_per_step = 2.0 * 16.0 * std::ldexp(1.0, n_local) * st.n_passes;
         }
-        sdb::write_text_out(sdb::describe_json(sp), json, cap, len);
+        std::string js = "{\"n_local\":" + std::to_string(n_local) + ",\"cycle_start\":" +
+                         std::to_string(cycle_start) + ",\"steps\":[";
+        for (size_t i = 0; i < steps.size(); ++i) js += (i ? "," : "") + sdb::describe_sharded_json(steps[i]);
+        js += "]}";
+        sdb::write_text_out(js, json, cap, len);
     });
 }
 
@@ -719,16 +941,101 @@ sd_status sd_plan_kernel_times(sd_plan* p, double* ms, uint64_t* launches, doubl
 
 sd_status sd_comm_unique_id(unsigned char id[128]) {
     return guard([&] {
-        (void)id;
-        throw std::runtime_error("NCCL exchange not built in this version");
+        require(id != nullptr, "null id buffer");
+        sdb::nccl_unique_id(id);
     });
 }
 
 sd_status sd_state_attach_comm(sd_state* h, const unsigned char id[128]) {
     return guard([&] {
-        (void)h;
-        (void)id;
-        throw std::runtime_error("NCCL exchange not built in this version");
+        sdb::StateImpl& s = st(h);
+        require(id != nullptr, "null id");
+        sdb::nccl_attach(s, id);
+    });
+}
+
+sd_status sd_state_canonicalize(sd_state* h) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        SDB_CUDA(cudaSetDevice(s.device));
+        if (is_identity(s.phys_of)) return;
+        if (s.world == 1) permute_local(s);
+        else canonicalize_nccl(s);
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
+sd_status sd_state_create_local_shards(int n, int world, const int* devices, sd_state** out) {
+    return guard([&] {
+        require(out != nullptr, "out is null");
+        require(world >= 1 && (world & (world - 1)) == 0, "world size must be a power of two");
+        for (int r = 0; r < world; ++r) out[r] = nullptr;
+        for (int r = 0; r < world; ++r) {
+            const sd_status st = sd_state_create_shard(n, r, world, devices ? devices[r] : 0, &out[r]);
+            if (st != SD_OK) {
+                for (int q = 0; q < r; ++q) sd_state_destroy(out[q]);
+                throw std::runtime_error(sd_last_error());
+            }
+        }
+    });
+}
+
+sd_status sd_evolve_local(sd_plan* const* plans, int world, double dt, int n_steps) {
+    return guard([&] {
+        require(plans != nullptr && world >= 1, "null plan array");
+        require(std::isfinite(dt), "plan needs finite total_time");
+        if (n_steps < 0) throw std::invalid_argument("plan needs n_steps >= 0");
+        std::vector<sdb::StateImpl*> shards(world);
+        for (int r = 0; r < world; ++r) {
+            require(plans[r] != nullptr && plans[r]->opts.fuse, "local evolution needs fused plans");
+            shards[r] = &plans[r]->state->impl;
+            require(shards[r]->rank == r && shards[r]->world == world, "plans[r] must drive shard r of `world`");
+        }
+        for (int step = 0; step < n_steps; ++step) {
+            std::vector<StepExec*> E(world);
+            for (int r = 0; r < world; ++r) {
+                require(shards[r]->phys_of == shards[0]->phys_of, "shards disagree on the layout");
+                SDB_CUDA(cudaSetDevice(shards[r]->device));
+                E[r] = &step_for(*plans[r], shards[r]->phys_of);
+            }
+            for (size_t seg = 0; seg < E[0]->ss.segs.size(); ++seg) {
+                for (int r = 0; r < world; ++r) {
+                    SDB_CUDA(cudaSetDevice(shards[r]->device));
+                    run_segment(*plans[r], *E[r], seg, dt);
+                }
+                if (E[0]->ss.segs[seg].exchange_after) sdb::exchange_local(shards, E[0]->ss.segs[seg].ex);
+            }
+            for (int r = 0; r < world; ++r) shards[r]->phys_of = E[r]->ss.phys_out;
+        }
+        for (int r = 0; r < world; ++r) {
+            SDB_CUDA(cudaSetDevice(shards[r]->device));
+            SDB_CUDA(cudaStreamSynchronize(shards[r]->stream));
+            harvest(*plans[r]);
+        }
+    });
+}
+
+sd_status sd_local_canonicalize(sd_state* const* hs, int world) {
+    return guard([&] {
+        require(hs != nullptr && world >= 1, "null shard array");
+        std::vector<sdb::StateImpl*> shards(world);
+        for (int r = 0; r < world; ++r) shards[r] = &st(hs[r]);
+        std::vector<int> L = shards[0]->phys_of;
+        if (is_identity(L)) return;
+        const auto exs = canonical_exchanges(L, shards[0]->n_local);
+        for (const sdb::ExchangeSpec& ex : exs) {
+            for (sdb::StateImpl* s : shards) {
+                SDB_CUDA(cudaSetDevice(s->device));
+                permute_into_xbuf(*s, ex.sigma);
+            }
+            sdb::exchange_local(shards, ex);
+        }
+        for (sdb::StateImpl* s : shards) {
+            SDB_CUDA(cudaSetDevice(s->device));
+            s->phys_of = L;
+            permute_local(*s);
+            SDB_CUDA(cudaStreamSynchronize(s->stream));
+        }
     });
 }
 

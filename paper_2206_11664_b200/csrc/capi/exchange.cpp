@@ -1,0 +1,192 @@
+// Qubit-remap exchanges of a sharded state (planner.hpp
+// ExchangeSpec). The pass in front of an exchange has already stored this
+// rank's shard through sigma into the exchange buffer B (s.xbuf), so the top
+// g' local bits T hold the qubits that leave. Rank r then, for every chunk
+// index c of those bits, sends B[c] to the peer whose swapped global bits are
+// c and receives that peer's chunk into A[c] (A = s.amps); c == own bits is a
+// device-local copy. Two transports share this routing:
+//   * NCCL (one process per GPU): grouped ncclSend/ncclRecv on the state's
+//     stream. libnccl.so.2 is resolved at run time (dlopen, reusing the copy
+//     torch has already loaded) so the library has no link-time NCCL
+//     dependency and single-GPU users never need it;
+//   * local (several shards driven by one process, e.g. virtual shards on one
+//     GPU for tests): cudaMemcpyPeerAsync between the shards' buffers.
+#include <cuda_runtime_api.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <bit>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "../internal.hpp"
+#include "../plan/planner.hpp"
+
+namespace sdb {
+
+namespace {
+
+struct NcclApi {
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
+    ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    const char* (*errorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    static std::string err;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            err = std::string("cannot load libnccl.so.2: ") + dlerror();
+            return;
+        }
+        auto sym = [&](auto& fn, const char* name) {
+            fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+            if (!fn) err = std::string("libnccl.so.2 lacks ") + name;
+        };
+        sym(api.getUniqueId, "ncclGetUniqueId");
+        sym(api.commInitRank, "ncclCommInitRank");
+        sym(api.commDestroy, "ncclCommDestroy");
+        sym(api.groupStart, "ncclGroupStart");
+        sym(api.groupEnd, "ncclGroupEnd");
+        sym(api.send, "ncclSend");
+        sym(api.recv, "ncclRecv");
+        sym(api.allReduce, "ncclAllReduce");
+        sym(api.errorString, "ncclGetErrorString");
+    });
+    if (!err.empty()) throw NcclError(err);
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) {
+        const NcclApi& a = nccl();
+        throw NcclError(std::string(what) + ": " + a.errorString(r));
+    }
+}
+
+// bits of rank r at the swapped global positions, packed (bit i <-> swap i)
+uint32_t swapped_bits(uint64_t r, int n_local, const ExchangeSpec& ex) {
+    uint32_t c = 0;
+    for (size_t i = 0; i < ex.swaps.size(); ++i) {
+        if ((r >> (ex.swaps[i].first - n_local)) & 1ull) c |= 1u << i;
+    }
+    return c;
+}
+
+uint64_t with_bits(uint64_t r, int n_local, const ExchangeSpec& ex, uint32_t c) {
+    for (size_t i = 0; i < ex.swaps.size(); ++i) {
+        const uint64_t b = 1ull << (ex.swaps[i].first - n_local);
+        r = ((c >> i) & 1u) ? (r | b) : (r & ~b);
+    }
+    return r;
+}
+
+void check_spec(const StateImpl& s, const ExchangeSpec& ex) {
+    const int gp = static_cast<int>(ex.swaps.size());
+    for (int i = 0; i < gp; ++i) {
+        if (ex.swaps[i].second != s.n_local - gp + i || ex.swaps[i].first < s.n_local || ex.swaps[i].first >= s.n) {
+            throw std::logic_error("exchange: swaps must pair global bits with the top local bits");
+        }
+    }
+}
+
+}  // namespace
+
+void nccl_unique_id(unsigned char out[128]) {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    nccl_check(nccl().getUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out, &id, sizeof(id));
+}
+
+void nccl_attach(StateImpl& s, const unsigned char id[128]) {
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    SDB_CUDA(cudaSetDevice(s.device));
+    ncclComm_t comm = nullptr;
+    nccl_check(nccl().commInitRank(&comm, s.world, uid, s.rank), "ncclCommInitRank");
+    if (s.nccl) nccl().commDestroy(static_cast<ncclComm_t>(s.nccl));
+    s.nccl = comm;
+    if (!s.reduce_buf) SDB_CUDA(cudaMalloc(reinterpret_cast<void**>(&s.reduce_buf), 148 * 16 * 16));
+}
+
+void nccl_detach(StateImpl& s) {
+    if (s.nccl) {
+        nccl().commDestroy(static_cast<ncclComm_t>(s.nccl));
+        s.nccl = nullptr;
+    }
+}
+
+double nccl_sum(StateImpl& s, double v) {
+    if (!s.nccl) throw std::runtime_error("sharded state has no communicator (sd_state_attach_comm)");
+    double* d = s.reduce_buf;
+    SDB_CUDA(cudaMemcpyAsync(d, &v, sizeof(double), cudaMemcpyHostToDevice, s.stream));
+    nccl_check(nccl().allReduce(d, d, 1, ncclDouble, ncclSum, static_cast<ncclComm_t>(s.nccl), s.stream),
+               "ncclAllReduce");
+    SDB_CUDA(cudaMemcpyAsync(&v, d, sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+    SDB_CUDA(cudaStreamSynchronize(s.stream));
+    return v;
+}
+
+void exchange_nccl(StateImpl& s, const ExchangeSpec& ex) {
+    if (!s.nccl) throw std::runtime_error("sharded state has no communicator (sd_state_attach_comm)");
+    check_spec(s, ex);
+    const int gp = static_cast<int>(ex.swaps.size());
+    const uint64_t chunk = uint64_t(1) << (s.n_local - gp);  // amplitudes per chunk
+    const uint32_t own = swapped_bits(static_cast<uint64_t>(s.rank), s.n_local, ex);
+    const NcclApi& a = nccl();
+    auto comm = static_cast<ncclComm_t>(s.nccl);
+    nccl_check(a.groupStart(), "ncclGroupStart");
+    for (uint32_t c = 0; c < (1u << gp); ++c) {
+        if (c == own) continue;
+        const int peer = static_cast<int>(with_bits(static_cast<uint64_t>(s.rank), s.n_local, ex, c));
+        nccl_check(a.send(s.xbuf + 2 * chunk * c, 2 * chunk, ncclDouble, peer, comm, s.stream), "ncclSend");
+        nccl_check(a.recv(s.amps + 2 * chunk * c, 2 * chunk, ncclDouble, peer, comm, s.stream), "ncclRecv");
+    }
+    nccl_check(a.groupEnd(), "ncclGroupEnd");
+    SDB_CUDA(cudaMemcpyAsync(s.amps + 2 * chunk * own, s.xbuf + 2 * chunk * own, 16 * chunk,
+                             cudaMemcpyDeviceToDevice, s.stream));
+}
+
+void exchange_local(const std::vector<StateImpl*>& shards, const ExchangeSpec& ex) {
+    const int world = static_cast<int>(shards.size());
+    StateImpl& s0 = *shards[0];
+    check_spec(s0, ex);
+    const int gp = static_cast<int>(ex.swaps.size());
+    const uint64_t chunk = uint64_t(1) << (s0.n_local - gp);
+    for (StateImpl* s : shards) {
+        SDB_CUDA(cudaSetDevice(s->device));
+        SDB_CUDA(cudaStreamSynchronize(s->stream));
+    }
+    for (int r = 0; r < world; ++r) {
+        StateImpl& src = *shards[r];
+        const uint32_t own = swapped_bits(static_cast<uint64_t>(r), src.n_local, ex);
+        for (uint32_t c = 0; c < (1u << gp); ++c) {
+            const int peer = static_cast<int>(with_bits(static_cast<uint64_t>(r), src.n_local, ex, c));
+            StateImpl& dst = *shards[peer];
+            // B_r[c] -> A_peer[own]: the peer receives rank r's chunk at r's swapped bits
+            SDB_CUDA(cudaSetDevice(src.device));
+            SDB_CUDA(cudaMemcpyPeerAsync(dst.amps + 2 * chunk * own, dst.device, src.xbuf + 2 * chunk * c,
+                                         src.device, 16 * chunk, src.stream));
+        }
+    }
+    for (StateImpl* s : shards) {
+        SDB_CUDA(cudaSetDevice(s->device));
+        SDB_CUDA(cudaStreamSynchronize(s->stream));
+    }
+}
+
+}  // namespace sdb

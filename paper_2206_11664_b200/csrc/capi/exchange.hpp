@@ -1,0 +1,21 @@
+// Qubit-remap exchanges between the shards of a state (exchange.cpp).
+#pragma once
+
+#include <vector>
+
+#include "../internal.hpp"
+#include "../plan/planner.hpp"
+
+namespace sdb {
+
+void nccl_unique_id(unsigned char out[128]);
+void nccl_attach(StateImpl& s, const unsigned char id[128]);
+void nccl_detach(StateImpl& s);
+// sum of v over all ranks of the state's communicator
+double nccl_sum(StateImpl& s, double v);
+// B = s.xbuf (already stored through sigma) -> A = s.amps, stream-ordered
+void exchange_nccl(StateImpl& s, const ExchangeSpec& ex);
+// same routing for shards driven by one process (shards[r] = rank r)
+void exchange_local(const std::vector<StateImpl*>& shards, const ExchangeSpec& ex);
+
+}  // namespace sdb

@@ -235,7 +235,8 @@ constexpr int kTbaseChunks = 4;  // outer bits covered by the tile-base tables: 
 
 template <int K, int RB>
 __global__ void __launch_bounds__(Cfg<K, RB>::NT, Cfg<K, RB>::MINB)
-k_tile_pass(double2* __restrict__ psi, PlanDev plan, int pass_index, double neg_dt, uint64_t rank_bits,
+k_tile_pass(const double2* __restrict__ psi, double2* __restrict__ out, PlanDev plan, int pass_index, double neg_dt,
+            uint64_t rank_bits,
             uint64_t n_tiles) {
     using C = Cfg<K, RB>;
     constexpr int R = C::R, NR = C::NR, NT = C::NT, N = C::N, LO = C::LO, HI = C::HI;
@@ -250,9 +251,18 @@ k_tile_pass(double2* __restrict__ psi, PlanDev plan, int pass_index, double neg_
     double2* const buf = reinterpret_cast<double2*>(smem_raw);            // transpose buffer
     double* const tab = reinterpret_cast<double*>(buf + N);               // angle table (if any)
     const int tab_words = P.tab_words;
+    // The micro-ops are staged in shared memory (the planner caps a pass's
+    // length); per-thread config bases and QT tables are read through L1
+    // (a few words per thread per tile).
     MicroOpDev* const s_ops = reinterpret_cast<MicroOpDev*>(tab + tab_words);
-    uint32_t* const s_cfg = reinterpret_cast<uint32_t*>(s_ops + n_ops);   // n_cfg x NT
-    uint32_t* const s_qt = s_cfg + n_cfg * NT;                            // QT bit tables
+    const uint32_t* const s_cfg = plan.cfg_tb + P.cfg_off;
+    const uint32_t* const s_qt = reinterpret_cast<const uint32_t*>(plan.qt_words + P.qt_off);
+    // store-side index tables (only for passes that store through a local bit
+    // permutation sigma, i.e. in front of a qubit-remap exchange)
+    uint64_t* const st_lo = reinterpret_cast<uint64_t*>(s_ops + n_ops);
+    uint64_t* const st_hi = st_lo + (1 << LO);
+    uint64_t* const st_tbase = st_hi + (1 << HI);  // [kTbaseChunks][128]
+    const bool store_perm = P.store_perm != 0;
     __shared__ uint64_t off_lo[1 << LO];
     __shared__ uint64_t off_hi[1 << HI];
     __shared__ uint64_t s_tbase[kTbaseChunks][128];  // tile index (7 bits per chunk) -> outer offset
@@ -264,9 +274,6 @@ k_tile_pass(double2* __restrict__ psi, PlanDev plan, int pass_index, double neg_
         int4* dst = reinterpret_cast<int4*>(s_ops);
         const int words = n_ops * static_cast<int>(sizeof(MicroOpDev) / sizeof(int4));
         for (int i = tid; i < words; i += NT) dst[i] = __ldg(src + i);
-        for (int i = tid; i < n_cfg * NT; i += NT) s_cfg[i] = __ldg(plan.cfg_tb + P.cfg_off + i);
-        const uint32_t* q32 = reinterpret_cast<const uint32_t*>(plan.qt_words + P.qt_off);
-        for (int i = tid; i < 2 * P.n_qt_words; i += NT) s_qt[i] = __ldg(q32 + i);
     }
     for (int i = tid; i < (1 << LO); i += NT) {
         uint64_t o = 0;
@@ -282,12 +289,30 @@ k_tile_pass(double2* __restrict__ psi, PlanDev plan, int pass_index, double neg_
     }
     for (int i = tid; i < kTbaseChunks * 128; i += NT) {
         const int c = i >> 7, v = i & 127;
-        uint64_t o = 0;
+        uint64_t o = 0, os = 0;
         for (int j = 0; j < 7; ++j) {
             const int q = 7 * c + j;
-            if (q < n_outer && ((v >> j) & 1)) o |= 1ull << P.opos[q];
+            if (q < n_outer && ((v >> j) & 1)) {
+                o |= 1ull << P.opos[q];
+                os |= 1ull << P.st_opos[q];
+            }
         }
         s_tbase[c][v] = o;
+        if (store_perm) st_tbase[i] = os;
+    }
+    if (store_perm) {
+        for (int i = tid; i < (1 << LO); i += NT) {
+            uint64_t o = 0;
+            for (int j = 0; j < LO; ++j)
+                if ((i >> j) & 1) o |= 1ull << P.st_lpos[j];
+            st_lo[i] = o;
+        }
+        for (int i = tid; i < (1 << HI); i += NT) {
+            uint64_t o = 0;
+            for (int j = 0; j < HI; ++j)
+                if ((i >> j) & 1) o |= 1ull << P.st_lpos[LO + j];
+            st_hi[i] = o;
+        }
     }
     if (has_table) {
         const PointDev& tp = plan.points[P.table_point];
@@ -319,7 +344,7 @@ k_tile_pass(double2* __restrict__ psi, PlanDev plan, int pass_index, double neg_
     for (uint64_t t = blockIdx.x; t < n_tiles; t += stride) {
         const uint64_t base = tile_base(t);
         const uint64_t full = rank_bits | base;
-        double2* const g = psi + base;
+        const double2* const g = psi + base;
 
         double2 v[NR];
         uint32_t tb = 0, swt = 0;  // local index / slot of this thread's register 0
@@ -329,7 +354,7 @@ k_tile_pass(double2* __restrict__ psi, PlanDev plan, int pass_index, double neg_
         bool smem_busy = true;     // smem may still be read by other threads (sync before writing)
 
         auto set_cfg = [&](const MicroOpDev& op) {
-            const uint32_t w = s_cfg[op.arg * NT + tid];
+            const uint32_t w = __ldg(s_cfg + op.arg * NT + tid);
             tb = w & 0xffffu;
             swt = w >> 16;
             cidx = op.cidx;
@@ -433,7 +458,7 @@ k_tile_pass(double2* __restrict__ psi, PlanDev plan, int pass_index, double neg_
                     if ((full & m) == m) q0 += 2u;
                 }
                 const uint32_t* qt = pt.qt_word >= 0 ? s_qt + 2 * pt.qt_word : nullptr;
-                auto qtb = [&](uint32_t l) -> unsigned { return qt ? (qt[l >> 5] >> (l & 31u)) & 1u : 0u; };
+                auto qtb = [&](uint32_t l) -> unsigned { return qt ? (__ldg(qt + (l >> 5)) >> (l & 31u)) & 1u : 0u; };
                 const unsigned qt_tb = qtb(tb);
                 q0 += __popc(tb & pt.s1L) + 2u * (__popc(tb & m2) + qt_tb);
                 unsigned dq[4];
@@ -563,13 +588,28 @@ k_tile_pass(double2* __restrict__ psi, PlanDev plan, int pass_index, double neg_
                 }
             } else {  // kOpStore
                 uint64_t o[NR];
-                phys_offsets(o);
+                double2* go;
+                if (store_perm) {
+                    // sigma is a bit permutation: sigma(base | off) = sigma(base) | sigma(off)
+                    uint64_t sb = 0;
+#pragma unroll
+                    for (int c = 0; c < kTbaseChunks; ++c) sb |= st_tbase[c * 128 + ((t >> (7 * c)) & 127)];
+                    go = out + sb;
+                    o[0] = st_lo[tb & ((1u << LO) - 1u)] | st_hi[tb >> LO];
+#pragma unroll
+                    for (int j = 0; j < R; ++j)
+#pragma unroll
+                        for (int s = 0; s < (1 << j); ++s) o[s + (1 << j)] = o[s] | op.c_off[j];
+                } else {
+                    go = out + base;
+                    phys_offsets(o);
+                }
                 if (op.mask & 2u) {
 #pragma unroll
-                    for (int s = 0; s < NR; ++s) __stcs(g + o[s], make_double2(v[s].x * scale, v[s].y * scale));
+                    for (int s = 0; s < NR; ++s) __stcs(go + o[s], make_double2(v[s].x * scale, v[s].y * scale));
                 } else {
 #pragma unroll
-                    for (int s = 0; s < NR; ++s) __stcs(g + o[s], v[s]);
+                    for (int s = 0; s < NR; ++s) __stcs(go + o[s], v[s]);
                 }
             }
         }
@@ -580,11 +620,12 @@ template <int K, int RB>
 size_t smem_bytes(const PassDev& ph) {
     using C = Cfg<K, RB>;
     return sizeof(double2) * C::N + sizeof(double) * ph.tab_words + sizeof(MicroOpDev) * ph.n_ops +
-           sizeof(uint32_t) * ph.n_cfg * C::NT + sizeof(uint64_t) * ph.n_qt_words;
+           (ph.store_perm ? sizeof(uint64_t) * ((1 << C::LO) + (1 << C::HI) + kTbaseChunks * 128) : 0);
 }
 
 template <int K, int RB>
-void launch_kr(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& plan, double dt, uint64_t rank_bits) {
+void launch_kr(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& plan, double dt, uint64_t rank_bits,
+               double* out) {
     using C = Cfg<K, RB>;
     const size_t smem = smem_bytes<K, RB>(ph);
     static size_t configured = 0;
@@ -601,17 +642,19 @@ void launch_kr(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& p
     uint64_t grid = static_cast<uint64_t>(s.sm_count) * static_cast<uint64_t>(occ);
     if (grid > n_tiles) grid = n_tiles;
     k_tile_pass<K, RB><<<static_cast<unsigned>(grid), C::NT, smem, s.stream>>>(
-        reinterpret_cast<double2*>(s.amps), plan, pass_index, -dt, rank_bits, n_tiles);
+        reinterpret_cast<const double2*>(s.amps), reinterpret_cast<double2*>(out ? out : s.amps), plan, pass_index,
+        -dt, rank_bits, n_tiles);
     SDB_CUDA(cudaGetLastError());
 }
 
 template <int K>
-void launch_k(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& plan, double dt, uint64_t rank_bits) {
+void launch_k(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& plan, double dt, uint64_t rank_bits,
+              double* out) {
     // R = 4 register coordinates (16 amplitudes per thread). R = 3 with twice the
     // threads spills at the 2-CTA/SM register budget and measured 1.5x slower
     // per step (profiles/r1_notes.md).
     if (ph.rbits != 4 && K >= 4) throw std::invalid_argument("tile pass: unsupported register config");
-    launch_kr<K, 4>(s, ph, pass_index, plan, dt, rank_bits);
+    launch_kr<K, 4>(s, ph, pass_index, plan, dt, rank_bits, out);
 }
 
 }  // namespace
@@ -619,11 +662,11 @@ void launch_k(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& pl
 int max_tile_qubits() { return 12; }
 
 void launch_tile_pass(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& plan, double dt,
-                      uint64_t rank_bits) {
+                      uint64_t rank_bits, double* out) {
     if (ph.n_outer > 7 * kTbaseChunks) throw std::invalid_argument("tile pass: too many outer bits");
     switch (ph.k) {
 #define SDB_K(KK) \
-    case KK: launch_k<KK>(s, ph, pass_index, plan, dt, rank_bits); break;
+    case KK: launch_k<KK>(s, ph, pass_index, plan, dt, rank_bits, out); break;
         SDB_K(1) SDB_K(2) SDB_K(3) SDB_K(4) SDB_K(5) SDB_K(6) SDB_K(7) SDB_K(8) SDB_K(9) SDB_K(10)
         SDB_K(11) SDB_K(12)
 #undef SDB_K

@@ -67,6 +67,7 @@ struct MicroOpDev {
     uint32_t cidx;  // LOAD/CFG: local coordinate index of register coordinate j in byte j
     int pad;        // POINT: bit s = QT(r_s) for the register combination s of the current config
     uint64_t c_off[4];  // LOAD/CFG: physical offsets of the register coordinates;
+                        // STORE with a store permutation: sigma-mapped offsets;
                         // POINT (factor mode): c_off[f] packs the swizzled compact
                         // slot offset of register coordinate j in bits 16j..16j+15
 };
@@ -155,8 +156,12 @@ struct PassDev {
     int n_qt_words;   // QT words staged into shared memory
     int tab_words;    // 8-byte words of the per-tile table region (even; 0 if none)
     double table_scale;  // factor mode: exact scale folded into E_0 (1 if applied elsewhere)
+    int store_perm;      // 1: store out of place through a local bit permutation sigma
+    int st_lpos[16];     // sigma(lpos[j])
+    int st_opos[64];     // sigma(opos[j])
 };
 constexpr int kPassNeedsTable = 1;
+
 
 struct PlanDev {
     const PassDev* passes;
@@ -210,8 +215,9 @@ void launch_permute_bits(StateImpl& s, const double* src, double* dst, const int
                          int n_bits);
 
 // Fused pass launcher (pass_kernel.cu).
+// out: destination buffer (nullptr = in place on s.amps).
 void launch_tile_pass(StateImpl& s, const PassDev& pass_host, int pass_index, const PlanDev& plan,
-                      double dt, uint64_t rank_bits);
+                      double dt, uint64_t rank_bits, double* out);
 int max_tile_qubits();
 
 }  // namespace sdb

@@ -489,10 +489,20 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
         MicroOpDev so{};
         so.kind = kOpStore;
         so.perm = -1;
+        if (!pp.store_sigma.empty()) {
+            pd.store_perm = 1;
+            for (int j = 0; j < K; ++j) pd.st_lpos[j] = pp.store_sigma[pp.lpos[j]];
+            for (int j = 0; j < pd.n_outer; ++j) pd.st_opos[j] = pp.store_sigma[pd.opos[j]];
+            int j = 0;
+            for (uint32_t m = cur; m && j < 4; m &= m - 1, ++j) {
+                so.c_off[j] = 1ull << pp.store_sigma[pp.lpos[std::countr_zero(m)]];
+            }
+        }
         if (pp.scale_exp > 0 && !scale_placed) so.mask |= 2u;
         A.ops.push_back(so);
         pd.n_ops = static_cast<int>(A.ops.size()) - pd.op_off;
         pd.n_qt_words = static_cast<int>(A.qt_words.size()) - pd.qt_off;
+        if (pd.n_ops > 2 * kMaxOpsPerPass + 4) throw std::logic_error("lower_plan: pass program too long");
         A.passes.push_back(pd);
         A.pass_class.push_back(only_point ? 1 : 0);
         A.transposes.push_back(transposes);

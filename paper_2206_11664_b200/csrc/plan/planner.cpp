@@ -144,8 +144,35 @@ double reference_sweeps(const std::vector<GroupSpec>& groups, int order) {
     return order == 2 ? 2.0 * per_step : per_step;
 }
 
+void finalize_scales(std::vector<PassPlan*>& passes) {
+    int cum = 0;
+    for (PassPlan* pp : passes) cum += pp->butterflies;
+    if (cum & 1) throw std::logic_error("plan_step: odd number of Hadamards in a step");
+    // Deferred exact normalisation: butterflies are unnormalised, and
+    // multiplying by 2^-e is exact in floating point, so the pending factor
+    // is applied only in passes that already multiply every amplitude by a
+    // phase (free), when it exceeds 2^48, or at the end of the step.
+    int pending = 0;
+    for (size_t p = 0; p < passes.size(); ++p) {
+        PassPlan& pp = *passes[p];
+        pending += pp.butterflies;
+        bool has_phase = false;
+        for (const PassStage& st : pp.stages) {
+            if (st.kind == PassStage::POINT && !pp.points[st.point].terms.empty()) has_phase = true;
+        }
+        const bool last = p + 1 == passes.size();
+        if (last || has_phase || pending >= 96) {
+            pp.scale_exp = pending / 2;
+            pending -= 2 * pp.scale_exp;
+        } else {
+            pp.scale_exp = 0;
+        }
+    }
+    if (pending != 0) throw std::logic_error("plan_step: normalisation did not close");
+}
+
 StepPlan plan_step(const std::vector<Op>& ops, const std::vector<GroupSpec>& groups, int n_local,
-                   int k, int n_fixed, const std::vector<int>& phys_of) {
+                   int k, int n_fixed, const std::vector<int>& phys_of, bool finalize) {
     if (k > n_local) k = n_local;
     if (n_fixed > k) n_fixed = k;
     StepPlan plan;
@@ -193,6 +220,7 @@ StepPlan plan_step(const std::vector<Op>& ops, const std::vector<GroupSpec>& gro
         std::vector<int> sched;
         extend();
         for (;;) {
+            if (sched.size() >= static_cast<size_t>(kMaxOpsPerPass)) break;
             long pick = -1;
             for (size_t j = first; j < hi; ++j) {
                 if (!done[j] && blockers[j] == 0 && (ops[j].need & ~L) == 0) {
@@ -318,30 +346,232 @@ StepPlan plan_step(const std::vector<Op>& ops, const std::vector<GroupSpec>& gro
         cum += levels;
         plan.passes.push_back(std::move(pp));
     }
-    if (cum & 1) throw std::logic_error("plan_step: odd number of Hadamards in a step");
-    // Deferred exact normalisation: butterflies are unnormalised, and
-    // multiplying by 2^-e is exact in floating point, so the pending factor
-    // is applied only in passes that already multiply every amplitude by a
-    // phase (free), when it exceeds 2^48, or at the end of the step.
-    int pending = 0;
-    for (size_t p = 0; p < plan.passes.size(); ++p) {
-        PassPlan& pp = plan.passes[p];
-        pending += pp.butterflies;
-        bool has_phase = false;
-        for (const PassStage& st : pp.stages) {
-            if (st.kind == PassStage::POINT && !pp.points[st.point].terms.empty()) has_phase = true;
-        }
-        const bool last = p + 1 == plan.passes.size();
-        if (last || has_phase || pending >= 96) {
-            pp.scale_exp = pending / 2;
-            pending -= 2 * pp.scale_exp;
-        } else {
-            pp.scale_exp = 0;
-        }
+    (void)cum;
+    if (finalize) {
+        std::vector<PassPlan*> ptrs;
+        for (PassPlan& pp : plan.passes) ptrs.push_back(&pp);
+        finalize_scales(ptrs);
     }
-    if (pending != 0) throw std::logic_error("plan_step: normalisation did not close");
     plan.ref_sweeps = 0.0;
     return plan;
+}
+
+ShardedStep plan_sharded_step(const std::vector<Op>& ops, const std::vector<GroupSpec>& groups, int n_local,
+                              int k, int n_fixed, const std::vector<int>& phys_in) {
+    ShardedStep out;
+    out.phys_in = phys_in;
+    const int n = static_cast<int>(phys_in.size());
+    const int g = n - n_local;
+    std::vector<int> L = phys_in;
+    auto global_set = [&]() {
+        uint64_t G = 0;
+        for (int q = 0; q < n; ++q) {
+            if (L[q] >= n_local) G |= bitq(q);
+        }
+        return G;
+    };
+    std::vector<int> rem(ops.size());
+    for (size_t i = 0; i < rem.size(); ++i) rem[i] = static_cast<int>(i);
+    constexpr size_t W = 1024;
+
+    // Chooses and applies one exchange bringing the global qubits that
+    // `upcoming` (op indices into `stream`) needs first.
+    auto make_exchange = [&](const std::vector<const Op*>& upcoming) {
+        const uint64_t G = global_set();
+        // the first op that needs a global qubit sets the mandatory part; later
+        // ops' global needs are added while enough local qubits that the first
+        // op does not need can be evicted for them
+        uint64_t incoming = 0, protect = 0;
+        int evictable = 0;
+        for (const Op* o : upcoming) {
+            const uint64_t want = o->need & G;
+            if (!want) continue;
+            if (!incoming) {
+                incoming = want;
+                protect = o->need & ~G;
+                for (int q = 0; q < n; ++q) {
+                    if (L[q] >= n_fixed && L[q] < n_local && !((protect >> q) & 1)) ++evictable;
+                }
+                if (std::popcount(incoming) > evictable) {
+                    throw std::logic_error("plan_sharded_step: tile too small for the shard (op needs more local qubits)");
+                }
+                continue;
+            }
+            if (std::popcount(incoming | want) > std::min(g, evictable)) break;
+            incoming |= want;
+        }
+        if (!incoming) throw std::logic_error("plan_sharded_step: exchange without a global need");
+        const int gp = std::popcount(incoming);
+        // next use of every qubit in the upcoming stream
+        std::vector<size_t> next_use(n, SIZE_MAX);
+        uint64_t seen = 0;
+        for (size_t i = 0; i < upcoming.size() && seen != (n >= 64 ? ~0ull : ((1ull << n) - 1)); ++i) {
+            uint64_t m = upcoming[i]->need & ~seen;
+            seen |= upcoming[i]->need;
+            while (m) {
+                const int q = std::countr_zero(m);
+                m &= m - 1;
+                next_use[q] = i;
+            }
+        }
+        // candidates: local qubits outside the always-local low bits
+        std::vector<int> cand;
+        for (int q = 0; q < n; ++q) {
+            if (L[q] >= n_fixed && L[q] < n_local) cand.push_back(q);
+        }
+        const int t0 = n_local - gp;
+        std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) {
+            if (next_use[a] != next_use[b]) return next_use[a] > next_use[b];
+            return L[a] > L[b];  // prefer qubits already high (fewer sigma moves)
+        });
+        if (static_cast<int>(cand.size()) < gp) throw std::logic_error("plan_sharded_step: no qubit to evict");
+        std::vector<int> evict(cand.begin(), cand.begin() + gp);
+        ExchangeSpec ex;
+        ex.sigma.resize(n_local);
+        for (int b = 0; b < n_local; ++b) ex.sigma[b] = b;
+        // place evicted qubits on T = t0..n_local-1 (keep those already there)
+        std::vector<int> tslot_owner(gp, -1);
+        std::vector<int> pending;
+        for (int e : evict) {
+            if (L[e] >= t0) tslot_owner[L[e] - t0] = e;
+            else pending.push_back(e);
+        }
+        std::vector<int> logical_at(n_local, -1);
+        for (int q = 0; q < n; ++q) {
+            if (L[q] < n_local) logical_at[L[q]] = q;
+        }
+        for (int e : pending) {
+            int slot = 0;
+            while (tslot_owner[slot] >= 0) ++slot;
+            const int pe = L[e], pt = t0 + slot;
+            std::swap(ex.sigma[pe], ex.sigma[pt]);
+            const int other = logical_at[pt];
+            if (other >= 0) L[other] = pe;
+            L[e] = pt;
+            logical_at[pe] = other;
+            logical_at[pt] = e;
+            tslot_owner[slot] = e;
+        }
+        // pair incoming global qubits (ascending global position) with T slots
+        std::vector<int> inc;
+        for (uint64_t m = incoming; m; m &= m - 1) inc.push_back(std::countr_zero(m));
+        std::sort(inc.begin(), inc.end(), [&](int a, int b) { return L[a] < L[b]; });
+        for (int i = 0; i < gp; ++i) {
+            const int qi = inc[i], qe = tslot_owner[i];
+            ex.swaps.emplace_back(L[qi], t0 + i);
+            L[qe] = L[qi];
+            L[qi] = t0 + i;
+        }
+        return ex;
+    };
+
+    while (true) {
+        const uint64_t G = global_set();
+        // dependency-closed set of remaining ops that need no global qubit
+        std::vector<int> take, rest;
+        {
+            // an op is taken if it needs no global qubit and commutes with every
+            // op held back before it; once many ops are held back the rest of
+            // the step simply waits for the next segment
+            constexpr size_t kMaxBlocked = 512;
+            std::vector<int> blocked;
+            for (size_t j = 0; j < rem.size(); ++j) {
+                const Op& o = ops[rem[j]];
+                bool ok = blocked.size() < kMaxBlocked && (o.need & G) == 0;
+                if (ok) {
+                    for (int b : blocked) {
+                        if (!commute(ops[b], o)) {
+                            ok = false;
+                            break;
+                        }
+                    }
+                }
+                if (ok) {
+                    take.push_back(rem[j]);
+                } else {
+                    rest.push_back(rem[j]);
+                    if (blocked.size() < kMaxBlocked) blocked.push_back(rem[j]);
+                }
+            }
+        }
+        Segment seg;
+        seg.phys_of = L;
+        if (!take.empty()) {
+            std::vector<Op> seg_ops;
+            for (int i : take) seg_ops.push_back(ops[i]);
+            seg.plan = plan_step(seg_ops, groups, n_local, k, n_fixed, L, false);
+        }
+        if (rest.empty()) {
+            // lookahead into the next step: remap now if its first op needs a global qubit
+            if (g > 0 && !ops.empty() && (ops[0].need & global_set())) {
+                std::vector<const Op*> up;
+                for (size_t i = 0; i < ops.size() && i < W; ++i) up.push_back(&ops[i]);
+                seg.exchange_after = true;
+                seg.ex = make_exchange(up);
+            }
+            out.segs.push_back(std::move(seg));
+            break;
+        }
+        if (take.empty() && !out.segs.empty() && out.segs.back().plan.passes.empty()) {
+            std::ostringstream os;
+            os << "plan_sharded_step: no progress at op " << rem.front() << " (kind " << ops[rem.front()].kind
+               << ", need 0x" << std::hex << ops[rem.front()].need << ", globals 0x" << G << ")";
+            throw std::logic_error(os.str());
+        }
+        std::vector<const Op*> up;
+        for (size_t i = 0; i < rest.size() && up.size() < W; ++i) up.push_back(&ops[rest[i]]);
+        for (size_t i = 0; i < ops.size() && up.size() < W; ++i) up.push_back(&ops[i]);
+        seg.exchange_after = true;
+        seg.ex = make_exchange(up);
+        out.segs.push_back(std::move(seg));
+        rem = std::move(rest);
+    }
+    out.phys_out = L;
+    // A segment that ends in an exchange stores its last pass out of place
+    // through sigma; a segment without passes gets a permute-only pass.
+    std::vector<PassPlan*> all;
+    for (Segment& sg : out.segs) {
+        if (sg.exchange_after) {
+            if (sg.plan.passes.empty()) {
+                PassPlan pp;
+                const int kk = std::min(k, n_local);
+                for (int b = 0; b < kk; ++b) pp.lpos.push_back(b);
+                sg.plan.passes.push_back(std::move(pp));
+            }
+            sg.plan.passes.back().store_sigma = sg.ex.sigma;
+        }
+        for (PassPlan& pp : sg.plan.passes) all.push_back(&pp);
+        out.n_exchanges += sg.exchange_after ? 1 : 0;
+    }
+    out.n_passes = static_cast<int>(all.size());
+    finalize_scales(all);
+    return out;
+}
+
+std::string describe_sharded_json(const ShardedStep& s) {
+    std::ostringstream os;
+    os << "{\"phys_in\":[";
+    for (size_t i = 0; i < s.phys_in.size(); ++i) os << (i ? "," : "") << s.phys_in[i];
+    os << "],\"phys_out\":[";
+    for (size_t i = 0; i < s.phys_out.size(); ++i) os << (i ? "," : "") << s.phys_out[i];
+    os << "],\"segments\":[";
+    for (size_t i = 0; i < s.segs.size(); ++i) {
+        const Segment& sg = s.segs[i];
+        os << (i ? "," : "") << "{\"plan\":" << describe_json(sg.plan) << ",\"exchange\":";
+        if (!sg.exchange_after) {
+            os << "null";
+        } else {
+            os << "{\"sigma\":[";
+            for (size_t b = 0; b < sg.ex.sigma.size(); ++b) os << (b ? "," : "") << sg.ex.sigma[b];
+            os << "],\"swaps\":[";
+            for (size_t b = 0; b < sg.ex.swaps.size(); ++b)
+                os << (b ? "," : "") << "[" << sg.ex.swaps[b].first << "," << sg.ex.swaps[b].second << "]";
+            os << "]}";
+        }
+        os << "}";
+    }
+    os << "]}";
+    return os.str();
 }
 
 std::string describe(const StepPlan& p) {

@@ -10,6 +10,10 @@
 
 namespace sdb {
 
+// Gate ops per pass (planner cap): every gate op lowers to <= 2 micro-ops, so
+// a pass's program staged in shared memory stays <= ~13 KiB.
+constexpr int kMaxOpsPerPass = 96;
+
 // One group as the planner sees it (a flattened DiagonalGroup).
 struct GroupSpec {
     std::vector<int> h_pre, s_layer, h_post;
@@ -64,6 +68,7 @@ struct PassPlan {
     int butterflies = 0;        // WHT levels applied in this pass
     int scale_exp = 0;          // store scale = 2^-scale_exp
     std::vector<int> op_ids;    // ops scheduled here (debug)
+    std::vector<int> store_sigma;  // non-empty: store out of place through this local bit permutation
 };
 
 struct StepPlan {
@@ -76,10 +81,54 @@ struct StepPlan {
 // Greedy list scheduling of `ops` into tile passes of <= k local qubits, of
 // which the lowest `n_fixed` physical bits are always local (coalescing).
 // phys_of maps logical qubit -> physical bit (identity for one device).
+// finalize_scales = false leaves scale_exp at 0 (the sharded planner places
+// the exact normalisation over all segments of a step, finalize_scales()).
 StepPlan plan_step(const std::vector<Op>& ops, const std::vector<GroupSpec>& groups, int n_local,
-                   int k, int n_fixed, const std::vector<int>& phys_of);
+                   int k, int n_fixed, const std::vector<int>& phys_of, bool finalize = true);
+
+// Deferred exact normalisation over a pass sequence (see planner.cpp).
+void finalize_scales(std::vector<PassPlan*>& passes);
 
 double reference_sweeps(const std::vector<GroupSpec>& groups, int order);
+
+// ------------------------------------------------------- sharded steps
+// A state sharded over P = 2^g ranks keeps physical bits >= n_local on the
+// rank index. A Hadamard or CNOT target on such a "global" bit needs a qubit
+// remap: the step is cut into segments whose needed qubits are all local,
+// and between segments an exchange swaps g' <= g global bits with the top
+// g' local bits T_i = n_local - g' + i. Before the swap a local bit
+// permutation sigma moves the evicted qubits onto T (folded into the last
+// pass of the segment, which stores out of place). Rank r then sends local
+// chunk c (top g' bits = c) to the rank whose swapped global bits equal c
+// and receives into chunk [sender's swapped global bits].
+struct ExchangeSpec {
+    std::vector<int> sigma;                  // new physical position of local bit b (size n_local)
+    std::vector<std::pair<int, int>> swaps;  // (global physical bit, local physical bit T_i)
+};
+
+struct Segment {
+    StepPlan plan;                // passes in the segment's starting layout
+    std::vector<int> phys_of;     // layout the passes run in
+    bool exchange_after = false;
+    ExchangeSpec ex;
+};
+
+struct ShardedStep {
+    std::vector<int> phys_in, phys_out;
+    std::vector<Segment> segs;
+    int n_exchanges = 0;
+    int n_passes = 0;   // including permute-only passes in front of exchanges
+};
+
+// Plans one Trotter step starting from layout phys_in. Exchanges are chosen
+// Belady-style (evict the local qubits whose next use is furthest, looking
+// into the next step); when the next step's first op would need a global
+// qubit the remap is scheduled at the end of this step, so every exchange
+// follows a pass of the same step except possibly the very first.
+ShardedStep plan_sharded_step(const std::vector<Op>& ops, const std::vector<GroupSpec>& groups, int n_local,
+                              int k, int n_fixed, const std::vector<int>& phys_in);
+
+std::string describe_sharded_json(const ShardedStep& s);
 
 std::string describe(const StepPlan& p);
 // Machine-readable schedule (tests emulate it on the CPU).

@@ -299,9 +299,12 @@ class StateVector:
     shard on the top log2(world) qubits.
     """
 
-    def __init__(self, n_qubits: int, device: int = 0, rank: int = 0, world: int = 1):
-        h = C.c_void_p()
-        check(A.sd_state_create_shard(n_qubits, rank, world, device, C.byref(h)))
+    def __init__(self, n_qubits: int, device: int = 0, rank: int = 0, world: int = 1, _handle=None):
+        if _handle is None:
+            h = C.c_void_p()
+            check(A.sd_state_create_shard(n_qubits, rank, world, device, C.byref(h)))
+        else:
+            h = C.c_void_p(_handle)
         self._s = h
         nl = C.c_int(0)
         check(A.sd_state_info(self._s, None, C.byref(nl), None, None))
@@ -386,6 +389,15 @@ class StateVector:
         p = C.c_void_p()
         check(A.sd_state_device_ptr(self._s, C.byref(p)))
         return p.value or 0
+
+    def attach_comm(self, unique_id: bytes) -> None:
+        """Bind this shard to an NCCL communicator (sd_state_attach_comm);
+        every rank passes the same 128-byte id from comm_unique_id()."""
+        check(A.sd_state_attach_comm(self._s, C.create_string_buffer(bytes(unique_id), 128)))
+
+    def canonicalize(self) -> None:
+        """Undo qubit relabelling (collective for NCCL-attached shards)."""
+        check(A.sd_state_canonicalize(self._s))
 
     def sync(self) -> None:
         check(A.sd_sync(self._s))
@@ -535,3 +547,46 @@ def evolve_grouped(groups: Sequence[DiagonalGroup], psi: StateVector, plan: Evol
     if plan.n_steps == 0:
         return
     TrotterPlan(psi, groups, order=plan.order, **options).evolve(dt, plan.n_steps)
+
+
+def comm_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it; broadcast it with torch.distributed)."""
+    buf = C.create_string_buffer(128)
+    check(A.sd_comm_unique_id(buf))
+    return buf.raw
+
+
+class LocalShards:
+    """`world` shards of one 2^n state driven by this process (devices may
+    repeat: virtual shards on one GPU). Exchanges are device copies with the
+    same routing as the NCCL path (sd_state_create_local_shards)."""
+
+    def __init__(self, n_qubits: int, world: int, devices: Optional[Sequence[int]] = None):
+        arr = (C.c_void_p * world)()
+        devs = (C.c_int * world)(*(devices if devices is not None else [0] * world))
+        check(A.sd_state_create_local_shards(n_qubits, world, devs, arr))
+        self.shards = [StateVector(n_qubits, devs[r], r, world, _handle=arr[r]) for r in range(world)]
+        self.n, self.world = n_qubits, world
+        self.n_local = self.shards[0].n_local
+        self.plans: List["TrotterPlan"] = []
+
+    def upload(self, amps: np.ndarray) -> None:
+        a = np.ascontiguousarray(amps, dtype=np.complex128).reshape(self.world, 1 << self.n_local)
+        for r, s in enumerate(self.shards):
+            s.upload(a[r])
+
+    def set_basis(self, index: int) -> None:
+        for s in self.shards:
+            s.set_basis(index)
+
+    def plan(self, groups: Sequence[DiagonalGroup], order: int = 1, tile_qubits: int = 0) -> None:
+        self.plans = [TrotterPlan(s, groups, order=order, tile_qubits=tile_qubits) for s in self.shards]
+
+    def evolve(self, dt: float, n_steps: int) -> None:
+        arr = (C.c_void_p * self.world)(*[p._p.value for p in self.plans])
+        check(A.sd_evolve_local(arr, self.world, dt, n_steps))
+
+    def amplitudes(self) -> np.ndarray:
+        arr = (C.c_void_p * self.world)(*[s._s.value for s in self.shards])
+        check(A.sd_local_canonicalize(arr, self.world))
+        return np.concatenate([s.amplitudes() for s in self.shards])

@@ -31,8 +31,10 @@ def test_schedule_matches_oracle(cfg, n, k, sd, port):
     sg = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
     order = M.CONFIGS[cfg]["order"]
     info, sched = sd.plan_preview(n, sg, order=order, tile_qubits=k)
-    assert info["n_passes_per_step"] == len(sched["passes"])
-    assert all(len(p["lpos"]) == min(k, n) for p in sched["passes"])
+    passes = sched["steps"][0]["segments"][0]["plan"]["passes"]
+    assert len(sched["steps"]) == 1 and len(sched["steps"][0]["segments"]) == 1
+    assert info["n_passes_per_step"] == len(passes)
+    assert all(len(p["lpos"]) == min(k, n) for p in passes)
     psi0 = initial(port, cfg, n)
     dt = M.CONFIGS[cfg]["dt"] * 7  # larger angles make ordering bugs visible
     want = port.evolve_grouped(psi0, n, og, dt, 2, order)
@@ -47,3 +49,32 @@ def test_fused_pass_count_beats_reference_sweeps(sd):
         g = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
         info, _ = sd.plan_preview(M.CONFIGS[cfg]["n"], g, order=M.CONFIGS[cfg]["order"], tile_qubits=12)
         assert info["n_passes_per_step"] * 8 < info["n_ref_sweeps_per_step"]
+
+
+SHARDED = [(1, 10, 6, 2), (2, 9, 5, 4), (3, 10, 6, 2), (3, 10, 6, 8), (4, 11, 6, 2), (4, 11, 7, 4), (4, 12, 8, 8),
+           (5, 10, 6, 4), (5, 11, 7, 2)]
+
+
+@pytest.mark.parametrize("cfg,n,k,world", SHARDED)
+def test_sharded_schedule_matches_oracle(cfg, n, k, world, sd, port):
+    """The sharded planner (segments + qubit-remap exchanges over `world`
+    ranks) emulated on the full state reproduces the oracle."""
+    text = M.config_text(cfg, n=n)
+    _, og = port.partition_and_diagonalize(text)
+    sg = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
+    order = M.CONFIGS[cfg]["order"]
+    info, sched = sd.plan_preview(n, sg, order=order, tile_qubits=k, world=world)
+    n_local = sched["n_local"]
+    for st in sched["steps"]:
+        for seg in st["segments"]:
+            for p in seg["plan"]["passes"]:
+                assert max(p["lpos"]) < n_local  # passes only touch local bits
+    psi0 = initial(port, cfg, n)
+    dt = M.CONFIGS[cfg]["dt"] * 7
+    steps = 3
+    want = port.evolve_grouped(psi0, n, og, dt, steps, order)
+    got = run_schedule(psi0, n, sched, dt, steps=steps)
+    assert np.max(np.abs(got - want)) < 1e-11
+    assert abs(np.linalg.norm(got) - 1) < 1e-13
+    if cfg == 4:
+        assert info["n_exchanges_per_step"] >= 4  # 2 groups with h_post = all qubits (SURVEY 8e bound)

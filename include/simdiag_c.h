@@ -258,6 +258,20 @@ sd_status sd_state_create_local_shards(int n_qubits, int world, const int* devic
 sd_status sd_evolve_local(sd_plan* const* plans, int world, double dt, int n_steps);
 sd_status sd_local_canonicalize(sd_state* const* shards, int world);
 
+/* Chunk routing of one remap exchange for `rank` (host-only; the routing both
+ * transports execute, exported for multi-process tests). swaps = 2*n_swaps
+ * ints (global bit, local bit) as in sd_plan_preview's JSON. Offsets and
+ * counts are in amplitudes of the rank's shard: send B[send_offset, +count)
+ * to peer, receive into A[recv_offset, +count); peer == rank is a local copy. */
+typedef struct sd_route {
+    int peer;
+    uint64_t send_offset;
+    uint64_t recv_offset;
+    uint64_t count;
+} sd_route;
+sd_status sd_exchange_routes(int n_qubits, int n_local, int rank, const int32_t* swaps, size_t n_swaps,
+                             sd_route* out, size_t cap, size_t* n_out);
+
 #ifdef __cplusplus
 }
 #endif

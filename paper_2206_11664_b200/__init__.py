@@ -22,6 +22,7 @@ from .simdiag import (  # noqa: F401
     commutes,
     diagonalize_group,
     evolve_grouped,
+    exchange_routes,
     fidelity,
     greedy_partition,
     norm,

@@ -148,6 +148,14 @@ sd_state_create_local_shards = _sig("sd_state_create_local_shards", [C.c_int, C.
 sd_evolve_local = _sig("sd_evolve_local", [C.POINTER(P), C.c_int, dbl, C.c_int])
 sd_local_canonicalize = _sig("sd_local_canonicalize", [C.POINTER(P), C.c_int])
 
+
+class Route(C.Structure):
+    _fields_ = [("peer", C.c_int), ("send_offset", u64), ("recv_offset", u64), ("count", u64)]
+
+
+sd_exchange_routes = _sig("sd_exchange_routes", [C.c_int, C.c_int, C.c_int, C.POINTER(i32), sz, C.POINTER(Route), sz,
+                                                 C.POINTER(sz)])
+
 EXPORTED = [
     "sd_last_error", "sd_version",
     "sd_hamiltonian_from_terms", "sd_hamiltonian_load_text", "sd_hamiltonian_load_file",
@@ -163,7 +171,7 @@ EXPORTED = [
     "sd_plan_options_default", "sd_plan_create", "sd_plan_destroy", "sd_plan_get_info",
     "sd_plan_describe", "sd_plan_preview", "sd_evolve", "sd_evolve_async", "sd_plan_set_profiling",
     "sd_plan_kernel_times", "sd_comm_unique_id", "sd_state_attach_comm", "sd_state_canonicalize",
-    "sd_state_create_local_shards", "sd_evolve_local", "sd_local_canonicalize",
+    "sd_state_create_local_shards", "sd_evolve_local", "sd_local_canonicalize", "sd_exchange_routes",
 ]
 
 

@@ -1039,4 +1039,19 @@ sd_status sd_local_canonicalize(sd_state* const* hs, int world) {
     });
 }
 
+sd_status sd_exchange_routes(int n, int n_local, int rank, const int32_t* swaps, size_t n_swaps, sd_route* out,
+                             size_t cap, size_t* n_out) {
+    return guard([&] {
+        require(n_swaps == 0 || swaps != nullptr, "null swap array");
+        require(rank >= 0 && n_local >= 1 && n_local <= n && rank < (1 << (n - n_local)), "rank out of range");
+        sdb::ExchangeSpec ex;
+        for (size_t i = 0; i < n_swaps; ++i) ex.swaps.emplace_back(swaps[2 * i], swaps[2 * i + 1]);
+        const auto routes = sdb::exchange_routes(n_local, n, rank, ex);
+        if (n_out) *n_out = routes.size();
+        for (size_t i = 0; i < routes.size() && i < cap && out; ++i) {
+            out[i] = sd_route{routes[i].peer, routes[i].send_off, routes[i].recv_off, routes[i].count};
+        }
+    });
+}
+
 }  // extern "C"

@@ -21,8 +21,7 @@
 #include <stdexcept>
 #include <string>
 
-#include "../internal.hpp"
-#include "../plan/planner.hpp"
+#include "exchange.hpp"
 
 namespace sdb {
 
@@ -77,15 +76,6 @@ void nccl_check(ncclResult_t r, const char* what) {
     }
 }
 
-// bits of rank r at the swapped global positions, packed (bit i <-> swap i)
-uint32_t swapped_bits(uint64_t r, int n_local, const ExchangeSpec& ex) {
-    uint32_t c = 0;
-    for (size_t i = 0; i < ex.swaps.size(); ++i) {
-        if ((r >> (ex.swaps[i].first - n_local)) & 1ull) c |= 1u << i;
-    }
-    return c;
-}
-
 uint64_t with_bits(uint64_t r, int n_local, const ExchangeSpec& ex, uint32_t c) {
     for (size_t i = 0; i < ex.swaps.size(); ++i) {
         const uint64_t b = 1ull << (ex.swaps[i].first - n_local);
@@ -94,16 +84,31 @@ uint64_t with_bits(uint64_t r, int n_local, const ExchangeSpec& ex, uint32_t c) 
     return r;
 }
 
-void check_spec(const StateImpl& s, const ExchangeSpec& ex) {
+void check_spec(int n_local, int n, const ExchangeSpec& ex) {
     const int gp = static_cast<int>(ex.swaps.size());
+    if (gp < 1 || gp > n - n_local) throw std::invalid_argument("exchange: bad number of swapped bits");
     for (int i = 0; i < gp; ++i) {
-        if (ex.swaps[i].second != s.n_local - gp + i || ex.swaps[i].first < s.n_local || ex.swaps[i].first >= s.n) {
-            throw std::logic_error("exchange: swaps must pair global bits with the top local bits");
+        if (ex.swaps[i].second != n_local - gp + i || ex.swaps[i].first < n_local || ex.swaps[i].first >= n) {
+            throw std::invalid_argument("exchange: swaps must pair global bits with the top local bits");
         }
     }
 }
 
 }  // namespace
+
+std::vector<Route> exchange_routes(int n_local, int n, int rank, const ExchangeSpec& ex) {
+    check_spec(n_local, n, ex);
+    const int gp = static_cast<int>(ex.swaps.size());
+    const uint64_t chunk = uint64_t(1) << (n_local - gp);
+    std::vector<Route> out;
+    for (uint32_t c = 0; c < (1u << gp); ++c) {
+        const int peer = static_cast<int>(with_bits(static_cast<uint64_t>(rank), n_local, ex, c));
+        // the peer holds our chunk c after the swap at our swapped bits; we
+        // receive its chunk (its swapped bits = c) into A[c]
+        out.push_back({peer, chunk * c, chunk * c, chunk});
+    }
+    return out;
+}
 
 void nccl_unique_id(unsigned char out[128]) {
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
@@ -143,44 +148,42 @@ double nccl_sum(StateImpl& s, double v) {
 
 void exchange_nccl(StateImpl& s, const ExchangeSpec& ex) {
     if (!s.nccl) throw std::runtime_error("sharded state has no communicator (sd_state_attach_comm)");
-    check_spec(s, ex);
-    const int gp = static_cast<int>(ex.swaps.size());
-    const uint64_t chunk = uint64_t(1) << (s.n_local - gp);  // amplitudes per chunk
-    const uint32_t own = swapped_bits(static_cast<uint64_t>(s.rank), s.n_local, ex);
+    const std::vector<Route> routes = exchange_routes(s.n_local, s.n, s.rank, ex);
     const NcclApi& a = nccl();
     auto comm = static_cast<ncclComm_t>(s.nccl);
     nccl_check(a.groupStart(), "ncclGroupStart");
-    for (uint32_t c = 0; c < (1u << gp); ++c) {
-        if (c == own) continue;
-        const int peer = static_cast<int>(with_bits(static_cast<uint64_t>(s.rank), s.n_local, ex, c));
-        nccl_check(a.send(s.xbuf + 2 * chunk * c, 2 * chunk, ncclDouble, peer, comm, s.stream), "ncclSend");
-        nccl_check(a.recv(s.amps + 2 * chunk * c, 2 * chunk, ncclDouble, peer, comm, s.stream), "ncclRecv");
+    for (const Route& rt : routes) {
+        if (rt.peer == s.rank) continue;
+        nccl_check(a.send(s.xbuf + 2 * rt.send_off, 2 * rt.count, ncclDouble, rt.peer, comm, s.stream), "ncclSend");
+        nccl_check(a.recv(s.amps + 2 * rt.recv_off, 2 * rt.count, ncclDouble, rt.peer, comm, s.stream), "ncclRecv");
     }
     nccl_check(a.groupEnd(), "ncclGroupEnd");
-    SDB_CUDA(cudaMemcpyAsync(s.amps + 2 * chunk * own, s.xbuf + 2 * chunk * own, 16 * chunk,
-                             cudaMemcpyDeviceToDevice, s.stream));
+    for (const Route& rt : routes) {
+        if (rt.peer != s.rank) continue;
+        SDB_CUDA(cudaMemcpyAsync(s.amps + 2 * rt.recv_off, s.xbuf + 2 * rt.send_off, 16 * rt.count,
+                                 cudaMemcpyDeviceToDevice, s.stream));
+    }
 }
 
 void exchange_local(const std::vector<StateImpl*>& shards, const ExchangeSpec& ex) {
     const int world = static_cast<int>(shards.size());
-    StateImpl& s0 = *shards[0];
-    check_spec(s0, ex);
-    const int gp = static_cast<int>(ex.swaps.size());
-    const uint64_t chunk = uint64_t(1) << (s0.n_local - gp);
     for (StateImpl* s : shards) {
         SDB_CUDA(cudaSetDevice(s->device));
         SDB_CUDA(cudaStreamSynchronize(s->stream));
     }
     for (int r = 0; r < world; ++r) {
-        StateImpl& src = *shards[r];
-        const uint32_t own = swapped_bits(static_cast<uint64_t>(r), src.n_local, ex);
-        for (uint32_t c = 0; c < (1u << gp); ++c) {
-            const int peer = static_cast<int>(with_bits(static_cast<uint64_t>(r), src.n_local, ex, c));
-            StateImpl& dst = *shards[peer];
-            // B_r[c] -> A_peer[own]: the peer receives rank r's chunk at r's swapped bits
-            SDB_CUDA(cudaSetDevice(src.device));
-            SDB_CUDA(cudaMemcpyPeerAsync(dst.amps + 2 * chunk * own, dst.device, src.xbuf + 2 * chunk * c,
-                                         src.device, 16 * chunk, src.stream));
+        StateImpl& dst = *shards[r];
+        // rank r receives, for each route, the peer's chunk destined for it
+        for (const Route& rt : exchange_routes(dst.n_local, dst.n, r, ex)) {
+            StateImpl& src = *shards[rt.peer];
+            // the peer's matching route towards r names the chunk it sends
+            uint64_t peer_send = 0;
+            for (const Route& pr : exchange_routes(src.n_local, src.n, rt.peer, ex)) {
+                if (pr.peer == r) peer_send = pr.send_off;
+            }
+            SDB_CUDA(cudaSetDevice(dst.device));
+            SDB_CUDA(cudaMemcpyPeerAsync(dst.amps + 2 * rt.recv_off, dst.device, src.xbuf + 2 * peer_send, src.device,
+                                         16 * rt.count, dst.stream));
         }
     }
     for (StateImpl* s : shards) {

@@ -13,6 +13,14 @@ void nccl_attach(StateImpl& s, const unsigned char id[128]);
 void nccl_detach(StateImpl& s);
 // sum of v over all ranks of the state's communicator
 double nccl_sum(StateImpl& s, double v);
+// Chunk routing of one exchange for `rank` (offsets and counts in amplitudes):
+// send B[send_off, +count) to `peer`, receive into A[recv_off, +count);
+// peer == rank is a local copy. Both transports use exactly this.
+struct Route {
+    int peer;
+    uint64_t send_off, recv_off, count;
+};
+std::vector<Route> exchange_routes(int n_local, int n, int rank, const ExchangeSpec& ex);
 // B = s.xbuf (already stored through sigma) -> A = s.amps, stream-ordered
 void exchange_nccl(StateImpl& s, const ExchangeSpec& ex);
 // same routing for shards driven by one process (shards[r] = rank r)

@@ -590,3 +590,15 @@ class LocalShards:
         arr = (C.c_void_p * self.world)(*[s._s.value for s in self.shards])
         check(A.sd_local_canonicalize(arr, self.world))
         return np.concatenate([s.amplitudes() for s in self.shards])
+
+
+def exchange_routes(n_qubits: int, n_local: int, rank: int, swaps) -> List[Tuple[int, int, int, int]]:
+    """(peer, send_offset, recv_offset, count) of one remap for `rank`
+    (sd_exchange_routes; host-only)."""
+    flat = [int(v) for p in swaps for v in p]
+    arr = (C.c_int32 * max(1, len(flat)))(*flat)
+    cnt = C.c_size_t(0)
+    check(A.sd_exchange_routes(n_qubits, n_local, rank, arr, len(swaps), None, 0, C.byref(cnt)))
+    out = (A.Route * max(1, cnt.value))()
+    check(A.sd_exchange_routes(n_qubits, n_local, rank, arr, len(swaps), out, cnt.value, C.byref(cnt)))
+    return [(r.peer, r.send_offset, r.recv_offset, r.count) for r in out[:cnt.value]]

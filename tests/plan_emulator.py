@@ -39,8 +39,13 @@ def exchange_map(n: int, n_local: int, ex: dict):
     return pos
 
 
-def run_passes(a: np.ndarray, n: int, passes, dt: float) -> np.ndarray:
-    idx = np.arange(1 << n, dtype=np.uint64)
+def run_passes(a: np.ndarray, n: int, passes, dt: float, idx=None) -> np.ndarray:
+    """Apply passes to `a`, whose entry j has global index idx[j] (default:
+    the whole state). Every stage only pairs entries that differ in local
+    bits, so a rank's shard can be emulated on its own."""
+    if idx is None:
+        idx = np.arange(1 << n, dtype=np.uint64)
+    base = idx[0] if len(idx) else np.uint64(0)
     for p in passes:
         lpos = p["lpos"]
         for st in p["stages"]:
@@ -49,8 +54,8 @@ def run_passes(a: np.ndarray, n: int, passes, dt: float) -> np.ndarray:
                     if (st["mask"] >> j) & 1:
                         b = 1 << lpos[j]
                         lo = (idx & np.uint64(b)) == 0
-                        i0 = idx[lo]
-                        i1 = i0 | np.uint64(b)
+                        i0 = (idx[lo] - base).astype(np.int64)
+                        i1 = i0 + b
                         x, y = a[i0].copy(), a[i1].copy()
                         a[i0], a[i1] = x + y, x - y
             elif st["kind"] == "cx":
@@ -60,8 +65,8 @@ def run_passes(a: np.ndarray, n: int, passes, dt: float) -> np.ndarray:
                         T |= 1 << lpos[j]
                 cb = lpos[st["ctrl_local"]] if st["ctrl_local"] >= 0 else st["ctrl_phys"]
                 on = ((idx >> np.uint64(cb)) & np.uint64(1)) == 1
-                src = np.where(on, idx ^ np.uint64(T), idx)
-                a = a[src]
+                src = np.where(on, idx ^ np.uint64(T), idx) - base
+                a = a[src.astype(np.int64)]
             else:
                 q = _popcount(idx & np.uint64(st["s1"])) + 2 * _popcount(idx & np.uint64(st["s2"]))
                 cz = np.zeros_like(idx)
@@ -70,7 +75,7 @@ def run_passes(a: np.ndarray, n: int, passes, dt: float) -> np.ndarray:
                 q = (q + 2 * cz) & np.uint64(3)
                 a = a * (1j ** q.astype(np.int64))
                 if st["terms"]:
-                    ang = np.zeros(1 << n)
+                    ang = np.zeros(len(idx))
                     for mask, c, s in st["terms"]:
                         par = _popcount(idx & np.uint64(mask)) & np.uint64(1)
                         ang += np.where(par == 1, -c * s, c * s)

@@ -172,23 +172,136 @@ __device__ void wht_table(double* __restrict__ tab, int bits) {
     }
 }
 
-// Per-tile tables of the pass's table point, built before any amplitude of
-// the tile is loaded. Full mode: angle table A[u] from the term segments,
-// WHT over the table_bits compact coordinates (phi/(-dt) per local index).
-// Factor mode: one angle table per factor, WHT each, then complex tables
-// E_f = exp(-i dt theta_f) (E_0 carries table_scale).
+// One factor table built by one warp, no block barriers: entry u = lane +
+// 32 j (j < M per lane). A[u] from the factor's segment of u (host index
+// fac_seg), WHT over register bits in place and over lane bits with
+// shuffles, then E[u] = exp(-i dt theta(u)) (times sc) into the
+// amplitude-swizzled complex table.
+template <int M>
+__device__ __forceinline__ void warp_factor_table(double2* __restrict__ E, const PlanDev& plan, const PointDev& pt,
+                                                  int f, uint64_t full, double neg_dt, double sc) {
+    const int lane = threadIdx.x & 31;
+    const int bits = pt.fac_bits[f];
+    const int size = 1 << bits;
+    const uint64_t* zh = plan.term_hmask + pt.term_off;
+    const double* cf = plan.term_coeffs + pt.term_off;
+    const int* seg_of = plan.fac_seg + pt.fac_soff[f];
+    double w[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+        const int u = lane + 32 * j;
+        double acc = 0.0;
+        if (u < size) {
+            const int sg = __ldg(seg_of + u);
+            if (sg >= 0) {
+                const SegDev d = plan.segs[pt.seg_off + sg];
+                for (int q = d.begin; q < d.end; ++q) {
+                    const uint64_t par = __popcll(full & __ldg(zh + q)) & 1ull;
+                    acc += __longlong_as_double(__double_as_longlong(__ldg(cf + q)) ^ static_cast<long long>(par << 63));
+                }
+            }
+        }
+        w[j] = acc;
+    }
+    // register bits (u bits 5..)
+#pragma unroll
+    for (int jb = 0; (1 << jb) < M; ++jb)
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            if ((j >> jb) & 1) continue;
+            const double x = w[j], y = w[j | (1 << jb)];
+            w[j] = x + y;
+            w[j | (1 << jb)] = x - y;
+        }
+    // lane bits (u bits 0..4)
+    for (int lb = 0; lb < 5 && lb < bits; ++lb) {
+        const bool hi = (lane >> lb) & 1;
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            const double o = __shfl_xor_sync(0xffffffffu, w[j], 1 << lb);
+            w[j] = hi ? o - w[j] : w[j] + o;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+        const int u = lane + 32 * j;
+        if (u < size) {
+            double sn, cs;
+            phase_sincos(neg_dt * w[j], &sn, &cs);
+            E[swz(static_cast<uint32_t>(u))] = make_double2(cs * sc, sn * sc);
+        }
+    }
+}
+
+// Same table built by one thread (CTAs narrower than a warp per factor, i.e.
+// tiny tiles): theta lives in E[.].x during the transform.
+__device__ void serial_factor_table(double2* __restrict__ E, const PlanDev& plan, const PointDev& pt, int f,
+                                    uint64_t full, double neg_dt, double sc) {
+    const int size = 1 << pt.fac_bits[f];
+    const uint64_t* zh = plan.term_hmask + pt.term_off;
+    const double* cf = plan.term_coeffs + pt.term_off;
+    const int* seg_of = plan.fac_seg + pt.fac_soff[f];
+    for (int u = 0; u < size; ++u) {
+        double acc = 0.0;
+        const int sg = __ldg(seg_of + u);
+        if (sg >= 0) {
+            const SegDev d = plan.segs[pt.seg_off + sg];
+            for (int q = d.begin; q < d.end; ++q) {
+                const uint64_t par = __popcll(full & __ldg(zh + q)) & 1ull;
+                acc += __longlong_as_double(__double_as_longlong(__ldg(cf + q)) ^ static_cast<long long>(par << 63));
+            }
+        }
+        E[swz(static_cast<uint32_t>(u))].x = acc;
+    }
+    for (int h = 1; h < size; h <<= 1)
+        for (int u = 0; u < size; ++u) {
+            if (u & h) continue;
+            const uint32_t i0 = swz(static_cast<uint32_t>(u)), i1 = swz(static_cast<uint32_t>(u | h));
+            const double x = E[i0].x, y = E[i1].x;
+            E[i0].x = x + y;
+            E[i1].x = x - y;
+        }
+    for (int u = 0; u < size; ++u) {
+        const uint32_t i = swz(static_cast<uint32_t>(u));
+        double sn, cs;
+        phase_sincos(neg_dt * E[i].x, &sn, &cs);
+        E[i] = make_double2(cs * sc, sn * sc);
+    }
+}
+
+// Per-tile tables of the pass's table point, built while the tile's loads
+// are in flight. Factor mode: warp f builds factor f's complex table
+// E_f = exp(-i dt theta_f) (E_0 carries table_scale) -- two block barriers
+// per tile. Full mode: angle table A[u] from the term segments, WHT over the
+// table_bits compact coordinates (phi/(-dt) per local index).
 template <int NT>
 __device__ void build_tables(double* __restrict__ tab, const PlanDev& plan, const PointDev& pt, uint64_t full,
                              double neg_dt, double tscale) {
     const int tid = threadIdx.x;
-    const bool fac = pt.n_fac > 0;
     __syncthreads();  // previous tile's readers are done with tab
-    if (fac) {
-        for (int f = 0; f < pt.n_fac; ++f)
-            for (int u = tid; u < (1 << pt.fac_bits[f]); u += NT) tab[pt.fac_doff[f] + u] = 0.0;
-    } else {
-        for (int u = tid; u < (1 << pt.table_bits); u += NT) tab[u] = 0.0;
+    if (pt.n_fac > 0) {
+        if (NT < 32 * 3) {  // narrow CTA (tiny tiles): one thread per factor
+            if (tid < pt.n_fac) {
+                serial_factor_table(reinterpret_cast<double2*>(tab + pt.fac_coff[tid]), plan, pt, tid, full, neg_dt,
+                                    tid == 0 ? tscale : 1.0);
+            }
+            __syncthreads();
+            return;
+        }
+        const int f = tid >> 5;
+        if (f < pt.n_fac) {
+            double2* const E = reinterpret_cast<double2*>(tab + pt.fac_coff[f]);
+            const double sc = f == 0 ? tscale : 1.0;
+            const int b = pt.fac_bits[f];
+            if (b <= 5) warp_factor_table<1>(E, plan, pt, f, full, neg_dt, sc);
+            else if (b == 6) warp_factor_table<2>(E, plan, pt, f, full, neg_dt, sc);
+            else if (b == 7) warp_factor_table<4>(E, plan, pt, f, full, neg_dt, sc);
+            else warp_factor_table<8>(E, plan, pt, f, full, neg_dt, sc);  // b <= kMaxFacBits = 8
+        }
+        __syncthreads();
+        return;
     }
+    for (int u = tid; u < (1 << pt.table_bits); u += NT) tab[u] = 0.0;
     __syncthreads();
     const uint64_t* zh = plan.term_hmask + pt.term_off;
     const double* cf = plan.term_coeffs + pt.term_off;
@@ -199,25 +312,10 @@ __device__ void build_tables(double* __restrict__ tab, const PlanDev& plan, cons
             const uint64_t par = __popcll(full & __ldg(zh + q)) & 1ull;
             acc += __longlong_as_double(__double_as_longlong(__ldg(cf + q)) ^ static_cast<long long>(par << 63));
         }
-        tab[(fac ? pt.fac_doff[sg.fac] : 0) + tsw(sg.u)] = acc;
+        tab[tsw(sg.u)] = acc;
     }
     __syncthreads();
-    if (!fac) {
-        wht_table<NT>(tab, pt.table_bits);
-        return;
-    }
-    for (int f = 0; f < pt.n_fac; ++f) wht_table<NT>(tab + pt.fac_doff[f], pt.fac_bits[f]);
-    for (int f = 0; f < pt.n_fac; ++f) {
-        const double sc = f == 0 ? tscale : 1.0;
-        double2* const E = reinterpret_cast<double2*>(tab + pt.fac_coff[f]);
-        const double* const th = tab + pt.fac_doff[f];
-        for (int x = tid; x < (1 << pt.fac_bits[f]); x += NT) {
-            double sn, cs;
-            phase_sincos(neg_dt * th[tsw(static_cast<uint32_t>(x))], &sn, &cs);
-            E[swz(static_cast<uint32_t>(x))] = make_double2(cs * sc, sn * sc);
-        }
-    }
-    __syncthreads();
+    wht_table<NT>(tab, pt.table_bits);
 }
 
 template <int K, int RB>

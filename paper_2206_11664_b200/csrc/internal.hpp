@@ -128,7 +128,7 @@ struct PointDev {
     int n_fac;
     uint32_t fac_mask[3];
     int fac_bits[3];
-    int fac_doff[3];  // angle scratch of factor f: double offset in the table region
+    int fac_soff[3];  // factor f: offset of its 2^b segment index (PlanDev::fac_seg, -1 = no term)
     int fac_coff[3];  // complex table of factor f: double offset (even) in the table region
 };
 
@@ -176,6 +176,7 @@ struct PlanDev {
     const uint64_t* term_hmask; // outer (physical) part of each term's z-mask
     const uint32_t* term_lmask; // local-coordinate part (direct mode)
     const double* term_coeffs;  // c_t * dt_scale; the kernel multiplies by -dt
+    const int* fac_seg;         // factor mode: compact index -> segment (relative to the point), -1 if none
 };
 
 // --------------------------------------------------------------- handles

@@ -101,7 +101,7 @@ std::vector<int> thread_order(uint32_t others) {
 // term's local part spans two sets (connected components of the "appear in
 // one term" relation, first-fit-decreasing into bins). Empty result: no such
 // cover, use the full angle table with a sincos per amplitude.
-constexpr int kMaxFacBits = 9;
+constexpr int kMaxFacBits = 8;
 std::vector<uint32_t> factor_cover(const std::vector<uint32_t>& us, uint32_t tm) {
     std::vector<int> parent(32);
     for (int i = 0; i < 32; ++i) parent[i] = i;
@@ -384,10 +384,6 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                         for (int f = 0; f < pt.n_fac; ++f) {
                             pt.fac_mask[f] = facs[f];
                             pt.fac_bits[f] = std::popcount(facs[f]);
-                            pt.fac_doff[f] = off;
-                            off += std::max(2, 1 << pt.fac_bits[f]);
-                        }
-                        for (int f = 0; f < pt.n_fac; ++f) {
                             pt.fac_coff[f] = off;
                             off += 2 * (1 << pt.fac_bits[f]);
                         }
@@ -420,6 +416,15 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                         i = j;
                     }
                     pt.n_seg = static_cast<int>(A.segs.size()) - pt.seg_off;
+                    for (int f = 0; f < pt.n_fac; ++f) {
+                        pt.fac_soff[f] = static_cast<int>(A.fac_seg.size());
+                        const size_t base = A.fac_seg.size();
+                        A.fac_seg.resize(base + (size_t(1) << pt.fac_bits[f]), -1);
+                        for (int sg = 0; sg < pt.n_seg; ++sg) {
+                            const SegDev& d = A.segs[pt.seg_off + sg];
+                            if (d.fac == f) A.fac_seg[base + d.u] = sg;
+                        }
+                    }
                     for (const T& t : sorted) {
                         A.term_hmask.push_back(t.zh);
                         A.term_lmask.push_back(0);

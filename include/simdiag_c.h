@@ -228,6 +228,14 @@ sd_status sd_plan_set_profiling(sd_plan* p, int enable);
 sd_status sd_plan_kernel_times(sd_plan* p, double* ms_by_class, uint64_t* launches_by_class,
                                double* bytes_by_class, int n_classes);
 
+/* Plans for large shards (default n_local >= 22; SDB_JIT=0/1 overrides) run
+ * each pass as a kernel specialised for its micro-program, generated and
+ * compiled for sm_100a with NVRTC at plan time. Host-only check: plan the
+ * first step for an n-qubit state over `world` ranks and compile every
+ * distinct pass program (no device needed). */
+sd_status sd_jit_compile_preview(int n_qubits, int world, const sd_group_desc* groups, size_t n_groups,
+                                 const sd_plan_options* opts, size_t* n_programs);
+
 /* ------------------------------------------------------------------ */
 /* Multi-rank exchange (NCCL over NVLink; one process per GPU)          */
 /* ------------------------------------------------------------------ */

@@ -13,6 +13,7 @@
 
 #include "../plan/lower.hpp"
 #include "exchange.hpp"
+#include "../cuda/jit.hpp"
 #include "../plan/planner.hpp"
 #include "guard.hpp"
 
@@ -32,6 +33,8 @@ struct StepExec {
     std::vector<sdb::PassDev> host_passes;
     std::vector<int> pass_class;  // 0 fused, 1 diagonal-only
     std::vector<int> seg_first, seg_count;
+    std::vector<void*> jit_fn;    // specialised kernel per pass (nullptr = interpreter)
+    std::vector<size_t> smem;     // dynamic shared memory per pass
     sdb::PlanDev dev{};
     void* dev_block = nullptr;
     std::string program;
@@ -178,6 +181,12 @@ void upload_step(sd_plan& p, StepExec& E, const sdb::StepPlan& combined) {
     sdb::HostPlanArrays A = sdb::lower_plan(combined, s.n_local, kTableThreshold, 4);
     E.pass_class = A.pass_class;
     E.program = sdb::describe_program(A);
+    E.jit_fn.assign(A.passes.size(), nullptr);
+    E.smem.resize(A.passes.size());
+    for (size_t i = 0; i < A.passes.size(); ++i) E.smem[i] = sdb::tile_pass_smem(A.passes[i]);
+    if (sdb::jit_wanted(s.n_local)) {
+        E.jit_fn = sdb::jit_pass_kernels(A, s.device);
+    }
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t sizes[] = {
         al(std::max<size_t>(1, A.passes.size()) * sizeof(sdb::PassDev)),
@@ -307,7 +316,12 @@ void run_segment(sd_plan& p, StepExec& E, size_t seg, double dt) {
     for (int i = first; i < first + count; ++i) {
         const bool to_buf = exch && i == first + count - 1;
         record_start(p, E.pass_class[i]);
-        sdb::launch_tile_pass(s, E.host_passes[i], i, E.dev, dt, rank_bits, to_buf ? s.xbuf : nullptr);
+        if (E.jit_fn[i]) {
+            sdb::launch_tile_pass_jit(E.jit_fn[i], s, E.host_passes[i], i, E.dev, dt, rank_bits,
+                                      to_buf ? s.xbuf : nullptr, E.smem[i]);
+        } else {
+            sdb::launch_tile_pass(s, E.host_passes[i], i, E.dev, dt, rank_bits, to_buf ? s.xbuf : nullptr);
+        }
         record_end(p, bytes);
         bump(s, s.amps_count(), s.amps_count());
         if (p.profiling && p.ev_used >= 4096) harvest(p);
@@ -1053,6 +1067,33 @@ sd_status sd_exchange_routes(int n, int n_local, int rank, const int32_t* swaps,
         for (size_t i = 0; i < routes.size() && i < cap && out; ++i) {
             out[i] = sd_route{routes[i].peer, routes[i].send_off, routes[i].recv_off, routes[i].count};
         }
+    });
+}
+
+sd_status sd_jit_compile_preview(int n, int world, const sd_group_desc* groups, size_t n_groups,
+                                 const sd_plan_options* opts, size_t* n_programs) {
+    return guard([&] {
+        require(n_groups == 0 || groups != nullptr, "null group array");
+        require(world >= 1 && (world & (world - 1)) == 0, "world size must be a power of two");
+        sd_plan_options o{};
+        if (opts) o = *opts;
+        else sd_plan_options_default(&o);
+        const int n_local = n - std::countr_zero(static_cast<unsigned>(world));
+        std::vector<sdb::GroupSpec> gs;
+        for (size_t i = 0; i < n_groups; ++i) gs.push_back(spec_of(groups[i]));
+        std::vector<int> phys(n);
+        std::iota(phys.begin(), phys.end(), 0);
+        int k = o.tile_qubits > 0 ? o.tile_qubits : 12;
+        k = std::min({k, sdb::max_tile_qubits(), n_local});
+        const auto ops = sdb::step_ops(gs, n, o.order, std::max(1, k - 3));
+        const sdb::ShardedStep ss = sdb::plan_sharded_step(ops, gs, n_local, k, 3, phys);
+        sdb::StepPlan combined;
+        combined.tile_qubits = k;
+        for (const sdb::Segment& sg : ss.segs)
+            for (const sdb::PassPlan& pp : sg.plan.passes) combined.passes.push_back(pp);
+        const sdb::HostPlanArrays A = sdb::lower_plan(combined, n_local, kTableThreshold, 4);
+        const size_t np = sdb::jit_compile_only(A);
+        if (n_programs) *n_programs = np;
     });
 }
 

@@ -1,0 +1,26 @@
+// Run-time specialised tile-pass kernels (jit.cpp).
+#pragma once
+
+#include <cstddef>
+#include <vector>
+
+#include "../internal.hpp"
+#include "../plan/lower.hpp"
+
+namespace sdb {
+
+// Whether plans for a state of this shard size use specialised kernels
+// (SDB_JIT=0/1 overrides; default: n_local >= 22, where compile time amortises).
+bool jit_wanted(int n_local);
+// CUfunction of every pass's specialised kernel (distinct programs compiled in
+// parallel, cached in-process and on disk).
+std::vector<void*> jit_pass_kernels(const HostPlanArrays& A, int device);
+void launch_tile_pass_jit(void* fn, StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& plan, double dt,
+                          uint64_t rank_bits, double* out, size_t smem);
+// Host-only: generate and NVRTC-compile every distinct pass program of A
+// (no device needed); returns the number of distinct programs.
+size_t jit_compile_only(const HostPlanArrays& A);
+// dynamic shared memory of a tile pass (same for both kernel kinds)
+size_t tile_pass_smem(const PassDev& ph);
+
+}  // namespace sdb

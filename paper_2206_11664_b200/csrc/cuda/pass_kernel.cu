@@ -1,717 +1,48 @@
-// Fused Clifford/diagonal tile pass for sm_100a (north star (a) + (b)).
-//
-// Two persistent CTAs per SM walk the tiles of a pass. A tile of 2^k
-// amplitudes is loaded from HBM straight into registers (16 amplitudes per
-// thread, 128-byte coalesced lines), transformed by the pass's host-compiled
-// micro-program (internal.hpp) and stored straight back. While one CTA is in
-// its compute phase (register butterflies for Hadamard layers, shared-memory
-// transposes between register configs with pending CNOT index maps applied
-// on the write side, pointwise quarter-turn phases and exp(-i dt Lambda)
-// with a per-tile Walsh-Hadamard angle table) the other CTA's loads and
-// stores keep HBM busy; the CTA-level double buffering costs no extra
-// shared-memory staging of the loaded tile.
-//
-// Reference semantics per op: proj/src/statevector.cpp:156-286
-// (apply_hadamard, apply_batched_cnot, apply_phase_layer, apply_diagonal_exp).
+// Fused Clifford/diagonal tile pass: the compiled interpreter. The device
+// code lives in pass_device.cuh; this kernel feeds its ops from the staged
+// micro-program. Large states can instead run a kernel specialised for the
+// pass's program at plan time (jit.cpp).
 #include <cuda_runtime.h>
 
 #include "../internal.hpp"
+#include "jit.hpp"
+#include "pass_device.cuh"
 
 namespace sdb {
 
 namespace {
 
-// 16-byte amplitude slots (host_swz twin, see internal.hpp).
-__host__ __device__ constexpr uint32_t swz(uint32_t l) {
-    return l ^ ((l >> 3) & 7u) ^ ((l >> 6) & 7u) ^ ((l >> 9) & 7u);
-}
-// 8-byte angle-table slots: XOR the low 4 bits with bits 4-7 and 8-11 so the
-// radix-16 table butterflies (lanes 16 entries apart) spread over the banks.
-__device__ __forceinline__ uint32_t tsw(uint32_t u) { return u ^ ((u >> 4) & 15u) ^ ((u >> 8) & 15u); }
+using dev::Cfg;
+using dev::kTbaseChunks;
 
-// gather the bits of v selected by mask into the low bits (ascending)
-__device__ __forceinline__ uint32_t pext32(uint32_t v, uint32_t mask) {
-    uint32_t out = 0, bit = 1;
-    for (uint32_t m = mask; m; m &= m - 1, bit <<= 1) {
-        if (v & m & (~m + 1u)) out |= bit;
-    }
-    return out;
-}
-
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
-}
-
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-
-// sin/cos of a phase. Cody-Waite reduction by pi/2 and the fdlibm kernels on
-// [-pi/4, pi/4] (errors < 1 ulp); arguments beyond 2^20 take CUDA's sincos.
-__device__ __forceinline__ void phase_sincos(double x, double* s, double* c) {
-    if (fabs(x) > 1048576.0) {
-        sincos(x, s, c);
-        return;
-    }
-    const double q = rint(x * 0.63661977236758134308);
-    double r = fma(-q, 1.57079632673412561417e+00, x);
-    r = fma(-q, 6.07710050650619224932e-11, r);
-    r = fma(-q, 2.02226624879595063154e-21, r);
-    const double z = r * r;
-    const double ps = fma(z, fma(z, fma(z, fma(z, fma(z, 1.58969099521155010221e-10, -2.50507602534068634195e-08),
-                                                2.75573137070700676789e-06),
-                                        -1.98412698298579493134e-04),
-                                8.33333333332248946124e-03),
-                          -1.66666666666666324348e-01);
-    const double sn = fma(r * z, ps, r);
-    const double pc = z * fma(z, fma(z, fma(z, fma(z, fma(z, -1.13596475577881948265e-11, 2.08757232129817482790e-09),
-                                                   -2.75573143513906633035e-07),
-                                           2.48015872894767294178e-05),
-                                   -1.38888888888741095749e-03),
-                             4.16666666666666019037e-02);
-    const double hz = 0.5 * z;
-    const double w = 1.0 - hz;
-    const double cs = w + (((1.0 - w) - hz) + z * pc);
-    const int quad = static_cast<int>(static_cast<long long>(q) & 3);
-    double so = sn, co = cs;
-    if (quad & 1) {
-        so = cs;
-        co = -sn;
-    }
-    if (quad & 2) {
-        so = -so;
-        co = -co;
-    }
-    *s = so;
-    *c = co;
-}
-
-// Butterflies on the register coordinates selected by the compile-time mask M.
-template <int R, int M>
-__device__ __forceinline__ void bfly(double2 (&v)[1 << R]) {
-#pragma unroll
-    for (int j = 0; j < R; ++j) {
-        if (!((M >> j) & 1)) continue;
-#pragma unroll
-        for (int s = 0; s < (1 << R); ++s) {
-            if ((s >> j) & 1) continue;
-            const double2 a = v[s], d = v[s | (1 << j)];
-            v[s] = cadd(a, d);
-            v[s | (1 << j)] = csub(a, d);
-        }
-    }
-}
-
-template <int R>
-__device__ __forceinline__ void bfly_dispatch(double2 (&v)[1 << R], uint32_t mask) {
-    switch (mask & ((1u << R) - 1u)) {
-#define SDB_B(M) \
-    case M:      \
-        if constexpr (M < (1 << R)) bfly<R, M>(v); \
-        break;
-        SDB_B(1) SDB_B(2) SDB_B(3) SDB_B(4) SDB_B(5) SDB_B(6) SDB_B(7) SDB_B(8) SDB_B(9) SDB_B(10) SDB_B(11)
-        SDB_B(12) SDB_B(13) SDB_B(14) SDB_B(15)
-#undef SDB_B
-        default: break;
-    }
-}
-
-// One radix-2^RB round of the in-place table WHT over compact coordinates
-// LO..LO+RB-1 (the swizzle is linear: slot(base | s << LO) = tsw(base) ^ tsw(s << LO)).
-template <int NT, int LO, int RB>
-__device__ __forceinline__ void wht_round(double* __restrict__ tab, int size) {
-    constexpr int M = 1 << RB;
-    const int groups = size >> RB;
-    constexpr uint32_t lowm = (1u << LO) - 1u;
-    for (int gi = threadIdx.x; gi < groups; gi += NT) {
-        const uint32_t g = static_cast<uint32_t>(gi);
-        const uint32_t b = tsw(((g >> LO) << (LO + RB)) | (g & lowm));
-        double w[M];
-#pragma unroll
-        for (int s = 0; s < M; ++s) w[s] = tab[b ^ tsw(static_cast<uint32_t>(s) << LO)];
-#pragma unroll
-        for (int j = 0; j < RB; ++j)
-#pragma unroll
-            for (int s = 0; s < M; ++s) {
-                if ((s >> j) & 1) continue;
-                const double a = w[s], d = w[s | (1 << j)];
-                w[s] = a + d;
-                w[s | (1 << j)] = a - d;
-            }
-#pragma unroll
-        for (int s = 0; s < M; ++s) tab[b ^ tsw(static_cast<uint32_t>(s) << LO)] = w[s];
-    }
-}
-
-// Radix-4 rounds (the tables are built while the tile's loads are in flight,
-// so the round keeps few registers live).
-template <int NT, int LO, int BITS>
-__device__ __forceinline__ void wht_rounds(double* __restrict__ tab) {
-    if constexpr (LO < BITS) {
-        constexpr int RB = BITS - LO >= 2 ? 2 : 1;
-        wht_round<NT, LO, RB>(tab, 1 << BITS);
-        __syncthreads();
-        wht_rounds<NT, LO + RB, BITS>(tab);
-    }
-}
-
-template <int NT, int BITS>
-__device__ __forceinline__ void wht_fixed(double* __restrict__ tab) {
-    wht_rounds<NT, 0, BITS>(tab);
-}
-
-// In-place WHT of a 2^bits table (tsw-swizzled); ends with a barrier.
-template <int NT>
-__device__ void wht_table(double* __restrict__ tab, int bits) {
-    switch (bits) {
-#define SDB_W(BB) \
-    case BB: wht_fixed<NT, BB>(tab); break;
-        SDB_W(1) SDB_W(2) SDB_W(3) SDB_W(4) SDB_W(5) SDB_W(6) SDB_W(7) SDB_W(8) SDB_W(9) SDB_W(10) SDB_W(11)
-        SDB_W(12)
-#undef SDB_W
-        default: break;
-    }
-}
-
-// One factor table built by one warp, no block barriers: entry u = lane +
-// 32 j (j < M per lane). A[u] from the factor's segment of u (host index
-// fac_seg), WHT over register bits in place and over lane bits with
-// shuffles, then E[u] = exp(-i dt theta(u)) (times sc) into the
-// amplitude-swizzled complex table.
-template <int M>
-__device__ __forceinline__ void warp_factor_table(double2* __restrict__ E, const PlanDev& plan, const PointDev& pt,
-                                                  int f, uint64_t full, double neg_dt, double sc) {
-    const int lane = threadIdx.x & 31;
-    const int bits = pt.fac_bits[f];
-    const int size = 1 << bits;
-    const uint64_t* zh = plan.term_hmask + pt.term_off;
-    const double* cf = plan.term_coeffs + pt.term_off;
-    const int* seg_of = plan.fac_seg + pt.fac_soff[f];
-    double w[M];
-#pragma unroll
-    for (int j = 0; j < M; ++j) {
-        const int u = lane + 32 * j;
-        double acc = 0.0;
-        if (u < size) {
-            const int sg = __ldg(seg_of + u);
-            if (sg >= 0) {
-                const SegDev d = plan.segs[pt.seg_off + sg];
-                for (int q = d.begin; q < d.end; ++q) {
-                    const uint64_t par = __popcll(full & __ldg(zh + q)) & 1ull;
-                    acc += __longlong_as_double(__double_as_longlong(__ldg(cf + q)) ^ static_cast<long long>(par << 63));
-                }
+struct Interpreter {
+    template <class Ctx, int NR>
+    __device__ __forceinline__ void operator()(Ctx& ctx, double2 (&v)[NR]) const {
+        const int n_ops = ctx.P.n_ops;
+        for (int oi = 0; oi < n_ops; ++oi) {
+            const MicroOpDev& op = ctx.s_ops[oi];
+            const int kind = op.kind;
+            if (kind == kOpLoad) {
+                ctx.load(ctx.cfg_of(op), v);
+            } else if (kind == kOpCfg) {
+                ctx.cfg(op, ctx.cfg_of(op), v);
+            } else if (kind == kOpBfly) {
+                dev::bfly_dispatch<Ctx::R>(v, op.mask);
+            } else if (kind == kOpPoint) {
+                ctx.point(op, v);
+            } else {
+                ctx.store(op, v);
             }
         }
-        w[j] = acc;
     }
-    // register bits (u bits 5..)
-#pragma unroll
-    for (int jb = 0; (1 << jb) < M; ++jb)
-#pragma unroll
-        for (int j = 0; j < M; ++j) {
-            if ((j >> jb) & 1) continue;
-            const double x = w[j], y = w[j | (1 << jb)];
-            w[j] = x + y;
-            w[j | (1 << jb)] = x - y;
-        }
-    // lane bits (u bits 0..4)
-    for (int lb = 0; lb < 5 && lb < bits; ++lb) {
-        const bool hi = (lane >> lb) & 1;
-#pragma unroll
-        for (int j = 0; j < M; ++j) {
-            const double o = __shfl_xor_sync(0xffffffffu, w[j], 1 << lb);
-            w[j] = hi ? o - w[j] : w[j] + o;
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < M; ++j) {
-        const int u = lane + 32 * j;
-        if (u < size) {
-            double sn, cs;
-            phase_sincos(neg_dt * w[j], &sn, &cs);
-            E[swz(static_cast<uint32_t>(u))] = make_double2(cs * sc, sn * sc);
-        }
-    }
-}
-
-// Same table built by one thread (CTAs narrower than a warp per factor, i.e.
-// tiny tiles): theta lives in E[.].x during the transform.
-__device__ void serial_factor_table(double2* __restrict__ E, const PlanDev& plan, const PointDev& pt, int f,
-                                    uint64_t full, double neg_dt, double sc) {
-    const int size = 1 << pt.fac_bits[f];
-    const uint64_t* zh = plan.term_hmask + pt.term_off;
-    const double* cf = plan.term_coeffs + pt.term_off;
-    const int* seg_of = plan.fac_seg + pt.fac_soff[f];
-    for (int u = 0; u < size; ++u) {
-        double acc = 0.0;
-        const int sg = __ldg(seg_of + u);
-        if (sg >= 0) {
-            const SegDev d = plan.segs[pt.seg_off + sg];
-            for (int q = d.begin; q < d.end; ++q) {
-                const uint64_t par = __popcll(full & __ldg(zh + q)) & 1ull;
-                acc += __longlong_as_double(__double_as_longlong(__ldg(cf + q)) ^ static_cast<long long>(par << 63));
-            }
-        }
-        E[swz(static_cast<uint32_t>(u))].x = acc;
-    }
-    for (int h = 1; h < size; h <<= 1)
-        for (int u = 0; u < size; ++u) {
-            if (u & h) continue;
-            const uint32_t i0 = swz(static_cast<uint32_t>(u)), i1 = swz(static_cast<uint32_t>(u | h));
-            const double x = E[i0].x, y = E[i1].x;
-            E[i0].x = x + y;
-            E[i1].x = x - y;
-        }
-    for (int u = 0; u < size; ++u) {
-        const uint32_t i = swz(static_cast<uint32_t>(u));
-        double sn, cs;
-        phase_sincos(neg_dt * E[i].x, &sn, &cs);
-        E[i] = make_double2(cs * sc, sn * sc);
-    }
-}
-
-// Per-tile tables of the pass's table point, built while the tile's loads
-// are in flight. Factor mode: warp f builds factor f's complex table
-// E_f = exp(-i dt theta_f) (E_0 carries table_scale) -- two block barriers
-// per tile. Full mode: angle table A[u] from the term segments, WHT over the
-// table_bits compact coordinates (phi/(-dt) per local index).
-template <int NT>
-__device__ void build_tables(double* __restrict__ tab, const PlanDev& plan, const PointDev& pt, uint64_t full,
-                             double neg_dt, double tscale) {
-    const int tid = threadIdx.x;
-    __syncthreads();  // previous tile's readers are done with tab
-    if (pt.n_fac > 0) {
-        if (NT < 32 * 3) {  // narrow CTA (tiny tiles): one thread per factor
-            if (tid < pt.n_fac) {
-                serial_factor_table(reinterpret_cast<double2*>(tab + pt.fac_coff[tid]), plan, pt, tid, full, neg_dt,
-                                    tid == 0 ? tscale : 1.0);
-            }
-            __syncthreads();
-            return;
-        }
-        const int f = tid >> 5;
-        if (f < pt.n_fac) {
-            double2* const E = reinterpret_cast<double2*>(tab + pt.fac_coff[f]);
-            const double sc = f == 0 ? tscale : 1.0;
-            const int b = pt.fac_bits[f];
-            if (b <= 5) warp_factor_table<1>(E, plan, pt, f, full, neg_dt, sc);
-            else if (b == 6) warp_factor_table<2>(E, plan, pt, f, full, neg_dt, sc);
-            else if (b == 7) warp_factor_table<4>(E, plan, pt, f, full, neg_dt, sc);
-            else warp_factor_table<8>(E, plan, pt, f, full, neg_dt, sc);  // b <= kMaxFacBits = 8
-        }
-        __syncthreads();
-        return;
-    }
-    for (int u = tid; u < (1 << pt.table_bits); u += NT) tab[u] = 0.0;
-    __syncthreads();
-    const uint64_t* zh = plan.term_hmask + pt.term_off;
-    const double* cf = plan.term_coeffs + pt.term_off;
-    for (int s = tid; s < pt.n_seg; s += NT) {
-        const SegDev sg = plan.segs[pt.seg_off + s];
-        double acc = 0.0;
-        for (int q = sg.begin; q < sg.end; ++q) {
-            const uint64_t par = __popcll(full & __ldg(zh + q)) & 1ull;
-            acc += __longlong_as_double(__double_as_longlong(__ldg(cf + q)) ^ static_cast<long long>(par << 63));
-        }
-        tab[tsw(sg.u)] = acc;
-    }
-    __syncthreads();
-    wht_table<NT>(tab, pt.table_bits);
-}
-
-template <int K, int RB>
-struct Cfg {
-    static constexpr int R = K < RB ? K : RB;
-    static constexpr int NR = 1 << R;        // amplitudes per thread
-    static constexpr int NT = 1 << (K - R);  // threads per CTA
-    static constexpr int N = 1 << K;
-    static constexpr int LO = K < 6 ? K : 6;
-    static constexpr int HI = K - LO;
-    static constexpr int MINB = K >= 12 ? 2 : 1;  // resident CTAs per SM the register budget is cut for
 };
-
-constexpr int kTbaseChunks = 4;  // outer bits covered by the tile-base tables: 4 x 7
 
 template <int K, int RB>
 __global__ void __launch_bounds__(Cfg<K, RB>::NT, Cfg<K, RB>::MINB)
 k_tile_pass(const double2* __restrict__ psi, double2* __restrict__ out, PlanDev plan, int pass_index, double neg_dt,
-            uint64_t rank_bits,
-            uint64_t n_tiles) {
-    using C = Cfg<K, RB>;
-    constexpr int R = C::R, NR = C::NR, NT = C::NT, N = C::N, LO = C::LO, HI = C::HI;
-    const PassDev& P = plan.passes[pass_index];
-    const int tid = threadIdx.x;
-    const int n_outer = P.n_outer;
-    const int n_ops = P.n_ops;
-    const int n_cfg = P.n_cfg;
-    const bool has_table = P.table_point >= 0;
-
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2* const buf = reinterpret_cast<double2*>(smem_raw);            // transpose buffer
-    double* const tab = reinterpret_cast<double*>(buf + N);               // angle table (if any)
-    const int tab_words = P.tab_words;
-    // The micro-ops are staged in shared memory (the planner caps a pass's
-    // length); per-thread config bases and QT tables are read through L1
-    // (a few words per thread per tile).
-    MicroOpDev* const s_ops = reinterpret_cast<MicroOpDev*>(tab + tab_words);
-    const uint32_t* const s_cfg = plan.cfg_tb + P.cfg_off;
-    const uint32_t* const s_qt = reinterpret_cast<const uint32_t*>(plan.qt_words + P.qt_off);
-    // store-side index tables (only for passes that store through a local bit
-    // permutation sigma, i.e. in front of a qubit-remap exchange)
-    uint64_t* const st_lo = reinterpret_cast<uint64_t*>(s_ops + n_ops);
-    uint64_t* const st_hi = st_lo + (1 << LO);
-    uint64_t* const st_tbase = st_hi + (1 << HI);  // [kTbaseChunks][128]
-    const bool store_perm = P.store_perm != 0;
-    __shared__ uint64_t off_lo[1 << LO];
-    __shared__ uint64_t off_hi[1 << HI];
-    __shared__ uint64_t s_tbase[kTbaseChunks][128];  // tile index (7 bits per chunk) -> outer offset
-    __shared__ uint32_t s_pl[3][64], s_ph[3][64];    // local index (low / high 6 bits) -> compact table index
-
-    // ---- stage the program and the index tables (once per launch)
-    {
-        const int4* src = reinterpret_cast<const int4*>(plan.ops + P.op_off);
-        int4* dst = reinterpret_cast<int4*>(s_ops);
-        const int words = n_ops * static_cast<int>(sizeof(MicroOpDev) / sizeof(int4));
-        for (int i = tid; i < words; i += NT) dst[i] = __ldg(src + i);
-    }
-    for (int i = tid; i < (1 << LO); i += NT) {
-        uint64_t o = 0;
-        for (int j = 0; j < LO; ++j)
-            if ((i >> j) & 1) o |= 1ull << P.lpos[j];
-        off_lo[i] = o;
-    }
-    for (int i = tid; i < (1 << HI); i += NT) {
-        uint64_t o = 0;
-        for (int j = 0; j < HI; ++j)
-            if ((i >> j) & 1) o |= 1ull << P.lpos[LO + j];
-        off_hi[i] = o;
-    }
-    for (int i = tid; i < kTbaseChunks * 128; i += NT) {
-        const int c = i >> 7, v = i & 127;
-        uint64_t o = 0, os = 0;
-        for (int j = 0; j < 7; ++j) {
-            const int q = 7 * c + j;
-            if (q < n_outer && ((v >> j) & 1)) {
-                o |= 1ull << P.opos[q];
-                os |= 1ull << P.st_opos[q];
-            }
-        }
-        s_tbase[c][v] = o;
-        if (store_perm) st_tbase[i] = os;
-    }
-    if (store_perm) {
-        for (int i = tid; i < (1 << LO); i += NT) {
-            uint64_t o = 0;
-            for (int j = 0; j < LO; ++j)
-                if ((i >> j) & 1) o |= 1ull << P.st_lpos[j];
-            st_lo[i] = o;
-        }
-        for (int i = tid; i < (1 << HI); i += NT) {
-            uint64_t o = 0;
-            for (int j = 0; j < HI; ++j)
-                if ((i >> j) & 1) o |= 1ull << P.st_lpos[LO + j];
-            st_hi[i] = o;
-        }
-    }
-    if (has_table) {
-        const PointDev& tp = plan.points[P.table_point];
-        const int nf = tp.n_fac > 0 ? tp.n_fac : 1;
-        for (int f = 0; f < nf; ++f) {
-            const uint32_t tm = tp.n_fac > 0 ? tp.fac_mask[f] : tp.table_mask;
-            const int nlo = __popc(tm & 63u);
-            for (int i = tid; i < 64; i += NT) {
-                const uint32_t lo = pext32(static_cast<uint32_t>(i), tm & 63u);
-                const uint32_t hi = pext32(static_cast<uint32_t>(i), tm >> 6) << nlo;
-                // factor tables hold complex entries in amplitude-swizzled slots
-                s_pl[f][i] = tp.n_fac > 0 ? swz(lo) : tsw(lo);
-                s_ph[f][i] = tp.n_fac > 0 ? swz(hi) : tsw(hi);
-            }
-        }
-    }
-    const double scale = P.scale;  // exact power of two
-    __syncthreads();
-
-    auto tile_base = [&](uint64_t t) {
-        uint64_t b = 0;
-#pragma unroll
-        for (int c = 0; c < kTbaseChunks; ++c) b |= s_tbase[c][(t >> (7 * c)) & 127];
-        return b;
-    };
-    auto off_of = [&](uint32_t l) -> uint64_t { return off_lo[l & ((1u << LO) - 1u)] | off_hi[l >> LO]; };
-
-    const uint64_t stride = gridDim.x;
-    for (uint64_t t = blockIdx.x; t < n_tiles; t += stride) {
-        const uint64_t base = tile_base(t);
-        const uint64_t full = rank_bits | base;
-        const double2* const g = psi + base;
-
-        double2 v[NR];
-        uint32_t tb = 0, swt = 0;  // local index / slot of this thread's register 0
-        uint32_t cidx = 0;         // local coordinate index of register coordinate j (byte j)
-        uint32_t swc[4] = {0, 0, 0, 0};
-        uint64_t coff[4] = {0, 0, 0, 0};
-        bool smem_busy = true;     // smem may still be read by other threads (sync before writing)
-
-        auto set_cfg = [&](const MicroOpDev& op) {
-            const uint32_t w = __ldg(s_cfg + op.arg * NT + tid);
-            tb = w & 0xffffu;
-            swt = w >> 16;
-            cidx = op.cidx;
-            swc[0] = op.swc01 & 0xffffu;
-            swc[1] = op.swc01 >> 16;
-            swc[2] = op.swc23 & 0xffffu;
-            swc[3] = op.swc23 >> 16;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) coff[j] = op.c_off[j];
-        };
-        auto phys_offsets = [&](uint64_t (&o)[NR]) {
-            o[0] = off_of(tb);
-#pragma unroll
-            for (int j = 0; j < R; ++j)
-#pragma unroll
-                for (int s = 0; s < (1 << j); ++s) o[s + (1 << j)] = o[s] | coff[j];
-        };
-
-        for (int oi = 0; oi < n_ops; ++oi) {
-            const MicroOpDev& op = s_ops[oi];
-            const int kind = op.kind;
-            if (kind == kOpLoad) {
-                set_cfg(op);
-                uint64_t o[NR];
-                phys_offsets(o);
-#pragma unroll
-                for (int s = 0; s < NR; ++s) v[s] = __ldcs(g + o[s]);
-                // Pull this CTA's next tile into L2 while the current one is
-                // transformed: HBM keeps streaming through the compute phase
-                // without holding registers or shared memory.
-                if (t + stride < n_tiles) {
-                    const double2* gn = psi + tile_base(t + stride);
-#pragma unroll
-                    for (int s = 0; s < NR; ++s) prefetch_l2(gn + o[s]);
-                }
-                // per-tile phase tables, built while the loads are in flight
-                if (has_table) build_tables<NT>(tab, plan, plan.points[P.table_point], full, neg_dt, P.table_scale);
-            } else if (kind == kOpCfg) {
-                if (smem_busy) __syncthreads();
-                if (op.perm >= 0) {
-                    const PermDev* pm = plan.perms + op.perm;
-                    uint32_t sb = 0;
-                    for (int j = 0; j < pm->n_ctrl; ++j)
-                        if ((full >> pm->ctrl_phys[j]) & 1ull) sb ^= pm->flip[j];
-                    uint32_t l[NR];
-                    l[0] = tb;
-#pragma unroll
-                    for (int j = 0; j < R; ++j)
-#pragma unroll
-                        for (int s = 0; s < (1 << j); ++s)
-                            l[s + (1 << j)] = l[s] | (1u << ((cidx >> (8 * j)) & 255u));
-#pragma unroll
-                    for (int s = 0; s < NR; ++s) {
-                        const uint32_t m = static_cast<uint32_t>(__ldg(&pm->lo[l[s] & 63u])) ^
-                                           static_cast<uint32_t>(__ldg(&pm->hi[l[s] >> 6])) ^ sb;
-                        buf[m] = v[s];
-                    }
-                } else {
-                    uint32_t a[NR];
-                    a[0] = swt;
-#pragma unroll
-                    for (int j = 0; j < R; ++j)
-#pragma unroll
-                        for (int s = 0; s < (1 << j); ++s) a[s + (1 << j)] = a[s] ^ swc[j];
-#pragma unroll
-                    for (int s = 0; s < NR; ++s) buf[a[s]] = v[s];
-                }
-                __syncthreads();
-                set_cfg(op);
-                {
-                    uint32_t a[NR];
-                    a[0] = swt;
-#pragma unroll
-                    for (int j = 0; j < R; ++j)
-#pragma unroll
-                        for (int s = 0; s < (1 << j); ++s) a[s + (1 << j)] = a[s] ^ swc[j];
-#pragma unroll
-                    for (int s = 0; s < NR; ++s) v[s] = buf[a[s]];
-                }
-                smem_busy = true;
-            } else if (kind == kOpBfly) {
-                bfly_dispatch<R>(v, op.mask);
-            } else if (kind == kOpPoint) {
-                const PointDev& pt = plan.points[op.arg];
-                const bool table = op.arg == P.table_point;
-                const bool scale_here = (op.mask & 1u) != 0;
-                const int n_terms = pt.n_terms;
-                uint32_t cb[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) cb[j] = 1u << ((cidx >> (8 * j)) & 255u);
-                // ---- quarter turns: q(tb ^ r_s) = q0 + sum_{j in s} dq_j + 2 QT(r_s)  (mod 4)
-                // (QT is a quadratic form: QT(a^b) = QT(a) + QT(b) + B(a,b), B bilinear)
-                uint32_t m2 = pt.s2L;
-                unsigned q0 = __popcll(full & pt.s1H) + 2u * __popcll(full & pt.s2H);
-                for (int j = 0; j < pt.n_lo; ++j) {
-                    const uint32_t wl = __ldg(plan.lo_pairs + pt.lo_off + j);
-                    if ((full >> (wl & 0xffu)) & 1ull) m2 ^= 1u << (wl >> 8);
-                }
-                for (int j = 0; j < pt.n_oo; ++j) {
-                    const uint64_t m = __ldg(plan.oo_pairs + pt.oo_off + j);
-                    if ((full & m) == m) q0 += 2u;
-                }
-                const uint32_t* qt = pt.qt_word >= 0 ? s_qt + 2 * pt.qt_word : nullptr;
-                auto qtb = [&](uint32_t l) -> unsigned { return qt ? (__ldg(qt + (l >> 5)) >> (l & 31u)) & 1u : 0u; };
-                const unsigned qt_tb = qtb(tb);
-                q0 += __popc(tb & pt.s1L) + 2u * (__popc(tb & m2) + qt_tb);
-                unsigned dq[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const unsigned bil = qt ? (qtb(tb ^ cb[j]) ^ qt_tb ^ qtb(cb[j])) : 0u;
-                    dq[j] = __popc(cb[j] & pt.s1L) + 2u * (__popc(cb[j] & m2) + bil);
-                }
-                const uint32_t qr = op.pad;  // bit s: QT(r_s), host-computed for this config
-                // ---- angle-table slots of this thread's registers (compact index, swizzle linear)
-                const int n_fac = table ? pt.n_fac : 0;
-                uint32_t ts0 = 0, tc[4] = {0, 0, 0, 0};
-                uint32_t fb[3] = {0, 0, 0};
-                if (table && n_fac == 0) {
-                    ts0 = s_pl[0][tb & 63u] ^ s_ph[0][tb >> 6];
-                    tc[0] = tsw(op.swc01 & 0xffffu);
-                    tc[1] = tsw(op.swc01 >> 16);
-                    tc[2] = tsw(op.swc23 & 0xffffu);
-                    tc[3] = tsw(op.swc23 >> 16);
-                }
-                const double2* E0 = nullptr;
-                const double2* E1 = nullptr;
-                const double2* E2 = nullptr;
-                uint32_t fo[3][4];
-                if (n_fac > 0) {
-#pragma unroll
-                    for (int f = 0; f < 3; ++f) {
-                        if (f < n_fac) fb[f] = s_pl[f][tb & 63u] ^ s_ph[f][tb >> 6];
-                        const uint64_t pk = f < n_fac ? op.c_off[f] : 0ull;
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) fo[f][j] = static_cast<uint32_t>(pk >> (16 * j)) & 0xffffu;
-                    }
-                    E0 = reinterpret_cast<const double2*>(tab + pt.fac_coff[0]);
-                    if (n_fac > 1) E1 = reinterpret_cast<const double2*>(tab + pt.fac_coff[1]);
-                    if (n_fac > 2) E2 = reinterpret_cast<const double2*>(tab + pt.fac_coff[2]);
-                }
-                // ---- direct-mode terms (few) with the tile's outer sign folded in
-                const bool direct = !table && n_terms > 0 && n_terms <= 8;
-                double dc[8];
-                uint32_t dz[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    dc[q] = 0.0;
-                    dz[q] = 0u;
-                }
-                if (direct) {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        if (q < n_terms) {
-                            const uint64_t par = __popcll(full & __ldg(plan.term_hmask + pt.term_off + q)) & 1ull;
-                            dc[q] = __longlong_as_double(__double_as_longlong(__ldg(plan.term_coeffs + pt.term_off + q)) ^
-                                                         static_cast<long long>(par << 63));
-                            dz[q] = __ldg(plan.term_lmask + pt.term_off + q);
-                        }
-                    }
-                }
-#pragma unroll
-                for (int s2 = 0; s2 < NR; ++s2) {
-                    unsigned q = q0 + 2u * ((qr >> s2) & 1u);
-#pragma unroll
-                    for (int j = 0; j < R; ++j)
-                        if ((s2 >> j) & 1) q += dq[j];
-                    q &= 3u;
-                    double2 a = v[s2];
-                    if (q & 2u) a = make_double2(-a.x, -a.y);
-                    if (q & 1u) a = make_double2(-a.y, a.x);
-                    if (n_fac > 0) {
-                        uint32_t x0 = fb[0], x1 = fb[1], x2 = fb[2];
-#pragma unroll
-                        for (int j = 0; j < R; ++j) {
-                            if ((s2 >> j) & 1) {
-                                x0 ^= fo[0][j];
-                                x1 ^= fo[1][j];
-                                x2 ^= fo[2][j];
-                            }
-                        }
-                        double2 e = E0[x0];
-                        if (E1) {
-                            const double2 t1 = E1[x1];
-                            e = make_double2(e.x * t1.x - e.y * t1.y, e.x * t1.y + e.y * t1.x);
-                        }
-                        if (E2) {
-                            const double2 t2 = E2[x2];
-                            e = make_double2(e.x * t2.x - e.y * t2.y, e.x * t2.y + e.y * t2.x);
-                        }
-                        a = make_double2(a.x * e.x - a.y * e.y, a.x * e.y + a.y * e.x);
-                    } else if (n_terms > 0) {
-                        double ang = 0.0;
-                        if (table) {
-                            uint32_t ti = ts0;
-#pragma unroll
-                            for (int j = 0; j < R; ++j)
-                                if ((s2 >> j) & 1) ti ^= tc[j];
-                            ang = tab[ti];
-                        } else if (direct) {
-                            uint32_t l = tb;
-#pragma unroll
-                            for (int j = 0; j < R; ++j)
-                                if ((s2 >> j) & 1) l |= cb[j];
-#pragma unroll
-                            for (int q2 = 0; q2 < 8; ++q2) {
-                                const long long sg = static_cast<long long>(__popc(l & dz[q2]) & 1u) << 63;
-                                ang += __longlong_as_double(__double_as_longlong(dc[q2]) ^ sg);
-                            }
-                        } else {
-                            uint32_t l = tb;
-#pragma unroll
-                            for (int j = 0; j < R; ++j)
-                                if ((s2 >> j) & 1) l |= cb[j];
-                            for (int q2 = 0; q2 < n_terms; ++q2) {
-                                const uint64_t zm = __ldg(plan.term_hmask + pt.term_off + q2);
-                                const uint32_t zl = __ldg(plan.term_lmask + pt.term_off + q2);
-                                const long long sg =
-                                    static_cast<long long>((__popcll(full & zm) + __popc(l & zl)) & 1u) << 63;
-                                ang += __longlong_as_double(__double_as_longlong(__ldg(plan.term_coeffs + pt.term_off + q2)) ^ sg);
-                            }
-                        }
-                        double sn, cs;
-                        phase_sincos(neg_dt * ang, &sn, &cs);
-                        if (scale_here) {
-                            sn *= scale;
-                            cs *= scale;
-                        }
-                        a = make_double2(a.x * cs - a.y * sn, a.x * sn + a.y * cs);
-                    }
-                    v[s2] = a;
-                }
-            } else {  // kOpStore
-                uint64_t o[NR];
-                double2* go;
-                if (store_perm) {
-                    // sigma is a bit permutation: sigma(base | off) = sigma(base) | sigma(off)
-                    uint64_t sb = 0;
-#pragma unroll
-                    for (int c = 0; c < kTbaseChunks; ++c) sb |= st_tbase[c * 128 + ((t >> (7 * c)) & 127)];
-                    go = out + sb;
-                    o[0] = st_lo[tb & ((1u << LO) - 1u)] | st_hi[tb >> LO];
-#pragma unroll
-                    for (int j = 0; j < R; ++j)
-#pragma unroll
-                        for (int s = 0; s < (1 << j); ++s) o[s + (1 << j)] = o[s] | op.c_off[j];
-                } else {
-                    go = out + base;
-                    phys_offsets(o);
-                }
-                if (op.mask & 2u) {
-#pragma unroll
-                    for (int s = 0; s < NR; ++s) __stcs(go + o[s], make_double2(v[s].x * scale, v[s].y * scale));
-                } else {
-#pragma unroll
-                    for (int s = 0; s < NR; ++s) __stcs(go + o[s], v[s]);
-                }
-            }
-        }
-    }
+            uint64_t rank_bits, uint64_t n_tiles) {
+    const Interpreter prog;
+    SDB_PASS_KERNEL_BODY(K, RB, prog)
 }
 
 template <int K, int RB>
@@ -758,6 +89,17 @@ void launch_k(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& pl
 }  // namespace
 
 int max_tile_qubits() { return 12; }
+
+size_t tile_pass_smem(const PassDev& ph) {
+    switch (ph.k) {
+#define SDB_K(KK) \
+    case KK: return smem_bytes<KK, 4>(ph);
+        SDB_K(1) SDB_K(2) SDB_K(3) SDB_K(4) SDB_K(5) SDB_K(6) SDB_K(7) SDB_K(8) SDB_K(9) SDB_K(10)
+        SDB_K(11) SDB_K(12)
+#undef SDB_K
+        default: throw std::invalid_argument("tile qubits out of range");
+    }
+}
 
 void launch_tile_pass(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& plan, double dt,
                       uint64_t rank_bits, double* out) {

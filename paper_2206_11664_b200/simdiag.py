@@ -602,3 +602,22 @@ def exchange_routes(n_qubits: int, n_local: int, rank: int, swaps) -> List[Tuple
     out = (A.Route * max(1, cnt.value))()
     check(A.sd_exchange_routes(n_qubits, n_local, rank, arr, len(swaps), out, cnt.value, C.byref(cnt)))
     return [(r.peer, r.send_offset, r.recv_offset, r.count) for r in out[:cnt.value]]
+
+
+def jit_compile_preview(n_qubits: int, groups: Sequence[DiagonalGroup], order: int = 1, tile_qubits: int = 0,
+                        world: int = 1) -> int:
+    """Host-only: NVRTC-compile the specialised kernels of the first step's
+    passes (sd_jit_compile_preview); returns the number of distinct programs."""
+    opts = A.PlanOptions()
+    check(A.sd_plan_options_default(C.byref(opts)))
+    opts.order = order
+    opts.tile_qubits = tile_qubits
+    descs = (A.GroupDesc * max(1, len(groups)))()
+    keep = []
+    for i, g in enumerate(groups):
+        d, k = g._desc()
+        descs[i] = d
+        keep.append(k)
+    n = C.c_size_t(0)
+    check(A.sd_jit_compile_preview(n_qubits, world, descs, len(groups), C.byref(opts), C.byref(n)))
+    return n.value

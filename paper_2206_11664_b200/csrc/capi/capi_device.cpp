@@ -201,7 +201,6 @@ void upload_step(sd_plan& p, StepExec& E, const sdb::StepPlan& combined) {
         al(std::max<size_t>(1, A.term_hmask.size()) * 8),
         al(std::max<size_t>(1, A.term_lmask.size()) * 4),
         al(std::max<size_t>(1, A.term_coeffs.size()) * 8),
-        al(std::max<size_t>(1, A.fac_seg.size()) * 4),
     };
     size_t total = 0;
     for (size_t v : sizes) total += v;
@@ -228,7 +227,6 @@ void upload_step(sd_plan& p, StepExec& E, const sdb::StepPlan& combined) {
     E.dev.term_hmask = static_cast<const uint64_t*>(put(A.term_hmask.data(), A.term_hmask.size() * 8));
     E.dev.term_lmask = static_cast<const uint32_t*>(put(A.term_lmask.data(), A.term_lmask.size() * 4));
     E.dev.term_coeffs = static_cast<const double*>(put(A.term_coeffs.data(), A.term_coeffs.size() * 8));
-    E.dev.fac_seg = static_cast<const int*>(put(A.fac_seg.data(), A.fac_seg.size() * 4));
     SDB_CUDA(cudaMemcpy(E.dev_block, host.data(), total, cudaMemcpyHostToDevice));
     E.host_passes = std::move(A.passes);
 }

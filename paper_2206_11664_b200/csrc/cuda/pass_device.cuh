@@ -174,100 +174,37 @@ __device__ void wht_table(double* __restrict__ tab, int bits) {
     }
 }
 
-// One factor table built by one warp, no block barriers: entry u = lane +
-// 32 j (j < M per lane). A[u] from the factor's segment of u (host index
-// fac_seg), WHT over register bits in place and over lane bits with
-// shuffles, then E[u] = exp(-i dt theta(u)) (times sc) into the
-// amplitude-swizzled complex table.
-template <int M>
-__device__ __forceinline__ void warp_factor_table(double2* __restrict__ E, const PlanDev& plan, const PointDev& pt,
-                                                  int f, uint64_t full, double neg_dt, double sc) {
-    const int lane = threadIdx.x & 31;
-    const int bits = pt.fac_bits[f];
-    const int size = 1 << bits;
+// Factor tables of one tile, every thread computing entries directly: entry
+// u of factor f (entries of all factors numbered consecutively) is
+//   E_f[u] = exp(-i dt sum_{segments s of f} A_s (-1)^{popc(u & u_s)}) (* sc),
+// A_s = sum_{terms q of s} c_q (-1)^{popc(h & zh_q)} -- a handful of terms per
+// factor, so no transform pass and no cross-thread exchange is needed.
+template <int NT>
+__device__ __forceinline__ void build_factor_tables(double* __restrict__ tab, const PlanDev& plan, const PointDev& pt,
+                                                    uint64_t full, double neg_dt, double tscale) {
     const uint64_t* zh = plan.term_hmask + pt.term_off;
     const double* cf = plan.term_coeffs + pt.term_off;
-    const int* seg_of = plan.fac_seg + pt.fac_soff[f];
-    double w[M];
-#pragma unroll
-    for (int j = 0; j < M; ++j) {
-        const int u = lane + 32 * j;
-        double acc = 0.0;
-        if (u < size) {
-            const int sg = __ldg(seg_of + u);
-            if (sg >= 0) {
-                const SegDev d = plan.segs[pt.seg_off + sg];
-                for (int q = d.begin; q < d.end; ++q) {
-                    const uint64_t par = __popcll(full & __ldg(zh + q)) & 1ull;
-                    acc += __longlong_as_double(__double_as_longlong(__ldg(cf + q)) ^ static_cast<long long>(par << 63));
-                }
-            }
-        }
-        w[j] = acc;
-    }
-    // register bits (u bits 5..)
-#pragma unroll
-    for (int jb = 0; (1 << jb) < M; ++jb)
-#pragma unroll
-        for (int j = 0; j < M; ++j) {
-            if ((j >> jb) & 1) continue;
-            const double x = w[j], y = w[j | (1 << jb)];
-            w[j] = x + y;
-            w[j | (1 << jb)] = x - y;
-        }
-    // lane bits (u bits 0..4)
-    for (int lb = 0; lb < 5 && lb < bits; ++lb) {
-        const bool hi = (lane >> lb) & 1;
-#pragma unroll
-        for (int j = 0; j < M; ++j) {
-            const double o = __shfl_xor_sync(0xffffffffu, w[j], 1 << lb);
-            w[j] = hi ? o - w[j] : w[j] + o;
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < M; ++j) {
-        const int u = lane + 32 * j;
-        if (u < size) {
-            double sn, cs;
-            phase_sincos(neg_dt * w[j], &sn, &cs);
-            E[swz(static_cast<uint32_t>(u))] = make_double2(cs * sc, sn * sc);
-        }
-    }
-}
-
-// Same table built by one thread (CTAs narrower than a warp per factor, i.e.
-// tiny tiles): theta lives in E[.].x during the transform.
-__device__ void serial_factor_table(double2* __restrict__ E, const PlanDev& plan, const PointDev& pt, int f,
-                                    uint64_t full, double neg_dt, double sc) {
-    const int size = 1 << pt.fac_bits[f];
-    const uint64_t* zh = plan.term_hmask + pt.term_off;
-    const double* cf = plan.term_coeffs + pt.term_off;
-    const int* seg_of = plan.fac_seg + pt.fac_soff[f];
-    for (int u = 0; u < size; ++u) {
-        double acc = 0.0;
-        const int sg = __ldg(seg_of + u);
-        if (sg >= 0) {
-            const SegDev d = plan.segs[pt.seg_off + sg];
+    const SegDev* segs = plan.segs + pt.seg_off;
+    const int n0 = 1 << pt.fac_bits[0];
+    const int n1 = pt.n_fac > 1 ? 1 << pt.fac_bits[1] : 0;
+    const int n2 = pt.n_fac > 2 ? 1 << pt.fac_bits[2] : 0;
+    for (int e = threadIdx.x; e < n0 + n1 + n2; e += NT) {
+        const int f = e < n0 ? 0 : (e < n0 + n1 ? 1 : 2);
+        const uint32_t u = static_cast<uint32_t>(e - (f == 0 ? 0 : (f == 1 ? n0 : n0 + n1)));
+        double th = 0.0;
+        for (int sg = pt.fac_sbeg[f]; sg < pt.fac_send[f]; ++sg) {
+            const SegDev d = segs[sg];
+            double acc = 0.0;
             for (int q = d.begin; q < d.end; ++q) {
                 const uint64_t par = __popcll(full & __ldg(zh + q)) & 1ull;
                 acc += __longlong_as_double(__double_as_longlong(__ldg(cf + q)) ^ static_cast<long long>(par << 63));
             }
+            th += (__popc(u & d.u) & 1) ? -acc : acc;
         }
-        E[swz(static_cast<uint32_t>(u))].x = acc;
-    }
-    for (int h = 1; h < size; h <<= 1)
-        for (int u = 0; u < size; ++u) {
-            if (u & h) continue;
-            const uint32_t i0 = swz(static_cast<uint32_t>(u)), i1 = swz(static_cast<uint32_t>(u | h));
-            const double x = E[i0].x, y = E[i1].x;
-            E[i0].x = x + y;
-            E[i1].x = x - y;
-        }
-    for (int u = 0; u < size; ++u) {
-        const uint32_t i = swz(static_cast<uint32_t>(u));
         double sn, cs;
-        phase_sincos(neg_dt * E[i].x, &sn, &cs);
-        E[i] = make_double2(cs * sc, sn * sc);
+        phase_sincos(neg_dt * th, &sn, &cs);
+        const double sc = f == 0 ? tscale : 1.0;
+        reinterpret_cast<double2*>(tab + pt.fac_coff[f])[swz(u)] = make_double2(cs * sc, sn * sc);
     }
 }
 
@@ -278,28 +215,17 @@ __device__ void serial_factor_table(double2* __restrict__ E, const PlanDev& plan
 // table_bits compact coordinates (phi/(-dt) per local index).
 template <int NT>
 __device__ void build_tables(double* __restrict__ tab, const PlanDev& plan, const PointDev& pt, uint64_t full,
-                             double neg_dt, double tscale) {
+                             double neg_dt, double tscale, bool nosync) {
     const int tid = threadIdx.x;
+    if (pt.n_fac > 0 && nosync) {
+        // double-buffered tables; the program's transposes order the writes
+        // before the POINT reads and this tile's reads before the reuse
+        build_factor_tables<NT>(tab, plan, pt, full, neg_dt, tscale);
+        return;
+    }
     __syncthreads();  // previous tile's readers are done with tab
     if (pt.n_fac > 0) {
-        if (NT < 32 * 3) {  // narrow CTA (tiny tiles): one thread per factor
-            if (tid < pt.n_fac) {
-                serial_factor_table(reinterpret_cast<double2*>(tab + pt.fac_coff[tid]), plan, pt, tid, full, neg_dt,
-                                    tid == 0 ? tscale : 1.0);
-            }
-            __syncthreads();
-            return;
-        }
-        const int f = tid >> 5;
-        if (f < pt.n_fac) {
-            double2* const E = reinterpret_cast<double2*>(tab + pt.fac_coff[f]);
-            const double sc = f == 0 ? tscale : 1.0;
-            const int b = pt.fac_bits[f];
-            if (b <= 5) warp_factor_table<1>(E, plan, pt, f, full, neg_dt, sc);
-            else if (b == 6) warp_factor_table<2>(E, plan, pt, f, full, neg_dt, sc);
-            else if (b == 7) warp_factor_table<4>(E, plan, pt, f, full, neg_dt, sc);
-            else warp_factor_table<8>(E, plan, pt, f, full, neg_dt, sc);  // b <= kMaxFacBits = 8
-        }
+        build_factor_tables<NT>(tab, plan, pt, full, neg_dt, tscale);
         __syncthreads();
         return;
     }
@@ -373,6 +299,8 @@ struct PassCtx {
     uint64_t t, base, full;
     const double2* g;
     bool smem_busy;
+    int tpar;  // tile parity (double-buffered phase tables)
+    uint64_t last_pat;  // sign pattern the current phase tables were built for
     RegCfg rc;
 
     __device__ __forceinline__ PassCtx(const PassDev& P_, const PlanDev& plan_, const double2* psi_, double2* out_,
@@ -384,6 +312,8 @@ struct PassCtx {
         tid = threadIdx.x;
         stride = gridDim.x;
         has_table = P.table_point >= 0;
+        tpar = 1;
+        last_pat = ~0ull;
         store_perm = P.store_perm != 0;
         scale = P.scale;  // exact power of two
         buf = reinterpret_cast<double2*>(smem_raw);  // transpose buffer
@@ -482,7 +412,9 @@ struct PassCtx {
         full = rank_bits | base;
         g = psi + base;
         smem_busy = true;  // smem may still be read by other threads (sync before writing)
+        tpar ^= 1;
     }
+    __device__ __forceinline__ double* tabc() const { return tab + ((P.tab_double && tpar) ? P.tab_half : 0); }
 
     // register config from the staged program (interpreter)
     __device__ __forceinline__ RegCfg cfg_of(const MicroOpDev& op) const {
@@ -531,7 +463,14 @@ struct PassCtx {
             for (int s = 0; s < NR; ++s) prefetch_l2(gn + o[s]);
         }
         // per-tile phase tables, built while the loads are in flight
-        if (has_table) build_tables<NT>(tab, plan, plan.points[P.table_point], full, neg_dt, P.table_scale);
+        // (rebuilt only when the tile's table sign pattern changes, see PassDev::pat_shift)
+        if (has_table) {
+            const uint64_t pat = P.pat_shift >= 64 ? t : (t >> P.pat_shift);
+            if (pat != last_pat) {
+                last_pat = pat;
+                build_tables<NT>(tabc(), plan, plan.points[P.table_point], full, neg_dt, P.table_scale, false);
+            }
+        }
     }
 
     // shared-memory transpose into config r; op.perm >= 0 applies a pending
@@ -572,12 +511,45 @@ struct PassCtx {
         smem_busy = true;
     }
 
+    // Phase mode of a POINT op (template parameter of point()):
+    //   0 quarter turns only, 1 <= 8 terms summed directly, 2 more terms
+    //   summed directly (no table left in the pass), 3 full angle table,
+    //   4 factor tables (NFAC of them).
+    static __device__ __forceinline__ int point_mode(const PassDev& P, const PointDev& pt, int arg) {
+        if (pt.n_terms == 0) return 0;
+        if (arg == P.table_point) return pt.n_fac > 0 ? 4 : 3;
+        return pt.n_terms <= 8 ? 1 : 2;
+    }
+
+    // Per-op constants of a POINT in the current register config: the JIT
+    // passes literals, the interpreter decodes the staged op (point_cfg).
+    struct PointCfg {
+        uint32_t qr;         // bit s: QT(r_s)
+        uint32_t tc[4];      // full table: swizzled compact offsets of the register coordinates
+        uint32_t fo[3][4];   // factor tables: swizzled compact offsets per factor
+        int coffE[3];        // factor tables: double offsets in the table region
+    };
+    __device__ __forceinline__ PointCfg point_cfg(const MicroOpDev& op, const PointDev& pt) const {
+        PointCfg c;
+        c.qr = static_cast<uint32_t>(op.pad);
+        c.tc[0] = tsw(op.swc01 & 0xffffu);
+        c.tc[1] = tsw(op.swc01 >> 16);
+        c.tc[2] = tsw(op.swc23 & 0xffffu);
+        c.tc[3] = tsw(op.swc23 >> 16);
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+            c.coffE[f] = pt.fac_coff[f];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) c.fo[f][j] = static_cast<uint32_t>(op.c_off[f] >> (16 * j)) & 0xffffu;
+        }
+        return c;
+    }
+
     // pointwise S/CZ quarter turns and exp(-i dt Lambda) (PointDev)
-    __device__ __forceinline__ void point(const MicroOpDev& op, double2 (&v)[NR]) {
+    template <int MODE, int NFAC>
+    __device__ __forceinline__ void point(const MicroOpDev& op, const PointCfg& pc, double2 (&v)[NR]) {
         const PointDev& pt = plan.points[op.arg];
-        const bool table = op.arg == P.table_point;
         const bool scale_here = (op.mask & 1u) != 0;
-        const int n_terms = pt.n_terms;
         uint32_t cb[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) cb[j] = 1u << ((rc.cidx >> (8 * j)) & 255u);
@@ -603,47 +575,27 @@ struct PassCtx {
             const unsigned bil = qt ? (qtb(rc.tb ^ cb[j]) ^ qt_tb ^ qtb(cb[j])) : 0u;
             dq[j] = __popc(cb[j] & pt.s1L) + 2u * (__popc(cb[j] & m2) + bil);
         }
-        const uint32_t qr = op.pad;  // bit s: QT(r_s), host-computed for this config
-        // ---- angle-table slots of this thread's registers (compact index, swizzle linear)
-        const int n_fac = table ? pt.n_fac : 0;
-        uint32_t ts0 = 0, tc[4] = {0, 0, 0, 0};
-        uint32_t fb[3] = {0, 0, 0};
-        if (table && n_fac == 0) {
-            ts0 = s_pl[rc.tb & 63u] ^ s_ph[rc.tb >> 6];
-            tc[0] = tsw(op.swc01 & 0xffffu);
-            tc[1] = tsw(op.swc01 >> 16);
-            tc[2] = tsw(op.swc23 & 0xffffu);
-            tc[3] = tsw(op.swc23 >> 16);
-        }
-        const double2* E0 = nullptr;
-        const double2* E1 = nullptr;
-        const double2* E2 = nullptr;
-        uint32_t fo[3][4];
-        if (n_fac > 0) {
+        // ---- table slots of this thread's registers (compact index, swizzle linear)
+        uint32_t ts0 = 0, fb[3] = {0, 0, 0};
+        const double2* E[3] = {nullptr, nullptr, nullptr};
+        if constexpr (MODE == 3) ts0 = s_pl[rc.tb & 63u] ^ s_ph[rc.tb >> 6];
+        if constexpr (MODE == 4) {
+            const double* tb_ = tabc();
 #pragma unroll
-            for (int f = 0; f < 3; ++f) {
-                if (f < n_fac) fb[f] = s_pl[f * 64 + (rc.tb & 63u)] ^ s_ph[f * 64 + (rc.tb >> 6)];
-                const uint64_t pk = f < n_fac ? op.c_off[f] : 0ull;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) fo[f][j] = static_cast<uint32_t>(pk >> (16 * j)) & 0xffffu;
+            for (int f = 0; f < NFAC; ++f) {
+                fb[f] = s_pl[f * 64 + (rc.tb & 63u)] ^ s_ph[f * 64 + (rc.tb >> 6)];
+                E[f] = reinterpret_cast<const double2*>(tb_ + pc.coffE[f]);
             }
-            E0 = reinterpret_cast<const double2*>(tab + pt.fac_coff[0]);
-            if (n_fac > 1) E1 = reinterpret_cast<const double2*>(tab + pt.fac_coff[1]);
-            if (n_fac > 2) E2 = reinterpret_cast<const double2*>(tab + pt.fac_coff[2]);
         }
         // ---- direct-mode terms (few) with the tile's outer sign folded in
-        const bool direct = !table && n_terms > 0 && n_terms <= 8;
-        double dc[8];
-        uint32_t dz[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            dc[q] = 0.0;
-            dz[q] = 0u;
-        }
-        if (direct) {
+        double dc[MODE == 1 ? 8 : 1];
+        uint32_t dz[MODE == 1 ? 8 : 1];
+        if constexpr (MODE == 1) {
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                if (q < n_terms) {
+                dc[q] = 0.0;
+                dz[q] = 0u;
+                if (q < pt.n_terms) {
                     const uint64_t par = __popcll(full & __ldg(plan.term_hmask + pt.term_off + q)) & 1ull;
                     dc[q] = __longlong_as_double(__double_as_longlong(__ldg(plan.term_coeffs + pt.term_off + q)) ^
                                                  static_cast<long long>(par << 63));
@@ -653,7 +605,7 @@ struct PassCtx {
         }
 #pragma unroll
         for (int s2 = 0; s2 < NR; ++s2) {
-            unsigned q = q0 + 2u * ((qr >> s2) & 1u);
+            unsigned q = q0 + 2u * ((pc.qr >> s2) & 1u);
 #pragma unroll
             for (int j = 0; j < R; ++j)
                 if ((s2 >> j) & 1) q += dq[j];
@@ -661,54 +613,41 @@ struct PassCtx {
             double2 a = v[s2];
             if (q & 2u) a = make_double2(-a.x, -a.y);
             if (q & 1u) a = make_double2(-a.y, a.x);
-            if (n_fac > 0) {
-                uint32_t x0 = fb[0], x1 = fb[1], x2 = fb[2];
+            if constexpr (MODE == 4) {
+                double2 e;
 #pragma unroll
-                for (int j = 0; j < R; ++j) {
-                    if ((s2 >> j) & 1) {
-                        x0 ^= fo[0][j];
-                        x1 ^= fo[1][j];
-                        x2 ^= fo[2][j];
-                    }
-                }
-                double2 e = E0[x0];
-                if (E1) {
-                    const double2 t1 = E1[x1];
-                    e = make_double2(e.x * t1.x - e.y * t1.y, e.x * t1.y + e.y * t1.x);
-                }
-                if (E2) {
-                    const double2 t2 = E2[x2];
-                    e = make_double2(e.x * t2.x - e.y * t2.y, e.x * t2.y + e.y * t2.x);
+                for (int f = 0; f < NFAC; ++f) {
+                    uint32_t x = fb[f];
+#pragma unroll
+                    for (int j = 0; j < R; ++j)
+                        if ((s2 >> j) & 1) x ^= pc.fo[f][j];
+                    const double2 t = E[f][x];
+                    e = f == 0 ? t : make_double2(e.x * t.x - e.y * t.y, e.x * t.y + e.y * t.x);
                 }
                 a = make_double2(a.x * e.x - a.y * e.y, a.x * e.y + a.y * e.x);
-            } else if (n_terms > 0) {
+            } else if constexpr (MODE != 0) {
                 double ang = 0.0;
-                if (table) {
+                uint32_t l = rc.tb;
+#pragma unroll
+                for (int j = 0; j < R; ++j)
+                    if ((s2 >> j) & 1) l |= cb[j];
+                if constexpr (MODE == 3) {
                     uint32_t ti = ts0;
 #pragma unroll
                     for (int j = 0; j < R; ++j)
-                        if ((s2 >> j) & 1) ti ^= tc[j];
-                    ang = tab[ti];
-                } else if (direct) {
-                    uint32_t l = rc.tb;
-#pragma unroll
-                    for (int j = 0; j < R; ++j)
-                        if ((s2 >> j) & 1) l |= cb[j];
+                        if ((s2 >> j) & 1) ti ^= pc.tc[j];
+                    ang = tabc()[ti];
+                } else if constexpr (MODE == 1) {
 #pragma unroll
                     for (int q2 = 0; q2 < 8; ++q2) {
                         const long long sg = static_cast<long long>(__popc(l & dz[q2]) & 1u) << 63;
                         ang += __longlong_as_double(__double_as_longlong(dc[q2]) ^ sg);
                     }
                 } else {
-                    uint32_t l = rc.tb;
-#pragma unroll
-                    for (int j = 0; j < R; ++j)
-                        if ((s2 >> j) & 1) l |= cb[j];
-                    for (int q2 = 0; q2 < n_terms; ++q2) {
+                    for (int q2 = 0; q2 < pt.n_terms; ++q2) {
                         const uint64_t zm = __ldg(plan.term_hmask + pt.term_off + q2);
                         const uint32_t zl = __ldg(plan.term_lmask + pt.term_off + q2);
-                        const long long sg =
-                            static_cast<long long>((__popcll(full & zm) + __popc(l & zl)) & 1u) << 63;
+                        const long long sg = static_cast<long long>((__popcll(full & zm) + __popc(l & zl)) & 1u) << 63;
                         ang += __longlong_as_double(__double_as_longlong(__ldg(plan.term_coeffs + pt.term_off + q2)) ^ sg);
                     }
                 }
@@ -721,6 +660,23 @@ struct PassCtx {
                 a = make_double2(a.x * cs - a.y * sn, a.x * sn + a.y * cs);
             }
             v[s2] = a;
+        }
+    }
+
+    // interpreter entry: decode the mode and the per-op constants at run time
+    __device__ __forceinline__ void point_any(const MicroOpDev& op, double2 (&v)[NR]) {
+        const PointDev& pt = plan.points[op.arg];
+        const PointCfg pc = point_cfg(op, pt);
+        switch (point_mode(P, pt, op.arg)) {
+            case 0: point<0, 0>(op, pc, v); break;
+            case 1: point<1, 0>(op, pc, v); break;
+            case 2: point<2, 0>(op, pc, v); break;
+            case 3: point<3, 0>(op, pc, v); break;
+            default:
+                if (pt.n_fac == 1) point<4, 1>(op, pc, v);
+                else if (pt.n_fac == 2) point<4, 2>(op, pc, v);
+                else point<4, 3>(op, pc, v);
+                break;
         }
     }
 

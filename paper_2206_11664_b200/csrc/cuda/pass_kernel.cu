@@ -29,7 +29,7 @@ struct Interpreter {
             } else if (kind == kOpBfly) {
                 dev::bfly_dispatch<Ctx::R>(v, op.mask);
             } else if (kind == kOpPoint) {
-                ctx.point(op, v);
+                ctx.point_any(op, v);
             } else {
                 ctx.store(op, v);
             }

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <bit>
 #include <cmath>
+#include <cstdlib>
 #include <sstream>
 #include <stdexcept>
 
@@ -417,13 +418,14 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                     }
                     pt.n_seg = static_cast<int>(A.segs.size()) - pt.seg_off;
                     for (int f = 0; f < pt.n_fac; ++f) {
-                        pt.fac_soff[f] = static_cast<int>(A.fac_seg.size());
-                        const size_t base = A.fac_seg.size();
-                        A.fac_seg.resize(base + (size_t(1) << pt.fac_bits[f]), -1);
+                        pt.fac_sbeg[f] = pt.n_seg;
+                        pt.fac_send[f] = 0;
                         for (int sg = 0; sg < pt.n_seg; ++sg) {
-                            const SegDev& d = A.segs[pt.seg_off + sg];
-                            if (d.fac == f) A.fac_seg[base + d.u] = sg;
+                            if (A.segs[pt.seg_off + sg].fac != f) continue;
+                            pt.fac_sbeg[f] = std::min(pt.fac_sbeg[f], sg);
+                            pt.fac_send[f] = std::max(pt.fac_send[f], sg + 1);
                         }
+                        if (pt.fac_send[f] == 0) pt.fac_sbeg[f] = 0;
                     }
                     for (const T& t : sorted) {
                         A.term_hmask.push_back(t.zh);
@@ -507,7 +509,30 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
         A.ops.push_back(so);
         pd.n_ops = static_cast<int>(A.ops.size()) - pd.op_off;
         pd.n_qt_words = static_cast<int>(A.qt_words.size()) - pd.qt_off;
-        if (pd.n_ops > 2 * kMaxOpsPerPass + 4) throw std::logic_error("lower_plan: pass program too long");
+        // Per-tile phase tables depend on the tile only through the outer bits
+        // of the table terms (PM). Those bits go to the top of the tile index,
+        // so a CTA walking t, t + grid, ... keeps the same table for long runs
+        // of tiles and rebuilds it only when t >> pat_shift changes.
+        pd.tab_half = pd.tab_words;
+        pd.pat_shift = 64;
+        static const bool reorder = [] {
+            const char* e = std::getenv("SDB_TABLE_REUSE");
+            return !e || std::atoi(e) != 0;
+        }();
+        if (pd.table_point >= 0 && reorder) {
+            const PointDev& tp = A.points[pd.table_point];
+            uint64_t pm = 0;
+            for (int q = 0; q < tp.n_terms; ++q) pm |= A.term_hmask[tp.term_off + q];
+            std::vector<int> rest, top;
+            for (int j = 0; j < pd.n_outer; ++j) ((pm >> pd.opos[j]) & 1 ? top : rest).push_back(pd.opos[j]);
+            int j = 0;
+            for (int b : rest) pd.opos[j++] = b;
+            for (int b : top) pd.opos[j++] = b;
+            pd.pat_shift = static_cast<int>(rest.size());
+            if (!pp.store_sigma.empty()) {
+                for (int q = 0; q < pd.n_outer; ++q) pd.st_opos[q] = pp.store_sigma[pd.opos[q]];
+            }
+        }
         A.passes.push_back(pd);
         A.pass_class.push_back(only_point ? 1 : 0);
         A.transposes.push_back(transposes);

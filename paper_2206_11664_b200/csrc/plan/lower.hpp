@@ -23,7 +23,6 @@ struct HostPlanArrays {
     std::vector<uint64_t> term_hmask;
     std::vector<uint32_t> term_lmask;
     std::vector<double> term_coeffs;
-    std::vector<int> fac_seg;
     std::vector<int> pass_class;   // 0 = transform pass, 1 = diagonal-only pass
     std::vector<int> transposes;   // shared-memory transposes per pass (CFG with a write side)
 };

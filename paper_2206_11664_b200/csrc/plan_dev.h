@@ -115,7 +115,8 @@ struct PointDev {
     int n_fac;
     uint32_t fac_mask[3];
     int fac_bits[3];
-    int fac_soff[3];  // factor f: offset of its 2^b segment index (PlanDev::fac_seg, -1 = no term)
+    int fac_sbeg[3];  // factor f: its segments are [fac_sbeg, fac_send) relative to seg_off
+    int fac_send[3];
     int fac_coff[3];  // complex table of factor f: double offset (even) in the table region
 };
 
@@ -141,7 +142,10 @@ struct PassDev {
     int rbits;        // R: register coordinates per config
     int qt_off;       // first QT word of this pass in PlanDev::qt_words
     int n_qt_words;   // QT words staged into shared memory
-    int tab_words;    // 8-byte words of the per-tile table region (even; 0 if none)
+    int tab_words;    // 8-byte words of the per-tile table region (even; 0 if none; both copies)
+    int tab_double;   // 1: two copies, tile parity selects (unused: see pat_shift)
+    int tab_half;     // words per copy when tab_double
+    int pat_shift;    // tile-index bits >= pat_shift select the table's sign pattern (rebuild on change)
     double table_scale;  // factor mode: exact scale folded into E_0 (1 if applied elsewhere)
     int store_perm;      // 1: store out of place through a local bit permutation sigma
     int st_lpos[16];     // sigma(lpos[j])
@@ -163,7 +167,6 @@ struct PlanDev {
     const uint64_t* term_hmask; // outer (physical) part of each term's z-mask
     const uint32_t* term_lmask; // local-coordinate part (direct mode)
     const double* term_coeffs;  // c_t * dt_scale; the kernel multiplies by -dt
-    const int* fac_seg;         // factor mode: compact index -> segment (relative to the point), -1 if none
 };
 
 }  // namespace sdb

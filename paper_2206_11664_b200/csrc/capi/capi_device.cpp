@@ -37,6 +37,8 @@ struct StepExec {
     std::vector<size_t> smem;     // dynamic shared memory per pass
     sdb::PlanDev dev{};
     void* dev_block = nullptr;
+    double2* tile_phase = nullptr;  // per-tile constant phases (passes with tphase_off >= 0)
+    double phase_dt = std::nan("");  // dt the tile phases were computed for
     std::string program;
 };
 
@@ -178,13 +180,16 @@ constexpr int kTableThreshold = 8;  // terms per POINT stage above which a per-t
 
 void upload_step(sd_plan& p, StepExec& E, const sdb::StepPlan& combined) {
     sdb::StateImpl& s = p.state->impl;
-    sdb::HostPlanArrays A = sdb::lower_plan(combined, s.n_local, kTableThreshold, 4);
+    const bool jit = sdb::jit_wanted(s.n_local);
+    int rbits = 4;
+    if (const char* e = std::getenv("SDB_RBITS"); e && jit) rbits = std::atoi(e) == 3 ? 3 : 4;
+    sdb::HostPlanArrays A = sdb::lower_plan(combined, s.n_local, kTableThreshold, rbits);
     E.pass_class = A.pass_class;
     E.program = sdb::describe_program(A);
     E.jit_fn.assign(A.passes.size(), nullptr);
     E.smem.resize(A.passes.size());
     for (size_t i = 0; i < A.passes.size(); ++i) E.smem[i] = sdb::tile_pass_smem(A.passes[i]);
-    if (sdb::jit_wanted(s.n_local)) {
+    if (jit) {
         E.jit_fn = sdb::jit_pass_kernels(A, s.device);
     }
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
@@ -227,6 +232,19 @@ void upload_step(sd_plan& p, StepExec& E, const sdb::StepPlan& combined) {
     E.dev.term_hmask = static_cast<const uint64_t*>(put(A.term_hmask.data(), A.term_hmask.size() * 8));
     E.dev.term_lmask = static_cast<const uint32_t*>(put(A.term_lmask.data(), A.term_lmask.size() * 4));
     E.dev.term_coeffs = static_cast<const double*>(put(A.term_coeffs.data(), A.term_coeffs.size() * 8));
+    // per-tile constant phase buffers (offsets assigned here, filled per dt)
+    size_t n_phase = 0;
+    for (sdb::PassDev& pd : A.passes) {
+        if (pd.tphase_off >= 0) {
+            pd.tphase_off = static_cast<int>(n_phase);
+            n_phase += size_t(1) << pd.n_outer;
+        }
+    }
+    if (n_phase) {
+        SDB_CUDA(cudaMalloc(reinterpret_cast<void**>(&E.tile_phase), n_phase * sizeof(double2)));
+        std::memcpy(host.data(), A.passes.data(), A.passes.size() * sizeof(sdb::PassDev));  // updated offsets
+    }
+    E.dev.tile_phase = E.tile_phase;
     SDB_CUDA(cudaMemcpy(E.dev_block, host.data(), total, cudaMemcpyHostToDevice));
     E.host_passes = std::move(A.passes);
 }
@@ -308,6 +326,15 @@ void harvest(sd_plan& p) {
 void run_segment(sd_plan& p, StepExec& E, size_t seg, double dt) {
     sdb::StateImpl& s = p.state->impl;
     const uint64_t rank_bits = uint64_t(s.rank) << s.n_local;
+    if (E.tile_phase && !(E.phase_dt == dt)) {
+        for (size_t i = 0; i < E.host_passes.size(); ++i) {
+            if (E.host_passes[i].tphase_off >= 0) {
+                sdb::launch_tile_phase(s, E.host_passes[i], static_cast<int>(i), E.dev, dt, rank_bits,
+                                       E.tile_phase + E.host_passes[i].tphase_off);
+            }
+        }
+        E.phase_dt = dt;
+    }
     const double bytes = 2.0 * 16.0 * double(s.amps_count());
     const bool exch = E.ss.segs[seg].exchange_after;
     const int first = E.seg_first[seg], count = E.seg_count[seg];
@@ -811,6 +838,7 @@ void sd_plan_destroy(sd_plan* p) {
     }
     for (auto& kv : p->steps) {
         if (kv.second->dev_block) cudaFree(kv.second->dev_block);
+        if (kv.second->tile_phase) cudaFree(kv.second->tile_phase);
     }
     delete p;
 }

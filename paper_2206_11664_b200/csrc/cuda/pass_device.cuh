@@ -208,6 +208,27 @@ __device__ __forceinline__ void build_factor_tables(double* __restrict__ tab, co
     }
 }
 
+// exp(-i dt theta_0(t)) of a pass's tile-constant table terms for tile t
+// (tile index in the pass's own tile order).
+__device__ __forceinline__ double2 tile_constant_phase(const PlanDev& plan, const PassDev& P, uint64_t t,
+                                                      uint64_t rank_bits, double neg_dt) {
+    uint64_t base = 0;
+    for (int j = 0; j < P.n_outer; ++j)
+        if ((t >> j) & 1ull) base |= 1ull << P.opos[j];
+    const uint64_t full = rank_bits | base;
+    const PointDev& pt = plan.points[P.table_point];
+    const SegDev d = plan.segs[pt.seg_off + pt.c0_seg];
+    double th = 0.0;
+    for (int q = d.begin; q < d.end; ++q) {
+        const uint64_t par = __popcll(full & plan.term_hmask[pt.term_off + q]) & 1ull;
+        th += __longlong_as_double(__double_as_longlong(plan.term_coeffs[pt.term_off + q]) ^
+                                   static_cast<long long>(par << 63));
+    }
+    double sn, cs;
+    phase_sincos(neg_dt * th, &sn, &cs);
+    return make_double2(cs, sn);
+}
+
 // Per-tile tables of the pass's table point, built while the tile's loads
 // are in flight. Factor mode: warp f builds factor f's complex table
 // E_f = exp(-i dt theta_f) (E_0 carries table_scale) -- two block barriers
@@ -284,6 +305,7 @@ struct PassCtx {
     double2* __restrict__ out;
     double neg_dt;
     uint64_t rank_bits, n_tiles, stride;
+    uint64_t t_first, t_last;  // this CTA's tiles: strided (t_first += grid) or a contiguous block
     int tid;
     bool has_table, store_perm;
     double scale;
@@ -310,7 +332,18 @@ struct PassCtx {
         : P(P_), plan(plan_), psi(psi_), out(out_), neg_dt(neg_dt_), rank_bits(rank_bits_), n_tiles(n_tiles_),
           off_lo(off_lo_), off_hi(off_hi_), s_tbase(s_tbase_), s_pl(s_pl_), s_ph(s_ph_) {
         tid = threadIdx.x;
-        stride = gridDim.x;
+        if (P.blocked) {
+            // contiguous block of tiles per CTA: consecutive tiles share the
+            // phase tables' sign pattern (PassDev::pat_shift)
+            const uint64_t per = (n_tiles + gridDim.x - 1) / gridDim.x;
+            t_first = blockIdx.x * per;
+            t_last = t_first + per < n_tiles ? t_first + per : n_tiles;
+            stride = 1;
+        } else {
+            t_first = blockIdx.x;
+            t_last = n_tiles;
+            stride = gridDim.x;
+        }
         has_table = P.table_point >= 0;
         tpar = 1;
         last_pat = ~0ull;
@@ -457,7 +490,7 @@ struct PassCtx {
         // Pull this CTA's next tile into L2 while the current one is
         // transformed: HBM keeps streaming through the compute phase
         // without holding registers or shared memory.
-        if (t + stride < n_tiles) {
+        if (t + stride < t_last) {
             const double2* gn = psi + tile_base(t + stride);
 #pragma unroll
             for (int s = 0; s < NR; ++s) prefetch_l2(gn + o[s]);
@@ -579,7 +612,9 @@ struct PassCtx {
         uint32_t ts0 = 0, fb[3] = {0, 0, 0};
         const double2* E[3] = {nullptr, nullptr, nullptr};
         if constexpr (MODE == 3) ts0 = s_pl[rc.tb & 63u] ^ s_ph[rc.tb >> 6];
+        double2 tph = make_double2(1.0, 0.0);
         if constexpr (MODE == 4) {
+            if (P.tphase_off >= 0) tph = plan.tile_phase[P.tphase_off + t];
             const double* tb_ = tabc();
 #pragma unroll
             for (int f = 0; f < NFAC; ++f) {
@@ -614,6 +649,7 @@ struct PassCtx {
             if (q & 2u) a = make_double2(-a.x, -a.y);
             if (q & 1u) a = make_double2(-a.y, a.x);
             if constexpr (MODE == 4) {
+                if (P.tphase_off >= 0) a = make_double2(a.x * tph.x - a.y * tph.y, a.x * tph.y + a.y * tph.x);
                 double2 e;
 #pragma unroll
                 for (int f = 0; f < NFAC; ++f) {
@@ -720,7 +756,7 @@ struct PassCtx {
     Ctx ctx(plan.passes[pass_index], plan, psi, out, neg_dt, rank_bits, n_tiles, smem_raw, sdb_off_lo,     \
             sdb_off_hi, sdb_tbase, sdb_pl, sdb_ph);                                                        \
     ctx.setup();                                                                                           \
-    for (uint64_t t = blockIdx.x; t < n_tiles; t += ctx.stride) {                                          \
+    for (uint64_t t = ctx.t_first; t < ctx.t_last; t += ctx.stride) {                                      \
         ctx.begin_tile(t);                                                                                 \
         double2 v[Ctx::NR];                                                                                \
         PROG(ctx, v);                                                                                      \

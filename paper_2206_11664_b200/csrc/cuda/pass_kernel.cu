@@ -37,6 +37,13 @@ struct Interpreter {
     }
 };
 
+__global__ void k_tile_phase(PlanDev plan, int pass_index, double neg_dt, uint64_t rank_bits, uint64_t n_tiles,
+                             double2* __restrict__ out) {
+    const PassDev& P = plan.passes[pass_index];
+    for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < n_tiles; t += uint64_t(gridDim.x) * blockDim.x)
+        out[t] = dev::tile_constant_phase(plan, P, t, rank_bits, neg_dt);
+}
+
 template <int K, int RB>
 __global__ void __launch_bounds__(Cfg<K, RB>::NT, Cfg<K, RB>::MINB)
 k_tile_pass(const double2* __restrict__ psi, double2* __restrict__ out, PlanDev plan, int pass_index, double neg_dt,
@@ -90,7 +97,17 @@ void launch_k(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& pl
 
 int max_tile_qubits() { return 12; }
 
+void launch_tile_phase(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& plan, double dt,
+                       uint64_t rank_bits, double2* out) {
+    const uint64_t n_tiles = 1ull << ph.n_outer;
+    uint64_t blocks = (n_tiles + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    k_tile_phase<<<static_cast<unsigned>(blocks), 256, 0, s.stream>>>(plan, pass_index, -dt, rank_bits, n_tiles, out);
+    SDB_CUDA(cudaGetLastError());
+}
+
 size_t tile_pass_smem(const PassDev& ph) {
+    if (ph.k == 12 && ph.rbits == 3) return smem_bytes<12, 3>(ph);
     switch (ph.k) {
 #define SDB_K(KK) \
     case KK: return smem_bytes<KK, 4>(ph);

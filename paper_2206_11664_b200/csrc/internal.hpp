@@ -73,5 +73,8 @@ void launch_permute_bits(StateImpl& s, const double* src, double* dst, const int
 void launch_tile_pass(StateImpl& s, const PassDev& pass_host, int pass_index, const PlanDev& plan,
                       double dt, uint64_t rank_bits, double* out);
 int max_tile_qubits();
+// per-tile constant phases of a pass's table point (PassDev::tphase_off)
+void launch_tile_phase(StateImpl& s, const PassDev& pass_host, int pass_index, const PlanDev& plan, double dt,
+                       uint64_t rank_bits, double2* out);
 
 }  // namespace sdb

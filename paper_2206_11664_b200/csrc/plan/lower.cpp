@@ -427,6 +427,16 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                         }
                         if (pt.fac_send[f] == 0) pt.fac_sbeg[f] = 0;
                     }
+                    // Terms with no local support (u = 0) give a phase that is
+                    // constant over the tile: in factor mode it is precomputed
+                    // per tile (tile_phase) instead of entering the tables, so
+                    // the tables depend only on the outer bits of mixed terms.
+                    pt.c0_seg = -1;
+                    if (pt.n_fac > 0 && pt.n_seg > 0 && A.segs[pt.seg_off].fac == 0 && A.segs[pt.seg_off].u == 0) {
+                        pt.c0_seg = 0;
+                        pt.fac_sbeg[0] = 1;
+                        if (pt.fac_send[0] < 1) pt.fac_send[0] = 1;
+                    }
                     for (const T& t : sorted) {
                         A.term_hmask.push_back(t.zh);
                         A.term_lmask.push_back(0);
@@ -515,6 +525,7 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
         // of tiles and rebuilds it only when t >> pat_shift changes.
         pd.tab_half = pd.tab_words;
         pd.pat_shift = 64;
+        pd.tphase_off = -1;
         static const bool reorder = [] {
             const char* e = std::getenv("SDB_TABLE_REUSE");
             return !e || std::atoi(e) != 0;
@@ -522,13 +533,23 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
         if (pd.table_point >= 0 && reorder) {
             const PointDev& tp = A.points[pd.table_point];
             uint64_t pm = 0;
-            for (int q = 0; q < tp.n_terms; ++q) pm |= A.term_hmask[tp.term_off + q];
+            for (int sg = 0; sg < tp.n_seg; ++sg) {
+                if (sg == tp.c0_seg) continue;  // tile-constant terms: tile_phase
+                const SegDev& d = A.segs[tp.seg_off + sg];
+                for (int q = d.begin; q < d.end; ++q) pm |= A.term_hmask[tp.term_off + q];
+            }
+            if (tp.c0_seg >= 0) pd.tphase_off = 0;  // assigned by the executor (tile_phase buffer)
             std::vector<int> rest, top;
             for (int j = 0; j < pd.n_outer; ++j) ((pm >> pd.opos[j]) & 1 ? top : rest).push_back(pd.opos[j]);
             int j = 0;
             for (int b : rest) pd.opos[j++] = b;
             for (int b : top) pd.opos[j++] = b;
             pd.pat_shift = static_cast<int>(rest.size());
+            static const bool blocked = [] {
+                const char* e = std::getenv("SDB_BLOCKED");
+                return !e || std::atoi(e) != 0;
+            }();
+            pd.blocked = blocked ? 1 : 0;
             if (!pp.store_sigma.empty()) {
                 for (int q = 0; q < pd.n_outer; ++q) pd.st_opos[q] = pp.store_sigma[pd.opos[q]];
             }

@@ -118,6 +118,7 @@ struct PointDev {
     int fac_sbeg[3];  // factor f: its segments are [fac_sbeg, fac_send) relative to seg_off
     int fac_send[3];
     int fac_coff[3];  // complex table of factor f: double offset (even) in the table region
+    int c0_seg;       // factor mode: segment of the tile-constant terms (u = 0), -1 if none (PlanDev::tile_phase)
 };
 
 struct SegDev {
@@ -146,6 +147,8 @@ struct PassDev {
     int tab_double;   // 1: two copies, tile parity selects (unused: see pat_shift)
     int tab_half;     // words per copy when tab_double
     int pat_shift;    // tile-index bits >= pat_shift select the table's sign pattern (rebuild on change)
+    int blocked;      // 1: each CTA walks a contiguous block of tiles (table reuse), 0: grid-strided
+    int tphase_off;   // >= 0: per-tile phase of the table point's tile-constant terms at PlanDev::tile_phase + off
     double table_scale;  // factor mode: exact scale folded into E_0 (1 if applied elsewhere)
     int store_perm;      // 1: store out of place through a local bit permutation sigma
     int st_lpos[16];     // sigma(lpos[j])
@@ -167,6 +170,7 @@ struct PlanDev {
     const uint64_t* term_hmask; // outer (physical) part of each term's z-mask
     const uint32_t* term_lmask; // local-coordinate part (direct mode)
     const double* term_coeffs;  // c_t * dt_scale; the kernel multiplies by -dt
+    const double2* tile_phase;  // per-tile exp(-i dt theta_0) of passes with tphase_off >= 0
 };
 
 }  // namespace sdb

@@ -362,7 +362,7 @@ def run_ours(args, rank, world, local_rank):
                    "floor_group_applications": info["n_group_applications"]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": load_traffic(), "peak_source": peak_src,
-                     "kernel": "k_tile_pass (fused Clifford/diagonal tile pass)",
+                     "kernel": "fused Clifford/diagonal tile pass (sdb_pass: NVRTC-specialised per program for n_local >= 22; k_tile_pass interpreter otherwise)",
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "avg_launch_ms": dom["ms"] / max(1, dom["launches"]),
                      "step_hbm_gbs": step_gbs, "step_frac": step_gbs / peak,

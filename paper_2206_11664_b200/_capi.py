@@ -18,7 +18,9 @@ if not os.path.exists(LIB_PATH):
         "(no CPU fallback exists by design)"
     )
 
-lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+# RTLD_LOCAL: the library exports the reference's C++ names (simdiag::...), which
+# must not interpose on the reference compiled into oracle/_ref by the tests.
+lib = C.CDLL(LIB_PATH, mode=C.RTLD_LOCAL)
 
 u64 = C.c_uint64
 i32 = C.c_int32

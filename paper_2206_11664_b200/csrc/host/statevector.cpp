@@ -5,6 +5,7 @@
 #include "simdiag/statevector.hpp"
 
 #include <cmath>
+#include <deque>
 #include <cstring>
 #include <istream>
 #include <ostream>
@@ -26,7 +27,7 @@ void check(sd_status st) {
     throw std::runtime_error(m);
 }
 
-sd_group_desc desc_of(const DiagonalGroup& g, std::vector<std::vector<int32_t>>& keep) {
+sd_group_desc desc_of(const DiagonalGroup& g, std::deque<std::vector<int32_t>>& keep) {
     const CliffordCircuit& c = g.circuit;
     auto& h0 = keep.emplace_back(c.h_pre.begin(), c.h_pre.end());
     auto& cx = keep.emplace_back();
@@ -151,7 +152,7 @@ void StateVector::apply_diagonal_exp(const DiagonalGroup& group, double dt) {
 void StateVector::apply_clifford(const CliffordCircuit& c) {
     DiagonalGroup g;
     g.circuit = c;
-    std::vector<std::vector<int32_t>> keep;
+    std::deque<std::vector<int32_t>> keep;  // stable element addresses
     const sd_group_desc d = desc_of(g, keep);
     check(sd_apply_clifford(sync_to_device(), &d));
 }
@@ -159,7 +160,7 @@ void StateVector::apply_clifford(const CliffordCircuit& c) {
 void StateVector::apply_clifford_inverse(const CliffordCircuit& c) {
     DiagonalGroup g;
     g.circuit = c;
-    std::vector<std::vector<int32_t>> keep;
+    std::deque<std::vector<int32_t>> keep;  // stable element addresses
     const sd_group_desc d = desc_of(g, keep);
     check(sd_apply_clifford_inverse(sync_to_device(), &d));
 }
@@ -212,7 +213,7 @@ void EvolutionPlan::validate() const {
 void evolve_grouped(std::span<const DiagonalGroup> groups, StateVector& psi, const EvolutionPlan& plan) {
     plan.validate();
     if (plan.n_steps == 0) return;
-    std::vector<std::vector<int32_t>> keep;
+    std::deque<std::vector<int32_t>> keep;  // stable element addresses
     std::vector<sd_group_desc> descs;
     for (const DiagonalGroup& g : groups) descs.push_back(desc_of(g, keep));
     sd_plan_options o;

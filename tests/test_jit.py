@@ -1,0 +1,70 @@
+"""Run-time specialised tile-pass kernels (csrc/cuda/jit.cpp): the NVRTC
+sources generated for a plan compile for sm_100a on CPU, and on the GPU the
+specialised kernels (used for shards >= 22 qubits, i.e. by the benchmark)
+reproduce the reference exactly like the interpreter kernel does."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2206_11664_b200 import models as M
+
+
+def test_jit_sources_compile_for_sm100a(sd):
+    for cfg, n in ((4, 16), (2, 12)):
+        groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(M.config_text(cfg, n=n)))
+        assert sd.simdiag.jit_compile_preview(n, groups, order=M.CONFIGS[cfg]["order"]) >= 1
+
+
+@pytest.fixture
+def force_jit():
+    old = os.environ.get("SDB_JIT")
+    os.environ["SDB_JIT"] = "1"
+    yield
+    if old is None:
+        del os.environ["SDB_JIT"]
+    else:
+        os.environ["SDB_JIT"] = old
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,n,k", [(4, 16, 12), (2, 12, 12), (3, 13, 12), (5, 13, 10)])
+def test_jit_evolution_matches_reference(cfg, n, k, sd, ref, port, force_jit):
+    text = M.config_text(cfg, n=n)
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
+    order, dt, steps = M.CONFIGS[cfg]["order"], M.CONFIGS[cfg]["dt"] * 5, 3
+    init = M.CONFIGS[cfg]["init"]
+    if init[0] == "plus":
+        psi0 = np.full(1 << n, 1 / np.sqrt(1 << n), np.complex128)
+    elif init[0] == "random":
+        psi0 = port.random_state(n, init[1])
+    else:
+        psi0 = np.zeros(1 << n, np.complex128)
+        psi0[M.initial_index(cfg, n)] = 1
+    s = sd.StateVector(n)
+    s.upload(psi0)
+    sd.TrotterPlan(s, groups, order=order, tile_qubits=k).evolve(dt, steps)
+    got = s.amplitudes()
+    h, _, _ = ref.partition_text(text)
+    want, _ = ref.evolve_grouped(h, psi0, n, dt, steps, order)
+    ref.free(h)
+    assert np.max(np.abs(got - want)) < 1e-10
+    assert abs(np.linalg.norm(got) - 1) < 1e-12
+
+
+@pytest.mark.gpu
+def test_jit_sharded_local_shards(sd, ref, force_jit):
+    cfg, n, world = 4, 14, 4
+    text = M.config_text(cfg, n=n)
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
+    psi0 = np.zeros(1 << n, np.complex128)
+    psi0[M.neel_index(n)] = 1
+    sh = sd.LocalShards(n, world)
+    sh.upload(psi0)
+    sh.plan(groups, tile_qubits=10)
+    sh.evolve(0.05, 3)
+    got = sh.amplitudes()
+    h, _, _ = ref.partition_text(text)
+    want, _ = ref.evolve_grouped(h, psi0, n, 0.05, 3, 1)
+    ref.free(h)
+    assert np.max(np.abs(got - want)) < 1e-10

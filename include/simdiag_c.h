@@ -180,7 +180,8 @@ typedef struct sd_plan_options {
     int order;        /* 1 = first-order Lie-Trotter (evolve_grouped), 2 = Suzuki S2 */
     int tile_qubits;  /* k: qubits per shared-memory tile; 0 = auto */
     int fuse;         /* 1 = fused tile passes (default); 0 = reference sweep sequence */
-    int use_graph;    /* 1 = capture one step as a CUDA graph when launch-bound */
+    int use_graph;    /* 0 = auto (replay each step as a CUDA graph for unsharded states of
+                         <= 20 qubits, which are launch-bound), 1 = always, -1 = never */
     int relabel;      /* 1 = allow qubit relabelling between passes (default) */
     int reserved[7];
 } sd_plan_options;

@@ -39,6 +39,8 @@ struct StepExec {
     void* dev_block = nullptr;
     double2* tile_phase = nullptr;  // per-tile constant phases (passes with tphase_off >= 0)
     double phase_dt = std::nan("");  // dt the tile phases were computed for
+    cudaGraphExec_t graph = nullptr; // one captured step (small, launch-bound states)
+    double graph_dt = std::nan("");
     std::string program;
 };
 
@@ -323,18 +325,24 @@ void harvest(sd_plan& p) {
     p.ev_used = 0;
 }
 
+// per-tile constant phases of the step's diagonal passes, once per dt
+void ensure_tile_phase(sd_plan& p, StepExec& E, double dt) {
+    if (!E.tile_phase || E.phase_dt == dt) return;
+    sdb::StateImpl& s = p.state->impl;
+    const uint64_t rank_bits = uint64_t(s.rank) << s.n_local;
+    for (size_t i = 0; i < E.host_passes.size(); ++i) {
+        if (E.host_passes[i].tphase_off >= 0) {
+            sdb::launch_tile_phase(s, E.host_passes[i], static_cast<int>(i), E.dev, dt, rank_bits,
+                                   E.tile_phase + E.host_passes[i].tphase_off);
+        }
+    }
+    E.phase_dt = dt;
+}
+
 void run_segment(sd_plan& p, StepExec& E, size_t seg, double dt) {
     sdb::StateImpl& s = p.state->impl;
     const uint64_t rank_bits = uint64_t(s.rank) << s.n_local;
-    if (E.tile_phase && !(E.phase_dt == dt)) {
-        for (size_t i = 0; i < E.host_passes.size(); ++i) {
-            if (E.host_passes[i].tphase_off >= 0) {
-                sdb::launch_tile_phase(s, E.host_passes[i], static_cast<int>(i), E.dev, dt, rank_bits,
-                                       E.tile_phase + E.host_passes[i].tphase_off);
-            }
-        }
-        E.phase_dt = dt;
-    }
+    ensure_tile_phase(p, E, dt);
     const double bytes = 2.0 * 16.0 * double(s.amps_count());
     const bool exch = E.ss.segs[seg].exchange_after;
     const int first = E.seg_first[seg], count = E.seg_count[seg];
@@ -386,14 +394,47 @@ void run_step_unfused(sd_plan& p, double dt) {
     }
 }
 
+// Small states are launch-bound (config 1: a 1 MiB state streams in well under
+// a microsecond): one step's launches are captured into a CUDA graph per
+// (layout, dt) and replayed. Used on one unsharded device when the shard has
+// <= 20 qubits (use_graph = 1 forces it, -1 disables it), not while profiling.
+bool graph_mode(const sd_plan& p) {
+    const sdb::StateImpl& s = p.state->impl;
+    if (!p.opts.fuse || s.world != 1 || p.profiling || p.opts.use_graph < 0) return false;
+    return p.opts.use_graph > 0 || s.n_local <= 20;
+}
+
+void run_step_graph(sd_plan& p, double dt) {
+    sdb::StateImpl& s = p.state->impl;
+    StepExec& E = step_for(p, s.phys_of);
+    if (!E.graph || !(E.graph_dt == dt)) {
+        if (E.graph) SDB_CUDA(cudaGraphExecDestroy(E.graph));
+        E.graph = nullptr;
+        ensure_tile_phase(p, E, dt);  // outside the graph: once per dt
+        cudaGraph_t g = nullptr;
+        SDB_CUDA(cudaStreamBeginCapture(s.stream, cudaStreamCaptureModeThreadLocal));
+        for (size_t seg = 0; seg < E.ss.segs.size(); ++seg) run_segment(p, E, seg, dt);
+        SDB_CUDA(cudaStreamEndCapture(s.stream, &g));
+        SDB_CUDA(cudaGraphInstantiate(&E.graph, g, 0));
+        SDB_CUDA(cudaGraphDestroy(g));
+        E.graph_dt = dt;
+    } else {
+        for (size_t i = 0; i < E.host_passes.size(); ++i) bump(s, s.amps_count(), s.amps_count());
+    }
+    SDB_CUDA(cudaGraphLaunch(E.graph, s.stream));
+    s.phys_of = E.ss.phys_out;
+}
+
 void evolve(sd_plan& p, double dt, int n_steps, bool wait) {
     require(std::isfinite(dt), "plan needs finite total_time");
     if (n_steps < 0) throw std::invalid_argument("plan needs n_steps >= 0");
     sdb::StateImpl& s = p.state->impl;
     SDB_CUDA(cudaSetDevice(s.device));
+    const bool graphs = graph_mode(p);
     for (int step = 0; step < n_steps; ++step) {
-        if (p.opts.fuse) run_step_fused(p, dt);
-        else run_step_unfused(p, dt);
+        if (!p.opts.fuse) run_step_unfused(p, dt);
+        else if (graphs) run_step_graph(p, dt);
+        else run_step_fused(p, dt);
     }
     if (wait) SDB_CUDA(cudaStreamSynchronize(s.stream));
     harvest(p);
@@ -837,6 +878,7 @@ void sd_plan_destroy(sd_plan* p) {
         cudaEventDestroy(e.second);
     }
     for (auto& kv : p->steps) {
+        if (kv.second->graph) cudaGraphExecDestroy(kv.second->graph);
         if (kv.second->dev_block) cudaFree(kv.second->dev_block);
         if (kv.second->tile_phase) cudaFree(kv.second->tile_phase);
     }

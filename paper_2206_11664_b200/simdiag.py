@@ -466,14 +466,14 @@ class TrotterPlan:
     over `groups`, bound to `psi`. Reusable across evolve() calls."""
 
     def __init__(self, psi: StateVector, groups: Sequence[DiagonalGroup], order: int = 1,
-                 tile_qubits: int = 0, fuse: bool = True, use_graph: bool = False):
+                 tile_qubits: int = 0, fuse: bool = True, use_graph: Optional[bool] = None):
         self.psi = psi
         opts = A.PlanOptions()
         check(A.sd_plan_options_default(C.byref(opts)))
         opts.order = order
         opts.tile_qubits = tile_qubits
         opts.fuse = 1 if fuse else 0
-        opts.use_graph = 1 if use_graph else 0
+        opts.use_graph = 0 if use_graph is None else (1 if use_graph else -1)  # None: auto (small states)
         descs = (A.GroupDesc * max(1, len(groups)))()
         self._keep = []
         for i, g in enumerate(groups):

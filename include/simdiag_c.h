@@ -170,6 +170,20 @@ sd_status sd_apply_diagonal_exp(sd_state* s, const uint64_t* z_masks, const doub
 sd_status sd_apply_clifford(sd_state* s, const sd_group_desc* g);
 sd_status sd_apply_clifford_inverse(sd_state* s, const sd_group_desc* g);
 
+/* ---- the paper's comparison method and observables */
+/* apply_pauli_rotation (statevector.cpp:288-337): exp(-i coeff dt P), P the
+ * Hermitian Pauli with symplectic masks (x, z) (pauli.hpp:23-61). */
+sd_status sd_apply_pauli_rotation(sd_state* s, uint64_t x_mask, uint64_t z_mask, double coeff, double dt);
+/* evolve_baseline (evolve.cpp:21-45): n_steps x one rotation sweep per term
+ * in the given order (Hamiltonian order, or groups flattened = group-major). */
+sd_status sd_evolve_baseline(sd_state* s, const uint64_t* x_masks, const uint64_t* z_masks, const double* coeffs,
+                             size_t n_terms, double dt, int n_steps);
+/* expectation (evolve.cpp:99-135): sum_k coeffs[k] <psi|P_k|psi>; real part
+ * in *re, |imaginary residue| in *imag_residue (may be NULL). Device
+ * reductions in a fixed order (bit-identical for any launch). */
+sd_status sd_expectation(sd_state* s, const uint64_t* x_masks, const uint64_t* z_masks, const double* coeffs,
+                         size_t n_terms, double* re, double* imag_residue);
+
 /* ------------------------------------------------------------------ */
 /* Fused Trotter plan (replaces evolve_grouped, evolve.cpp:47-58)       */
 /* ------------------------------------------------------------------ */

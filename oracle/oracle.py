@@ -243,6 +243,9 @@ class Ref:
         L.ref_plus_state.argtypes = [C.c_int, dblp]
         L.ref_kernel.argtypes = [C.c_int, dblp, C.c_int, C.c_int, C.c_uint64, i32p, C.c_size_t, u64p, dblp,
                                  C.c_size_t, C.c_double]
+        L.ref_pauli_rotation.argtypes = [dblp, C.c_int, C.c_uint64, C.c_uint64, C.c_double, C.c_double]
+        L.ref_evolve_baseline_text.argtypes = [C.c_char_p, C.c_size_t, dblp, C.c_int, C.c_double, C.c_int]
+        L.ref_expectation_text.argtypes = [C.c_char_p, C.c_size_t, dblp, C.c_int, dblp, dblp]
         L.ref_norm.argtypes = [dblp, C.c_int]
         L.ref_norm.restype = C.c_double
 
@@ -321,6 +324,27 @@ class Ref:
     def norm(self, psi, n) -> float:
         a = np.ascontiguousarray(psi, dtype=np.complex128)
         return self.lib.ref_norm(a.ctypes.data_as(dblp), n)
+
+    def pauli_rotation(self, psi, n, x, z, coeff, dt):
+        """StateVector::apply_pauli_rotation (statevector.cpp:288-337)."""
+        a = np.ascontiguousarray(psi, dtype=np.complex128).copy()
+        self._err(self.lib.ref_pauli_rotation(a.ctypes.data_as(dblp), n, x, z, coeff, dt))
+        return a
+
+    def evolve_baseline(self, text: str, psi, n, dt, steps):
+        """evolve_baseline(Hamiltonian, ...) (evolve.cpp:21-32), restated loop."""
+        a = np.ascontiguousarray(psi, dtype=np.complex128).copy()
+        b = text.encode()
+        self._err(self.lib.ref_evolve_baseline_text(b, len(b), a.ctypes.data_as(dblp), n, dt, steps))
+        return a
+
+    def expectation(self, text: str, psi, n):
+        """expectation (evolve.cpp:99-135), restated loop: (re, |imag residue|)."""
+        a = np.ascontiguousarray(psi, dtype=np.complex128)
+        b = text.encode()
+        re, im = C.c_double(), C.c_double()
+        self._err(self.lib.ref_expectation_text(b, len(b), a.ctypes.data_as(dblp), n, C.byref(re), C.byref(im)))
+        return re.value, im.value
 
 
 def port() -> Port:

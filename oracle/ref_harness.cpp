@@ -8,6 +8,9 @@
 // in this image), so evolve_grouped's 12-line loop (proj/src/evolve.cpp:47-58)
 // is restated here with the same calls in the same order; S2 is the
 // composition SURVEY §8a D1 defines (the reference has no S2).
+#include <algorithm>
+#include <bit>
+#include <complex>
 #include <cstring>
 #include <memory>
 #include <sstream>
@@ -214,6 +217,67 @@ int ref_kernel(int which, double* re_im, int n, int a, uint64_t mask, const int3
             default: throw std::invalid_argument("unknown kernel");
         }
         store_state(psi, re_im);
+    });
+}
+
+// StateVector::apply_pauli_rotation (statevector.cpp:288-337) on one term.
+int ref_pauli_rotation(double* re_im, int n, uint64_t x, uint64_t z, double coeff, double dt) {
+    return guarded([&] {
+        simdiag::StateVector psi(n);
+        load_state(psi, re_im);
+        psi.apply_pauli_rotation(simdiag::WeightedTerm{coeff, simdiag::PauliString::from_masks(n, x, z)}, dt);
+        store_state(psi, re_im);
+    });
+}
+
+// evolve_baseline(const Hamiltonian&, ...) restated (evolve.cpp:21-32: same
+// calls, same order; evolve.cpp itself needs Eigen).
+int ref_evolve_baseline_text(const char* text, size_t len, double* re_im, int n, double dt, int steps) {
+    return guarded([&] {
+        std::istringstream in(std::string(text, len));
+        const auto h = simdiag::Hamiltonian::load(in);
+        simdiag::StateVector psi(n);
+        load_state(psi, re_im);
+        for (int s = 0; s < steps; ++s)
+            for (const auto& term : h.terms()) psi.apply_pauli_rotation(term, dt);
+        store_state(psi, re_im);
+    });
+}
+
+// expectation (evolve.cpp:99-135) restated: the same 256 fixed chunks per term.
+int ref_expectation_text(const char* text, size_t len, const double* re_im, int n, double* re, double* imag) {
+    return guarded([&] {
+        std::istringstream in(std::string(text, len));
+        const auto h = simdiag::Hamiltonian::load(in);
+        simdiag::StateVector psi(n);
+        load_state(psi, re_im);
+        const std::uint64_t dim = psi.dim();
+        const std::complex<double> i_pow[4] = {{1, 0}, {0, 1}, {-1, 0}, {0, -1}};
+        std::complex<double> total = 0.0;
+        for (const auto& term : h.terms()) {
+            const std::uint64_t x = term.pauli.x_mask();
+            const std::uint64_t z = term.pauli.z_mask();
+            const std::complex<double> base = i_pow[term.pauli.phase_exp()];
+            constexpr int kChunks = 256;
+            std::complex<double> partial[kChunks] = {};
+            const std::uint64_t chunk_len = (dim + kChunks - 1) / kChunks;
+            for (int c = 0; c < kChunks; ++c) {
+                const std::uint64_t begin = c * chunk_len;
+                const std::uint64_t end = std::min(dim, begin + chunk_len);
+                std::complex<double> acc = 0.0;
+                for (std::uint64_t b = begin; b < end; ++b) {
+                    const bool parity = std::popcount((b ^ x) & z) & 1;
+                    const std::complex<double> ph = parity ? -base : base;
+                    acc += std::conj(psi[b]) * ph * psi[b ^ x];
+                }
+                partial[c] = acc;
+            }
+            std::complex<double> sum = 0.0;
+            for (int c = 0; c < kChunks; ++c) sum += partial[c];
+            total += term.coeff * sum;
+        }
+        *re = total.real();
+        *imag = std::abs(total.imag());
     });
 }
 

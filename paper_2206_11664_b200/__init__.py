@@ -21,8 +21,10 @@ from .simdiag import (  # noqa: F401
     comm_unique_id,
     commutes,
     diagonalize_group,
+    evolve_baseline,
     evolve_grouped,
     exchange_routes,
+    expectation,
     fidelity,
     greedy_partition,
     norm,
@@ -35,5 +37,5 @@ __all__ = [
     "CliffordCircuit", "CommutingGroup", "DiagonalGroup", "EvolutionPlan", "Hamiltonian",
     "PauliString", "StateVector", "TrotterPlan", "WeightedTerm", "commutes", "diagonalize_group",
     "evolve_grouped", "fidelity", "greedy_partition", "norm", "partition_and_diagonalize", "models",
-    "LocalShards", "comm_unique_id", "plan_preview",
+    "LocalShards", "comm_unique_id", "plan_preview", "evolve_baseline", "expectation",
 ]

@@ -146,6 +146,10 @@ sd_plan_kernel_times = _sig(
 sd_comm_unique_id = _sig("sd_comm_unique_id", [C.c_char_p])
 sd_state_attach_comm = _sig("sd_state_attach_comm", [P, C.c_char_p])
 sd_state_canonicalize = _sig("sd_state_canonicalize", [P])
+sd_apply_pauli_rotation = _sig("sd_apply_pauli_rotation", [P, u64, u64, dbl, dbl])
+sd_evolve_baseline = _sig("sd_evolve_baseline", [P, C.POINTER(u64), C.POINTER(u64), C.POINTER(dbl), sz, dbl, C.c_int])
+sd_expectation = _sig("sd_expectation", [P, C.POINTER(u64), C.POINTER(u64), C.POINTER(dbl), sz, C.POINTER(dbl),
+                                         C.POINTER(dbl)])
 sd_jit_compile_preview = _sig("sd_jit_compile_preview", [C.c_int, C.c_int, C.POINTER(GroupDesc), sz,
                                                          C.POINTER(PlanOptions), C.POINTER(sz)])
 sd_state_create_local_shards = _sig("sd_state_create_local_shards", [C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(P)])
@@ -176,7 +180,7 @@ EXPORTED = [
     "sd_plan_describe", "sd_plan_preview", "sd_evolve", "sd_evolve_async", "sd_plan_set_profiling",
     "sd_plan_kernel_times", "sd_comm_unique_id", "sd_state_attach_comm", "sd_state_canonicalize",
     "sd_state_create_local_shards", "sd_evolve_local", "sd_local_canonicalize", "sd_exchange_routes",
-    "sd_jit_compile_preview",
+    "sd_jit_compile_preview", "sd_apply_pauli_rotation", "sd_evolve_baseline", "sd_expectation",
 ]
 
 

@@ -1165,4 +1165,68 @@ sd_status sd_jit_compile_preview(int n, int world, const sd_group_desc* groups, 
     });
 }
 
+sd_status sd_apply_pauli_rotation(sd_state* h, uint64_t x_mask, uint64_t z_mask, double coeff, double dt) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require_unsharded(s);
+        require_identity_layout(s);
+        const uint64_t all = s.amps_count() - 1;
+        if ((x_mask | z_mask) & ~all) throw std::invalid_argument("pauli rotation: qubit count mismatch");
+        SDB_CUDA(cudaSetDevice(s.device));
+        sdb::launch_pauli_rotation(s, x_mask, z_mask, coeff, dt);
+        bump(s, s.amps_count(), s.amps_count());
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
+sd_status sd_evolve_baseline(sd_state* h, const uint64_t* x, const uint64_t* z, const double* coeffs, size_t n_terms,
+                             double dt, int n_steps) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require_unsharded(s);
+        require_identity_layout(s);
+        require(n_terms == 0 || (x && z && coeffs), "null term arrays");
+        if (n_steps < 0) throw std::invalid_argument("plan needs n_steps >= 0");
+        if (!std::isfinite(dt)) throw std::invalid_argument("plan needs finite total_time");
+        const uint64_t all = s.amps_count() - 1;
+        for (size_t k = 0; k < n_terms; ++k) {
+            if ((x[k] | z[k]) & ~all) throw std::invalid_argument("hamiltonian/state qubit counts differ");
+        }
+        SDB_CUDA(cudaSetDevice(s.device));
+        for (int step = 0; step < n_steps; ++step) {
+            for (size_t k = 0; k < n_terms; ++k) {
+                sdb::launch_pauli_rotation(s, x[k], z[k], coeffs[k], dt);
+                bump(s, s.amps_count(), s.amps_count());
+            }
+        }
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
+sd_status sd_expectation(sd_state* h, const uint64_t* x, const uint64_t* z, const double* coeffs, size_t n_terms,
+                         double* re, double* imag_residue) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require_unsharded(s);
+        require(re != nullptr, "null output");
+        require(n_terms == 0 || (x && z && coeffs), "null term arrays");
+        if (!is_identity(s.phys_of)) {
+            SDB_CUDA(cudaSetDevice(s.device));
+            permute_local(s);
+        }
+        const uint64_t all = s.amps_count() - 1;
+        SDB_CUDA(cudaSetDevice(s.device));
+        double tr = 0.0, ti = 0.0;
+        for (size_t k = 0; k < n_terms; ++k) {
+            if ((x[k] | z[k]) & ~all) throw std::invalid_argument("hamiltonian/state qubit counts differ");
+            double r = 0.0, i = 0.0;
+            sdb::device_expectation_term(s, x[k], z[k], &r, &i);
+            tr += coeffs[k] * r;
+            ti += coeffs[k] * i;
+        }
+        *re = tr;
+        if (imag_residue) *imag_residue = std::abs(ti);
+    });
+}
+
 }  // extern "C"

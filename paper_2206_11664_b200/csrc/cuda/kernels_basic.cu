@@ -112,6 +112,66 @@ __global__ void k_reduce(const double2* __restrict__ a, const double2* __restric
     if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
 }
 
+// <psi| P |psi> partial sums for one Pauli term P = i^{phase} X^x Z^z
+// (expectation, reference evolve.cpp:99-135): sum_b conj(psi[b]) ph(b) psi[b^x],
+// ph(b) = base * (-1)^{popc((b^x) & z)}; same fixed-order block partials as k_reduce.
+__global__ void k_expect(const double2* __restrict__ a, uint64_t n, uint64_t x, uint64_t z, double2 base,
+                         double2* __restrict__ partial) {
+    __shared__ double2 red[kThreads];
+    double sr = 0.0, si = 0.0;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const double2 u = a[i];
+        const double2 w = a[i ^ x];
+        const bool odd = __popcll((i ^ x) & z) & 1;
+        const double pr = odd ? -base.x : base.x, pi = odd ? -base.y : base.y;
+        const double tr = pr * w.x - pi * w.y, ti = pr * w.y + pi * w.x;  // ph * psi[b^x]
+        sr += u.x * tr + u.y * ti;                                        // conj(psi[b]) * (...)
+        si += u.x * ti - u.y * tr;
+    }
+    red[threadIdx.x] = make_double2(sr, si);
+    __syncthreads();
+    for (int w = kThreads / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            red[threadIdx.x].x += red[threadIdx.x + w].x;
+            red[threadIdx.x].y += red[threadIdx.x + w].y;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+// apply_pauli_rotation (reference statevector.cpp:288-337): exp(-i theta P).
+// x == 0: a[b] *= (cos, -+sin) by the parity of b & z; otherwise over pairs
+// (b, b^x): a0' = c a0 + w0 a1, a1' = c a1 + w1 a0 with w = -i sin(theta) i^{phase}
+// and its sign from the parities of the pair's z bits.
+__global__ void k_pauli_rotation(double2* __restrict__ a, uint64_t n, uint64_t x, uint64_t z, double c, double s,
+                                 double2 w, int t0, int y_parity) {
+    if (x == 0) {
+        for (uint64_t b = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; b < n;
+             b += uint64_t(gridDim.x) * blockDim.x) {
+            const bool odd = __popcll(b & z) & 1;
+            const double fr = c, fi = odd ? s : -s;
+            const double2 v = a[b];
+            a[b] = make_double2(v.x * fr - v.y * fi, v.x * fi + v.y * fr);
+        }
+        return;
+    }
+    const uint64_t pairs = n >> 1;
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < pairs;
+         p += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i0 = insert_zero(p, t0);
+        const uint64_t i1 = i0 ^ x;
+        const bool par0 = __popcll(i0 & z) & 1;
+        const bool par1 = par0 ^ (y_parity != 0);
+        const double2 w0 = par1 ? make_double2(-w.x, -w.y) : w;
+        const double2 w1 = par0 ? make_double2(-w.x, -w.y) : w;
+        const double2 a0 = a[i0], a1 = a[i1];
+        a[i0] = make_double2(c * a0.x + (w0.x * a1.x - w0.y * a1.y), c * a0.y + (w0.x * a1.y + w0.y * a1.x));
+        a[i1] = make_double2(c * a1.x + (w1.x * a0.x - w1.y * a0.y), c * a1.y + (w1.x * a0.y + w1.y * a0.x));
+    }
+}
+
 // apply_hadamard (reference statevector.cpp:156-174): one sweep over pairs,
 // scaled by fl(1/sqrt2) per gate exactly as the reference does.
 __global__ void k_hadamard(double2* __restrict__ a, uint64_t pairs, int t) {
@@ -309,6 +369,52 @@ void launch_diag_exp(StateImpl& s, const std::vector<uint64_t>& masks,
     SDB_CUDA(cudaGetLastError());
     if (dm) SDB_CUDA(cudaFreeAsync(dm, s.stream));
     if (dc) SDB_CUDA(cudaFreeAsync(dc, s.stream));
+}
+
+void launch_pauli_rotation(StateImpl& s, uint64_t x, uint64_t z, double coeff, double dt) {
+    const double theta = coeff * dt;
+    const double c = std::cos(theta), sn = std::sin(theta);
+    // w = -i sin(theta) * i^{phase_exp}, phase_exp = popc(x & z) & 3 (pauli.cpp:64-66)
+    double wr = 0.0, wi = -sn;
+    const int ph = __builtin_popcountll(x & z) & 3;
+    for (int k = 0; k < ph; ++k) {
+        const double t = wr;
+        wr = -wi;
+        wi = t;
+    }
+    const uint64_t n = s.amps_count();
+    const int t0 = x ? __builtin_ctzll(x) : 0;
+    const int ypar = __builtin_popcountll(z & x) & 1;
+    k_pauli_rotation<<<grid_for(x ? n >> 1 : n), kThreads, 0, s.stream>>>(d2(s), n, x, z, c, sn, make_double2(wr, wi),
+                                                                         t0, ypar);
+    SDB_CUDA(cudaGetLastError());
+}
+
+void device_expectation_term(StateImpl& s, uint64_t x, uint64_t z, double* re, double* im) {
+    const uint64_t n = s.amps_count();
+    const unsigned blocks = grid_for(n);
+    if (!s.reduce_buf) SDB_CUDA(cudaMalloc(reinterpret_cast<void**>(&s.reduce_buf), 148 * 16 * sizeof(double2)));
+    double2* part = reinterpret_cast<double2*>(s.reduce_buf);
+    const int ph = __builtin_popcountll(x & z) & 3;
+    const double2 base[4] = {{1, 0}, {0, 1}, {-1, 0}, {0, -1}};
+    k_expect<<<blocks, kThreads, 0, s.stream>>>(d2(s), n, x, z, base[ph], part);
+    SDB_CUDA(cudaGetLastError());
+    std::vector<double2> h(blocks);
+    SDB_CUDA(cudaMemcpyAsync(h.data(), part, blocks * sizeof(double2), cudaMemcpyDeviceToHost, s.stream));
+    SDB_CUDA(cudaStreamSynchronize(s.stream));
+    while (h.size() > 1) {
+        std::vector<double2> nx((h.size() + 1) / 2);
+        for (size_t i = 0; i < nx.size(); ++i) {
+            nx[i] = h[2 * i];
+            if (2 * i + 1 < h.size()) {
+                nx[i].x += h[2 * i + 1].x;
+                nx[i].y += h[2 * i + 1].y;
+            }
+        }
+        h.swap(nx);
+    }
+    *re = h[0].x;
+    *im = h[0].y;
 }
 
 void launch_permute_bits(StateImpl& s, const double* src, double* dst, const int* new_pos_host,

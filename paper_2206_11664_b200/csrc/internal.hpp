@@ -67,6 +67,10 @@ void launch_diag_exp(StateImpl& s, const std::vector<uint64_t>& masks,
                      const std::vector<double>& coeffs, double dt);
 void launch_permute_bits(StateImpl& s, const double* src, double* dst, const int* new_pos,
                          int n_bits);
+// apply_pauli_rotation (statevector.cpp:288-337) and one term of expectation
+// (evolve.cpp:99-135): <psi| i^{phase} X^x Z^z |psi>
+void launch_pauli_rotation(StateImpl& s, uint64_t x, uint64_t z, double coeff, double dt);
+void device_expectation_term(StateImpl& s, uint64_t x, uint64_t z, double* re, double* im);
 
 // Fused pass launcher (pass_kernel.cu).
 // out: destination buffer (nullptr = in place on s.amps).

@@ -429,6 +429,10 @@ class StateVector:
         d, keep = g._desc()
         check(A.sd_apply_clifford_inverse(self._s, C.byref(d)))
 
+    def apply_pauli_rotation(self, term: WeightedTerm, dt: float) -> None:
+        """exp(-i coeff dt P) (statevector.cpp:288-337)."""
+        check(A.sd_apply_pauli_rotation(self._s, term.pauli.x_mask, term.pauli.z_mask, term.coeff, dt))
+
 
 def norm(psi: StateVector) -> float:
     return psi.norm()
@@ -547,6 +551,41 @@ def evolve_grouped(groups: Sequence[DiagonalGroup], psi: StateVector, plan: Evol
     if plan.n_steps == 0:
         return
     TrotterPlan(psi, groups, order=plan.order, **options).evolve(dt, plan.n_steps)
+
+
+def _term_arrays(terms):
+    xs = _u64arr([t.pauli.x_mask for t in terms])
+    zs = _u64arr([t.pauli.z_mask for t in terms])
+    cs = _dblarr([t.coeff for t in terms])
+    return xs, zs, cs
+
+
+def evolve_baseline(h, psi: StateVector, plan: EvolutionPlan) -> None:
+    """The paper's per-term baseline (evolve.cpp:21-45): n_steps x one rotation
+    sweep per term; `h` is a Hamiltonian (input order) or a list of
+    CommutingGroup/DiagonalGroup (group-major order)."""
+    plan.validate()
+    if isinstance(h, Hamiltonian):
+        if h.n_qubits != psi.n:
+            raise ValueError("hamiltonian/state qubit counts differ")
+        terms = h.terms()
+    else:
+        terms = [t for g in h for t in g.terms]
+    dt = plan.dt() if plan.n_steps > 0 else 0.0
+    xs, zs, cs = _term_arrays(terms)
+    check(A.sd_evolve_baseline(psi._s, xs, zs, cs, len(terms), dt, plan.n_steps))
+
+
+def expectation(h: "Hamiltonian", psi: StateVector, with_residue: bool = False):
+    """<psi|H|psi> (evolve.cpp:99-135) as device reductions; returns the real
+    part (and the |imaginary residue| when with_residue)."""
+    if h.n_qubits != psi.n:
+        raise ValueError("hamiltonian/state qubit counts differ")
+    terms = h.terms()
+    xs, zs, cs = _term_arrays(terms)
+    re, im = C.c_double(), C.c_double()
+    check(A.sd_expectation(psi._s, xs, zs, cs, len(terms), C.byref(re), C.byref(im)))
+    return (re.value, im.value) if with_residue else re.value
 
 
 def comm_unique_id() -> bytes:

@@ -281,6 +281,19 @@ sd_status sd_state_create_local_shards(int n_qubits, int world, const int* devic
 sd_status sd_evolve_local(sd_plan* const* plans, int world, double dt, int n_steps);
 sd_status sd_local_canonicalize(sd_state* const* shards, int world);
 
+/* Fused exchange over peer memory: the pass in front of a remap stores every
+ * amplitude straight into the receiving rank's buffer (NVLink stores, one
+ * kernel for compute + exchange; no separate collective), followed by one
+ * barrier; state and receive buffers then swap roles. Multi-process:
+ * sd_state_ipc_handles gives this shard's two 64-byte cudaIpcMemHandles (state,
+ * receive buffer); the caller all-gathers them (world x 128 bytes in rank
+ * order) and passes them to sd_state_attach_peers on every rank (after
+ * sd_state_attach_comm, which supplies the barrier). In-process shards:
+ * sd_local_enable_p2p. */
+sd_status sd_state_ipc_handles(sd_state* s, unsigned char out[128]);
+sd_status sd_state_attach_peers(sd_state* s, const unsigned char* handles);
+sd_status sd_local_enable_p2p(sd_state* const* shards, int world);
+
 /* Chunk routing of one remap exchange for `rank` (host-only; the routing both
  * transports execute, exported for multi-process tests). swaps = 2*n_swaps
  * ints (global bit, local bit) as in sd_plan_preview's JSON. Offsets and

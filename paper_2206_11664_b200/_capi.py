@@ -155,6 +155,9 @@ sd_jit_compile_preview = _sig("sd_jit_compile_preview", [C.c_int, C.c_int, C.POI
 sd_state_create_local_shards = _sig("sd_state_create_local_shards", [C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(P)])
 sd_evolve_local = _sig("sd_evolve_local", [C.POINTER(P), C.c_int, dbl, C.c_int])
 sd_local_canonicalize = _sig("sd_local_canonicalize", [C.POINTER(P), C.c_int])
+sd_local_enable_p2p = _sig("sd_local_enable_p2p", [C.POINTER(P), C.c_int])
+sd_state_ipc_handles = _sig("sd_state_ipc_handles", [P, C.c_char_p])
+sd_state_attach_peers = _sig("sd_state_attach_peers", [P, C.c_char_p])
 
 
 class Route(C.Structure):
@@ -181,6 +184,7 @@ EXPORTED = [
     "sd_plan_kernel_times", "sd_comm_unique_id", "sd_state_attach_comm", "sd_state_canonicalize",
     "sd_state_create_local_shards", "sd_evolve_local", "sd_local_canonicalize", "sd_exchange_routes",
     "sd_jit_compile_preview", "sd_apply_pauli_rotation", "sd_evolve_baseline", "sd_expectation",
+    "sd_local_enable_p2p", "sd_state_ipc_handles", "sd_state_attach_peers",
 ]
 
 

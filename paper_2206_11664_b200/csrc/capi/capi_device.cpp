@@ -325,6 +325,26 @@ void harvest(sd_plan& p) {
     p.ev_used = 0;
 }
 
+// Destination table of a fused exchange store: chunk c of this rank's
+// (sigma-stored) shard goes to the current receive buffer of the rank whose
+// swapped global bits are c (exchange_routes), itself included.
+void set_exchange_destinations(sdb::StateImpl& s, const sdb::ExchangeSpec& ex) {
+    if (!s.xdst_dev) SDB_CUDA(cudaMalloc(reinterpret_cast<void**>(&s.xdst_dev), 256 * sizeof(double2*)));
+    std::vector<double2*> tab(256, nullptr);
+    for (const sdb::Route& rt : sdb::exchange_routes(s.n_local, s.n, s.rank, ex)) {
+        const auto& pb = s.peer_buf.at(static_cast<size_t>(rt.peer));
+        double* recv = s.parity == 0 ? pb.second : pb.first;
+        tab[rt.send_off / rt.count] = reinterpret_cast<double2*>(recv);
+    }
+    SDB_CUDA(cudaMemcpyAsync(s.xdst_dev, tab.data(), tab.size() * sizeof(double2*), cudaMemcpyHostToDevice, s.stream));
+}
+
+// after every rank's fused exchange pass has completed
+void finish_p2p_exchange(sdb::StateImpl& s) {
+    std::swap(s.amps, s.xbuf);
+    s.parity ^= 1;
+}
+
 // per-tile constant phases of the step's diagonal passes, once per dt
 void ensure_tile_phase(sd_plan& p, StepExec& E, double dt) {
     if (!E.tile_phase || E.phase_dt == dt) return;
@@ -348,12 +368,18 @@ void run_segment(sd_plan& p, StepExec& E, size_t seg, double dt) {
     const int first = E.seg_first[seg], count = E.seg_count[seg];
     for (int i = first; i < first + count; ++i) {
         const bool to_buf = exch && i == first + count - 1;
-        record_start(p, E.pass_class[i]);
+        // fused exchange: the pass stores straight into the peers' receive buffers
+        double2* const* xdst = nullptr;
+        if (to_buf && s.p2p) {
+            set_exchange_destinations(s, E.ss.segs[seg].ex);
+            xdst = s.xdst_dev;
+        }
+        record_start(p, xdst ? 2 : E.pass_class[i]);
         if (E.jit_fn[i]) {
             sdb::launch_tile_pass_jit(E.jit_fn[i], s, E.host_passes[i], i, E.dev, dt, rank_bits,
-                                      to_buf ? s.xbuf : nullptr, E.smem[i]);
+                                      to_buf ? s.xbuf : nullptr, E.smem[i], xdst);
         } else {
-            sdb::launch_tile_pass(s, E.host_passes[i], i, E.dev, dt, rank_bits, to_buf ? s.xbuf : nullptr);
+            sdb::launch_tile_pass(s, E.host_passes[i], i, E.dev, dt, rank_bits, to_buf ? s.xbuf : nullptr, xdst);
         }
         record_end(p, bytes);
         bump(s, s.amps_count(), s.amps_count());
@@ -367,6 +393,11 @@ void run_step_fused(sd_plan& p, double dt) {
     for (size_t seg = 0; seg < E.ss.segs.size(); ++seg) {
         run_segment(p, E, seg, dt);
         if (E.ss.segs[seg].exchange_after) {
+            if (s.p2p) {
+                sdb::nccl_barrier(s);  // every rank's fused store has landed
+                finish_p2p_exchange(s);
+                continue;
+            }
             const double xb = 2.0 * 16.0 * double(s.amps_count()) *
                               (1.0 - std::ldexp(1.0, -static_cast<int>(E.ss.segs[seg].ex.swaps.size())));
             record_start(p, 2);
@@ -538,6 +569,7 @@ void permute_local(sdb::StateImpl& s) {
     if (ident) return;
     permute_into_xbuf(s, new_pos);
     std::swap(s.amps, s.xbuf);
+    s.parity ^= 1;
     for (int q = 0; q < s.n_local; ++q) s.phys_of[q] = q;
 }
 
@@ -608,6 +640,8 @@ void sd_state_destroy(sd_state* h) {
         sdb::nccl_detach(s);
     } catch (...) {
     }
+    for (void* ptr : s.ipc_opened) cudaIpcCloseMemHandle(ptr);
+    if (s.xdst_dev) cudaFree(s.xdst_dev);
     if (s.amps) cudaFree(s.amps);
     if (s.xbuf) cudaFree(s.xbuf);
     if (s.reduce_buf) cudaFree(s.reduce_buf);
@@ -1087,7 +1121,17 @@ sd_status sd_evolve_local(sd_plan* const* plans, int world, double dt, int n_ste
                     SDB_CUDA(cudaSetDevice(shards[r]->device));
                     run_segment(*plans[r], *E[r], seg, dt);
                 }
-                if (E[0]->ss.segs[seg].exchange_after) sdb::exchange_local(shards, E[0]->ss.segs[seg].ex);
+                if (E[0]->ss.segs[seg].exchange_after) {
+                    if (shards[0]->p2p) {
+                        for (sdb::StateImpl* sh : shards) {
+                            SDB_CUDA(cudaSetDevice(sh->device));
+                            SDB_CUDA(cudaStreamSynchronize(sh->stream));
+                        }
+                        for (sdb::StateImpl* sh : shards) finish_p2p_exchange(*sh);
+                    } else {
+                        sdb::exchange_local(shards, E[0]->ss.segs[seg].ex);
+                    }
+                }
             }
             for (int r = 0; r < world; ++r) shards[r]->phys_of = E[r]->ss.phys_out;
         }
@@ -1226,6 +1270,92 @@ sd_status sd_expectation(sd_state* h, const uint64_t* x, const uint64_t* z, cons
         }
         *re = tr;
         if (imag_residue) *imag_residue = std::abs(ti);
+    });
+}
+
+namespace {
+void ensure_xbuf(sdb::StateImpl& s) {
+    if (s.xbuf) return;
+    SDB_CUDA(cudaSetDevice(s.device));
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&s.xbuf), 16 * s.amps_count());
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw sdb::OomError("cannot allocate the exchange buffer");
+    }
+    s.xbuf_amps = s.amps_count();
+}
+}  // namespace
+
+sd_status sd_local_enable_p2p(sd_state* const* hs, int world) {
+    return guard([&] {
+        require(hs != nullptr && world >= 1, "null shard array");
+        std::vector<sdb::StateImpl*> shards(world);
+        for (int r = 0; r < world; ++r) {
+            shards[r] = &st(hs[r]);
+            require(shards[r]->rank == r && shards[r]->world == world, "shards[r] must be rank r of `world`");
+            ensure_xbuf(*shards[r]);
+        }
+        for (sdb::StateImpl* a : shards) {
+            SDB_CUDA(cudaSetDevice(a->device));
+            for (sdb::StateImpl* b : shards) {
+                if (b->device == a->device) continue;
+                int ok = 0;
+                SDB_CUDA(cudaDeviceCanAccessPeer(&ok, a->device, b->device));
+                if (!ok) throw std::runtime_error("devices cannot access each other's memory");
+                const cudaError_t e = cudaDeviceEnablePeerAccess(b->device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) SDB_CUDA(e);
+                cudaGetLastError();
+            }
+        }
+        for (sdb::StateImpl* a : shards) {
+            a->peer_buf.clear();
+            for (sdb::StateImpl* b : shards) a->peer_buf.emplace_back(b->amps, b->xbuf);
+            a->parity = 0;
+            a->p2p = true;
+        }
+    });
+}
+
+sd_status sd_state_ipc_handles(sd_state* h, unsigned char out[128]) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require(out != nullptr, "null output");
+        ensure_xbuf(s);
+        SDB_CUDA(cudaSetDevice(s.device));
+        cudaIpcMemHandle_t a, b;
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+        SDB_CUDA(cudaIpcGetMemHandle(&a, s.amps));
+        SDB_CUDA(cudaIpcGetMemHandle(&b, s.xbuf));
+        std::memcpy(out, &a, 64);
+        std::memcpy(out + 64, &b, 64);
+    });
+}
+
+sd_status sd_state_attach_peers(sd_state* h, const unsigned char* handles) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require(handles != nullptr, "null handles");
+        require(s.nccl != nullptr, "attach the NCCL communicator first (sd_state_attach_comm)");
+        ensure_xbuf(s);
+        SDB_CUDA(cudaSetDevice(s.device));
+        s.peer_buf.assign(static_cast<size_t>(s.world), {nullptr, nullptr});
+        for (int r = 0; r < s.world; ++r) {
+            if (r == s.rank) {
+                s.peer_buf[r] = {s.amps, s.xbuf};
+                continue;
+            }
+            void* p[2] = {nullptr, nullptr};
+            for (int k = 0; k < 2; ++k) {
+                cudaIpcMemHandle_t hd;
+                std::memcpy(&hd, handles + 128 * r + 64 * k, 64);
+                SDB_CUDA(cudaIpcOpenMemHandle(&p[k], hd, cudaIpcMemLazyEnablePeerAccess));
+                s.ipc_opened.push_back(p[k]);
+            }
+            s.peer_buf[r] = {static_cast<double*>(p[0]), static_cast<double*>(p[1])};
+        }
+        s.parity = 0;
+        s.p2p = true;
+        sdb::nccl_barrier(s);
     });
 }
 

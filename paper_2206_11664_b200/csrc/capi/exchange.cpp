@@ -135,6 +135,13 @@ void nccl_detach(StateImpl& s) {
     }
 }
 
+void nccl_barrier(StateImpl& s) {
+    if (!s.nccl) throw std::runtime_error("sharded state has no communicator (sd_state_attach_comm)");
+    nccl_check(nccl().allReduce(s.reduce_buf, s.reduce_buf, 1, ncclDouble, ncclSum, static_cast<ncclComm_t>(s.nccl),
+                                s.stream),
+               "ncclAllReduce");
+}
+
 double nccl_sum(StateImpl& s, double v) {
     if (!s.nccl) throw std::runtime_error("sharded state has no communicator (sd_state_attach_comm)");
     double* d = s.reduce_buf;

@@ -11,6 +11,8 @@ namespace sdb {
 void nccl_unique_id(unsigned char out[128]);
 void nccl_attach(StateImpl& s, const unsigned char id[128]);
 void nccl_detach(StateImpl& s);
+// stream-ordered barrier over the communicator (a 1-element all-reduce)
+void nccl_barrier(StateImpl& s);
 // sum of v over all ranks of the state's communicator
 double nccl_sum(StateImpl& s, double v);
 // Chunk routing of one exchange for `rank` (offsets and counts in amplitudes):

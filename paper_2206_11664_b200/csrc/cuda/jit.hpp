@@ -16,7 +16,7 @@ bool jit_wanted(int n_local);
 // parallel, cached in-process and on disk).
 std::vector<void*> jit_pass_kernels(const HostPlanArrays& A, int device);
 void launch_tile_pass_jit(void* fn, StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& plan, double dt,
-                          uint64_t rank_bits, double* out, size_t smem);
+                          uint64_t rank_bits, double* out, size_t smem, double2* const* xdst = nullptr);
 // Host-only: generate and NVRTC-compile every distinct pass program of A
 // (no device needed); returns the number of distinct programs.
 size_t jit_compile_only(const HostPlanArrays& A);

@@ -303,6 +303,7 @@ struct PassCtx {
     const PlanDev& plan;
     const double2* __restrict__ psi;
     double2* __restrict__ out;
+    double2* const* xdst;  // fused exchange destinations per chunk (nullptr: local store)
     double neg_dt;
     uint64_t rank_bits, n_tiles, stride;
     uint64_t t_first, t_last;  // this CTA's tiles: strided (t_first += grid) or a contiguous block
@@ -326,10 +327,11 @@ struct PassCtx {
     RegCfg rc;
 
     __device__ __forceinline__ PassCtx(const PassDev& P_, const PlanDev& plan_, const double2* psi_, double2* out_,
-                                       double neg_dt_, uint64_t rank_bits_, uint64_t n_tiles_, unsigned char* smem_raw,
+                                       double2* const* xdst_, double neg_dt_, uint64_t rank_bits_, uint64_t n_tiles_,
+                                       unsigned char* smem_raw,
                                        uint64_t* off_lo_, uint64_t* off_hi_, uint64_t* s_tbase_, uint32_t* s_pl_,
                                        uint32_t* s_ph_)
-        : P(P_), plan(plan_), psi(psi_), out(out_), neg_dt(neg_dt_), rank_bits(rank_bits_), n_tiles(n_tiles_),
+        : P(P_), plan(plan_), psi(psi_), out(out_), xdst(xdst_), neg_dt(neg_dt_), rank_bits(rank_bits_), n_tiles(n_tiles_),
           off_lo(off_lo_), off_hi(off_hi_), s_tbase(s_tbase_), s_pl(s_pl_), s_ph(s_ph_) {
         tid = threadIdx.x;
         if (P.blocked) {
@@ -734,7 +736,24 @@ struct PassCtx {
             go = out + base;
             phys_offsets(o);
         }
-        if (op.mask & 2u) {
+        const bool sc = (op.mask & 2u) != 0;
+        if (xdst && P.x_bits > 0) {
+            // fused exchange: every amplitude goes straight to its receiving
+            // rank's buffer (peer memory over NVLink), at its final position
+            const uint64_t sb = static_cast<uint64_t>(go - out);
+            uint64_t own = 0;
+            for (int i = 0; i < P.x_bits; ++i) own |= ((rank_bits >> P.x_gpos[i]) & 1ull) << i;
+            const uint64_t low = (1ull << P.x_t0) - 1ull;
+            const uint64_t ownsh = own << P.x_t0;
+#pragma unroll
+            for (int s = 0; s < NR; ++s) {
+                const uint64_t y = sb | o[s];
+                double2* const d = xdst[y >> P.x_t0] + ((y & low) | ownsh);
+                __stcs(d, sc ? make_double2(v[s].x * scale, v[s].y * scale) : v[s]);
+            }
+            return;
+        }
+        if (sc) {
 #pragma unroll
             for (int s = 0; s < NR; ++s) __stcs(go + o[s], make_double2(v[s].x * scale, v[s].y * scale));
         } else {
@@ -753,7 +772,7 @@ struct PassCtx {
     __shared__ uint64_t sdb_off_hi[1 << Ctx::HI];                                                          \
     __shared__ uint64_t sdb_tbase[::sdb::dev::kTbaseChunks * 128];                                         \
     __shared__ uint32_t sdb_pl[3 * 64], sdb_ph[3 * 64];                                                    \
-    Ctx ctx(plan.passes[pass_index], plan, psi, out, neg_dt, rank_bits, n_tiles, smem_raw, sdb_off_lo,     \
+    Ctx ctx(plan.passes[pass_index], plan, psi, out, xdst, neg_dt, rank_bits, n_tiles, smem_raw, sdb_off_lo, \
             sdb_off_hi, sdb_tbase, sdb_pl, sdb_ph);                                                        \
     ctx.setup();                                                                                           \
     for (uint64_t t = ctx.t_first; t < ctx.t_last; t += ctx.stride) {                                      \

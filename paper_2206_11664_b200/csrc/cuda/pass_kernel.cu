@@ -46,8 +46,8 @@ __global__ void k_tile_phase(PlanDev plan, int pass_index, double neg_dt, uint64
 
 template <int K, int RB>
 __global__ void __launch_bounds__(Cfg<K, RB>::NT, Cfg<K, RB>::MINB)
-k_tile_pass(const double2* __restrict__ psi, double2* __restrict__ out, PlanDev plan, int pass_index, double neg_dt,
-            uint64_t rank_bits, uint64_t n_tiles) {
+k_tile_pass(const double2* __restrict__ psi, double2* __restrict__ out, double2* const* xdst, PlanDev plan,
+            int pass_index, double neg_dt, uint64_t rank_bits, uint64_t n_tiles) {
     const Interpreter prog;
     SDB_PASS_KERNEL_BODY(K, RB, prog)
 }
@@ -61,7 +61,7 @@ size_t smem_bytes(const PassDev& ph) {
 
 template <int K, int RB>
 void launch_kr(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& plan, double dt, uint64_t rank_bits,
-               double* out) {
+               double* out, double2* const* xdst) {
     using C = Cfg<K, RB>;
     const size_t smem = smem_bytes<K, RB>(ph);
     static size_t configured = 0;
@@ -78,19 +78,19 @@ void launch_kr(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& p
     uint64_t grid = static_cast<uint64_t>(s.sm_count) * static_cast<uint64_t>(occ);
     if (grid > n_tiles) grid = n_tiles;
     k_tile_pass<K, RB><<<static_cast<unsigned>(grid), C::NT, smem, s.stream>>>(
-        reinterpret_cast<const double2*>(s.amps), reinterpret_cast<double2*>(out ? out : s.amps), plan, pass_index,
-        -dt, rank_bits, n_tiles);
+        reinterpret_cast<const double2*>(s.amps), reinterpret_cast<double2*>(out ? out : s.amps), xdst, plan,
+        pass_index, -dt, rank_bits, n_tiles);
     SDB_CUDA(cudaGetLastError());
 }
 
 template <int K>
 void launch_k(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& plan, double dt, uint64_t rank_bits,
-              double* out) {
+              double* out, double2* const* xdst) {
     // R = 4 register coordinates (16 amplitudes per thread). R = 3 with twice the
     // threads spills at the 2-CTA/SM register budget and measured 1.5x slower
     // per step (profiles/r1_notes.md).
     if (ph.rbits != 4 && K >= 4) throw std::invalid_argument("tile pass: unsupported register config");
-    launch_kr<K, 4>(s, ph, pass_index, plan, dt, rank_bits, out);
+    launch_kr<K, 4>(s, ph, pass_index, plan, dt, rank_bits, out, xdst);
 }
 
 }  // namespace
@@ -119,11 +119,11 @@ size_t tile_pass_smem(const PassDev& ph) {
 }
 
 void launch_tile_pass(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& plan, double dt,
-                      uint64_t rank_bits, double* out) {
+                      uint64_t rank_bits, double* out, double2* const* xdst) {
     if (ph.n_outer > 7 * kTbaseChunks) throw std::invalid_argument("tile pass: too many outer bits");
     switch (ph.k) {
 #define SDB_K(KK) \
-    case KK: launch_k<KK>(s, ph, pass_index, plan, dt, rank_bits, out); break;
+    case KK: launch_k<KK>(s, ph, pass_index, plan, dt, rank_bits, out, xdst); break;
         SDB_K(1) SDB_K(2) SDB_K(3) SDB_K(4) SDB_K(5) SDB_K(6) SDB_K(7) SDB_K(8) SDB_K(9) SDB_K(10)
         SDB_K(11) SDB_K(12)
 #undef SDB_K

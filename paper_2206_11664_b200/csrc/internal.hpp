@@ -47,6 +47,15 @@ struct StateImpl {
     void* nccl = nullptr;    // ncclComm_t when attached
     double* xbuf = nullptr;  // exchange receive buffer (lazily allocated)
     uint64_t xbuf_amps = 0;
+    // Fused exchange over peer memory (sd_state_attach_peers /
+    // sd_local_enable_p2p): peer_buf[r] = rank r's two state buffers as they
+    // were when peers were attached; amps/xbuf swap roles at every exchange and
+    // `parity` tracks which of the two is a rank's current receive buffer.
+    bool p2p = false;
+    int parity = 0;
+    std::vector<std::pair<double*, double*>> peer_buf;
+    std::vector<void*> ipc_opened;       // peer mappings to close on destroy
+    double2** xdst_dev = nullptr;        // device table: destination per chunk
     double* reduce_buf = nullptr;
     int sm_count = 0;
     uint64_t amps_count() const { return uint64_t(1) << n_local; }
@@ -73,9 +82,10 @@ void launch_pauli_rotation(StateImpl& s, uint64_t x, uint64_t z, double coeff, d
 void device_expectation_term(StateImpl& s, uint64_t x, uint64_t z, double* re, double* im);
 
 // Fused pass launcher (pass_kernel.cu).
-// out: destination buffer (nullptr = in place on s.amps).
+// out: destination buffer (nullptr = in place on s.amps); xdst: device table of
+// per-chunk destination buffers for a fused exchange store (nullptr: none).
 void launch_tile_pass(StateImpl& s, const PassDev& pass_host, int pass_index, const PlanDev& plan,
-                      double dt, uint64_t rank_bits, double* out);
+                      double dt, uint64_t rank_bits, double* out, double2* const* xdst = nullptr);
 int max_tile_qubits();
 // per-tile constant phases of a pass's table point (PassDev::tphase_off)
 void launch_tile_phase(StateImpl& s, const PassDev& pass_host, int pass_index, const PlanDev& plan, double dt,

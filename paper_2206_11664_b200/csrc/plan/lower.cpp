@@ -506,6 +506,11 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
         MicroOpDev so{};
         so.kind = kOpStore;
         so.perm = -1;
+        if (!pp.xswaps.empty()) {
+            pd.x_bits = static_cast<int>(pp.xswaps.size());
+            pd.x_t0 = n_local - pd.x_bits;
+            for (int i = 0; i < pd.x_bits && i < 8; ++i) pd.x_gpos[i] = pp.xswaps[i].first;
+        }
         if (!pp.store_sigma.empty()) {
             pd.store_perm = 1;
             for (int j = 0; j < K; ++j) pd.st_lpos[j] = pp.store_sigma[pp.lpos[j]];

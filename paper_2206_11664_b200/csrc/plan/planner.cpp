@@ -539,6 +539,7 @@ ShardedStep plan_sharded_step(const std::vector<Op>& ops, const std::vector<Grou
                 sg.plan.passes.push_back(std::move(pp));
             }
             sg.plan.passes.back().store_sigma = sg.ex.sigma;
+            sg.plan.passes.back().xswaps = sg.ex.swaps;
         }
         for (PassPlan& pp : sg.plan.passes) all.push_back(&pp);
         out.n_exchanges += sg.exchange_after ? 1 : 0;

@@ -69,6 +69,7 @@ struct PassPlan {
     int scale_exp = 0;          // store scale = 2^-scale_exp
     std::vector<int> op_ids;    // ops scheduled here (debug)
     std::vector<int> store_sigma;  // non-empty: store out of place through this local bit permutation
+    std::vector<std::pair<int, int>> xswaps;  // the exchange that follows (global bit, top local bit)
 };
 
 struct StepPlan {

@@ -153,6 +153,14 @@ struct PassDev {
     int store_perm;      // 1: store out of place through a local bit permutation sigma
     int st_lpos[16];     // sigma(lpos[j])
     int st_opos[64];     // sigma(opos[j])
+    // Fused qubit-remap exchange (store_perm passes in front of an exchange):
+    // with a destination table (kernel argument xdst) the store writes each
+    // amplitude straight into the receiving rank's buffer over peer memory:
+    // chunk c = sigma-index >> x_t0 goes to xdst[c] at its low bits | own << x_t0,
+    // own = this rank's bits at the swapped global positions x_gpos.
+    int x_bits;          // swapped bits g' (0: no exchange follows)
+    int x_t0;            // n_local - g'
+    int x_gpos[8];       // global (physical) bit of swap i
 };
 constexpr int kPassNeedsTable = 1;
 

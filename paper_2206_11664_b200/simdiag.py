@@ -395,6 +395,18 @@ class StateVector:
         every rank passes the same 128-byte id from comm_unique_id()."""
         check(A.sd_state_attach_comm(self._s, C.create_string_buffer(bytes(unique_id), 128)))
 
+    def ipc_handles(self) -> bytes:
+        """This shard's two cudaIpcMemHandles (state, receive buffer), 128 bytes."""
+        buf = C.create_string_buffer(128)
+        check(A.sd_state_ipc_handles(self._s, buf))
+        return buf.raw
+
+    def attach_peers(self, all_handles: Sequence[bytes]) -> None:
+        """Fused exchange over peer memory: every rank's ipc_handles(), in rank
+        order (sd_state_attach_peers; needs attach_comm first)."""
+        blob = b"".join(bytes(h) for h in all_handles)
+        check(A.sd_state_attach_peers(self._s, C.create_string_buffer(blob, len(blob))))
+
     def canonicalize(self) -> None:
         """Undo qubit relabelling (collective for NCCL-attached shards)."""
         check(A.sd_state_canonicalize(self._s))
@@ -617,6 +629,12 @@ class LocalShards:
     def set_basis(self, index: int) -> None:
         for s in self.shards:
             s.set_basis(index)
+
+    def enable_p2p(self) -> None:
+        """Fused exchanges: each remap's last pass stores straight into the
+        receiving shard's buffer (sd_local_enable_p2p)."""
+        arr = (C.c_void_p * self.world)(*[s._s.value for s in self.shards])
+        check(A.sd_local_enable_p2p(arr, self.world))
 
     def plan(self, groups: Sequence[DiagonalGroup], order: int = 1, tile_qubits: int = 0) -> None:
         self.plans = [TrotterPlan(s, groups, order=order, tile_qubits=tile_qubits) for s in self.shards]

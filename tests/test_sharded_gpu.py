@@ -26,14 +26,17 @@ def initial(port, cfg, n):
     return a
 
 
+@pytest.mark.parametrize("fused", [False, True], ids=["copy-exchange", "fused-p2p"])
 @pytest.mark.parametrize("cfg,n,world,k", [(1, 12, 2, 8), (2, 12, 4, 8), (3, 12, 2, 9), (4, 13, 2, 9),
                                            (4, 13, 8, 8), (4, 15, 4, 12), (5, 12, 4, 8), (5, 13, 8, 9)])
-def test_local_shards_match_reference(cfg, n, world, k, sd, ref, port):
+def test_local_shards_match_reference(cfg, n, world, k, fused, sd, ref, port):
     text = M.config_text(cfg, n=n)
     groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
     order, dt, steps = M.CONFIGS[cfg]["order"], M.CONFIGS[cfg]["dt"] * 5, 3
     psi0 = initial(port, cfg, n)
     sh = sd.LocalShards(n, world)
+    if fused:
+        sh.enable_p2p()
     sh.upload(psi0)
     sh.plan(groups, order=order, tile_qubits=k)
     sh.evolve(dt, steps)

@@ -316,6 +316,7 @@ struct PassCtx {
     const uint32_t* s_cfg;
     const uint32_t* s_qt;
     uint64_t *st_lo, *st_hi, *st_tbase;
+    uint32_t* qt_smem;  // QT bit tables staged in shared memory
     uint64_t *off_lo, *off_hi, *s_tbase;  // s_tbase: [kTbaseChunks][128]
     uint32_t *s_pl, *s_ph;                // [3][64]
     // per tile
@@ -357,12 +358,13 @@ struct PassCtx {
         // length); per-thread config bases and QT tables are read through L1.
         s_ops = reinterpret_cast<MicroOpDev*>(tab + P.tab_words);
         s_cfg = plan.cfg_tb + P.cfg_off;
-        s_qt = reinterpret_cast<const uint32_t*>(plan.qt_words + P.qt_off);
+        s_qt = reinterpret_cast<const uint32_t*>(plan.qt_words + P.qt_off);  // staged into smem in setup()
         // store-side index tables (only for passes that store through a local
         // bit permutation sigma, i.e. in front of a qubit-remap exchange)
         st_lo = reinterpret_cast<uint64_t*>(s_ops + P.n_ops);
         st_hi = st_lo + (1 << LO);
         st_tbase = st_hi + (1 << HI);
+        qt_smem = reinterpret_cast<uint32_t*>(st_lo + (P.store_perm ? (1 << LO) + (1 << HI) + kTbaseChunks * 128 : 0));
     }
 
     // ---- stage the program and the index tables (once per launch)
@@ -374,6 +376,8 @@ struct PassCtx {
             const int words = P.n_ops * static_cast<int>(sizeof(MicroOpDev) / sizeof(int4));
             for (int i = tid; i < words; i += NT) dst[i] = __ldg(src + i);
         }
+        for (int i = tid; i < 2 * P.n_qt_words; i += NT) qt_smem[i] = __ldg(s_qt + i);
+        s_qt = qt_smem;
         for (int i = tid; i < (1 << LO); i += NT) {
             uint64_t o = 0;
             for (int j = 0; j < LO; ++j)
@@ -563,6 +567,13 @@ struct PassCtx {
         uint32_t tc[4];      // full table: swizzled compact offsets of the register coordinates
         uint32_t fo[3][4];   // factor tables: swizzled compact offsets per factor
         int coffE[3];        // factor tables: double offsets in the table region
+        // S/CZ quadratic form of the tile (literals in specialised kernels;
+        // n_lo < 0: read PointDev's pair lists at run time)
+        int n_lo, n_oo;
+        uint32_t lo[16];     // (coord << 8) | outer physical bit
+        uint64_t oo[8];      // outer-outer pair masks
+        uint32_t s1L, s2L;
+        uint64_t s1H, s2H;
     };
     __device__ __forceinline__ PointCfg point_cfg(const MicroOpDev& op, const PointDev& pt) const {
         PointCfg c;
@@ -577,6 +588,12 @@ struct PassCtx {
 #pragma unroll
             for (int j = 0; j < 4; ++j) c.fo[f][j] = static_cast<uint32_t>(op.c_off[f] >> (16 * j)) & 0xffffu;
         }
+        c.n_lo = -1;
+        c.n_oo = 0;
+        c.s1L = pt.s1L;
+        c.s2L = pt.s2L;
+        c.s1H = pt.s1H;
+        c.s2H = pt.s2H;
         return c;
     }
 
@@ -590,25 +607,34 @@ struct PassCtx {
         for (int j = 0; j < 4; ++j) cb[j] = 1u << ((rc.cidx >> (8 * j)) & 255u);
         // ---- quarter turns: q(tb ^ r_s) = q0 + sum_{j in s} dq_j + 2 QT(r_s)  (mod 4)
         // (QT is a quadratic form: QT(a^b) = QT(a) + QT(b) + B(a,b), B bilinear)
-        uint32_t m2 = pt.s2L;
-        unsigned q0 = __popcll(full & pt.s1H) + 2u * __popcll(full & pt.s2H);
-        for (int j = 0; j < pt.n_lo; ++j) {
-            const uint32_t wl = __ldg(plan.lo_pairs + pt.lo_off + j);
-            if ((full >> (wl & 0xffu)) & 1ull) m2 ^= 1u << (wl >> 8);
-        }
-        for (int j = 0; j < pt.n_oo; ++j) {
-            const uint64_t m = __ldg(plan.oo_pairs + pt.oo_off + j);
-            if ((full & m) == m) q0 += 2u;
+        uint32_t m2 = pc.s2L;
+        unsigned q0 = __popcll(full & pc.s1H) + 2u * __popcll(full & pc.s2H);
+        if (pc.n_lo >= 0) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (j < pc.n_lo && ((full >> (pc.lo[j] & 0xffu)) & 1ull)) m2 ^= 1u << (pc.lo[j] >> 8);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j < pc.n_oo && (full & pc.oo[j]) == pc.oo[j]) q0 += 2u;
+        } else {
+            for (int j = 0; j < pt.n_lo; ++j) {
+                const uint32_t wl = __ldg(plan.lo_pairs + pt.lo_off + j);
+                if ((full >> (wl & 0xffu)) & 1ull) m2 ^= 1u << (wl >> 8);
+            }
+            for (int j = 0; j < pt.n_oo; ++j) {
+                const uint64_t m = __ldg(plan.oo_pairs + pt.oo_off + j);
+                if ((full & m) == m) q0 += 2u;
+            }
         }
         const uint32_t* qt = pt.qt_word >= 0 ? s_qt + 2 * pt.qt_word : nullptr;
-        auto qtb = [&](uint32_t l) -> unsigned { return qt ? (__ldg(qt + (l >> 5)) >> (l & 31u)) & 1u : 0u; };
+        auto qtb = [&](uint32_t l) -> unsigned { return qt ? (qt[l >> 5] >> (l & 31u)) & 1u : 0u; };
         const unsigned qt_tb = qtb(rc.tb);
-        q0 += __popc(rc.tb & pt.s1L) + 2u * (__popc(rc.tb & m2) + qt_tb);
+        q0 += __popc(rc.tb & pc.s1L) + 2u * (__popc(rc.tb & m2) + qt_tb);
         unsigned dq[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const unsigned bil = qt ? (qtb(rc.tb ^ cb[j]) ^ qt_tb ^ qtb(cb[j])) : 0u;
-            dq[j] = __popc(cb[j] & pt.s1L) + 2u * (__popc(cb[j] & m2) + bil);
+            dq[j] = __popc(cb[j] & pc.s1L) + 2u * (__popc(cb[j] & m2) + bil);
         }
         // ---- table slots of this thread's registers (compact index, swizzle linear)
         uint32_t ts0 = 0, fb[3] = {0, 0, 0};

@@ -56,6 +56,7 @@ template <int K, int RB>
 size_t smem_bytes(const PassDev& ph) {
     using C = Cfg<K, RB>;
     return sizeof(double2) * C::N + sizeof(double) * ph.tab_words + sizeof(MicroOpDev) * ph.n_ops +
+           sizeof(uint64_t) * ph.n_qt_words +
            (ph.store_perm ? sizeof(uint64_t) * ((1 << C::LO) + (1 << C::HI) + kTbaseChunks * 128) : 0);
 }
 

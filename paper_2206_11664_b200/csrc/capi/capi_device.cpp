@@ -256,7 +256,7 @@ StepExec& step_for(sd_plan& p, const std::vector<int>& layout) {
     if (it != p.steps.end()) return *it->second;
     sdb::StateImpl& s = p.state->impl;
     auto E = std::make_unique<StepExec>();
-    E->ss = sdb::plan_sharded_step(p.ops, p.groups, s.n_local, p.k, 3, layout);
+    E->ss = sdb::plan_sharded_step(p.ops, p.groups, s.n_local, p.k, sdb::fixed_bits_for(p.k), layout);
     sdb::StepPlan combined;
     combined.tile_qubits = p.k;
     for (const sdb::Segment& sg : E->ss.segs) {
@@ -995,7 +995,7 @@ sd_status sd_plan_preview(int n, int world, const sd_group_desc* groups, size_t 
                 break;
             }
             seen.push_back(phys);
-            steps.push_back(sdb::plan_sharded_step(ops, gs, n_local, k, 3, phys));
+            steps.push_back(sdb::plan_sharded_step(ops, gs, n_local, k, sdb::fixed_bits_for(k), phys));
             phys = steps.back().phys_out;
         }
         if (info) {
@@ -1198,7 +1198,7 @@ sd_status sd_jit_compile_preview(int n, int world, const sd_group_desc* groups, 
         int k = o.tile_qubits > 0 ? o.tile_qubits : 12;
         k = std::min({k, sdb::max_tile_qubits(), n_local});
         const auto ops = sdb::step_ops(gs, n, o.order, std::max(1, k - 3));
-        const sdb::ShardedStep ss = sdb::plan_sharded_step(ops, gs, n_local, k, 3, phys);
+        const sdb::ShardedStep ss = sdb::plan_sharded_step(ops, gs, n_local, k, sdb::fixed_bits_for(k), phys);
         sdb::StepPlan combined;
         combined.tile_qubits = k;
         for (const sdb::Segment& sg : ss.segs)

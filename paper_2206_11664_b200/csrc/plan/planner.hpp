@@ -14,6 +14,10 @@ namespace sdb {
 // a pass's program staged in shared memory stays <= ~13 KiB.
 constexpr int kMaxOpsPerPass = 96;
 
+// Physical bits kept local in every pass (0..2: 8 lanes x 16 B = one 128-byte
+// line); tiles of <= 3 qubits keep at least one free coordinate.
+inline int fixed_bits_for(int k) { return k - 1 < 3 ? (k - 1 > 0 ? k - 1 : 0) : 3; }
+
 // One group as the planner sees it (a flattened DiagonalGroup).
 struct GroupSpec {
     std::vector<int> h_pre, s_layer, h_post;

@@ -1,0 +1,76 @@
+"""Edge cases of the fused device path against the reference compiled from
+its sources: the smallest registers (n = 1..4, tile wider than the state),
+identity and constant terms, single-term and diagonal-only groups, terms on
+the top qubit, duplicate terms merged by from_terms, an empty Hamiltonian,
+order-2 steps, and n_steps = 0."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rand_state(n, seed):
+    rng = np.random.default_rng(seed)
+    a = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    return a / np.linalg.norm(a)
+
+
+def run_both(sd, ref, text, n, dt=0.11, steps=3, order=1, k=0):
+    psi0 = rand_state(n, n + steps)
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
+    s = sd.StateVector(n)
+    s.upload(psi0)
+    sd.TrotterPlan(s, groups, order=order, tile_qubits=k).evolve(dt, steps)
+    got = s.amplitudes()
+    h, _, _ = ref.partition_text(text)
+    want, _ = ref.evolve_grouped(h, psi0, n, dt, steps, order)
+    ref.free(h)
+    return got, want
+
+
+@pytest.mark.parametrize("text,n", [
+    ("0.7 X\n-0.3 Z\n0.2 Y\n", 1),
+    ("1.0 XX\n0.5 YY\n-0.25 ZZ\n0.4 ZI\n", 2),
+    ("0.9 XYZ\n-0.4 ZZZ\n0.3 IXI\n0.8 YIY\n", 3),
+    ("1.0 XZYX\n1.0 ZXXY\n-0.5 IIIZ\n0.3 YYYY\n0.2 ZIZI\n", 4),
+])
+@pytest.mark.parametrize("order", [1, 2])
+def test_tiny_registers(text, n, order, sd, ref):
+    got, want = run_both(sd, ref, text, n, order=order)
+    assert np.max(np.abs(got - want)) < 1e-12
+    assert abs(np.linalg.norm(got) - 1) < 1e-12
+
+
+def test_identity_and_duplicate_terms(sd, ref):
+    # identity term (global phase), duplicates merged in first-seen order, a
+    # term cancelling to zero (dropped), a term on the top qubit
+    text = "0.5 IIIIIIII\n0.3 XXIIIIII\n0.2 XXIIIIII\n0.4 ZIIIIIIZ\n-0.4 ZIIIIIIZ\n0.6 IIIIIIIY\n0.1 YZIIIIIX\n"
+    got, want = run_both(sd, ref, text, 8)
+    assert np.max(np.abs(got - want)) < 1e-12
+
+
+def test_diagonal_only_and_single_term_groups(sd, ref):
+    text = "0.3 ZZIIIIIIII\n-0.7 IZZIIIIIII\n0.2 IIIIIIIIIZ\n0.9 XIIIIIIIIX\n"
+    got, want = run_both(sd, ref, text, 10, k=6)
+    assert np.max(np.abs(got - want)) < 1e-12
+
+
+def test_every_tile_width(sd, ref):
+    text = "0.4 XZYIXZ\n0.3 ZZZZZZ\n-0.2 YIYIYI\n0.5 IXIXIX\n0.1 XXXXXX\n"
+    outs = []
+    for k in range(1, 7):
+        got, want = run_both(sd, ref, text, 6, k=k)
+        assert np.max(np.abs(got - want)) < 1e-12, k
+        outs.append(got)
+
+
+def test_empty_hamiltonian_and_zero_steps(sd):
+    n = 5
+    psi0 = rand_state(n, 1)
+    s = sd.StateVector(n)
+    s.upload(psi0)
+    sd.TrotterPlan(s, [], order=1).evolve(0.1, 4)
+    assert np.max(np.abs(s.amplitudes() - psi0)) == 0.0
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load("1.0 XIIII\n"))
+    sd.TrotterPlan(s, groups).evolve(0.1, 0)
+    assert np.max(np.abs(s.amplitudes() - psi0)) == 0.0

@@ -64,6 +64,14 @@ struct sd_plan {
 
 namespace {
 
+// Largest CNOT run (same control) kept as one op; same-control CNOTs commute,
+// so a run can be cut anywhere. SDB_CX_SPLIT overrides (experiments).
+int cx_split(int k) {
+    if (const char* e = std::getenv("SDB_CX_SPLIT")) return std::max(1, std::atoi(e));
+    (void)k;
+    return 1;  // single CNOTs schedule best (config 5: 3471 -> 2003 passes/step)
+}
+
 using sdb::guard;
 using sdb::require;
 
@@ -287,7 +295,7 @@ void plan_build(sd_plan& p) {
     if (!p.opts.fuse) return;
     int k = p.opts.tile_qubits > 0 ? p.opts.tile_qubits : 12;
     p.k = std::min({k, sdb::max_tile_qubits(), s.n_local});
-    p.ops = sdb::step_ops(p.groups, s.n, order, std::max(1, p.k - 3));
+    p.ops = sdb::step_ops(p.groups, s.n, order, cx_split(p.k));
     std::vector<int> ident(s.n);
     std::iota(ident.begin(), ident.end(), 0);
     p.first = &step_for(p, ident);
@@ -983,7 +991,7 @@ sd_status sd_plan_preview(int n, int world, const sd_group_desc* groups, size_t 
         std::iota(phys.begin(), phys.end(), 0);
         int k = o.tile_qubits > 0 ? o.tile_qubits : 12;
         k = std::min({k, sdb::max_tile_qubits(), n_local});
-        const auto ops = sdb::step_ops(gs, n, o.order, std::max(1, k - 3));
+        const auto ops = sdb::step_ops(gs, n, o.order, cx_split(k));
         // steps until the layout repeats (the executor caches one plan per layout)
         std::vector<sdb::ShardedStep> steps;
         std::vector<std::vector<int>> seen;
@@ -1197,7 +1205,7 @@ sd_status sd_jit_compile_preview(int n, int world, const sd_group_desc* groups, 
         std::iota(phys.begin(), phys.end(), 0);
         int k = o.tile_qubits > 0 ? o.tile_qubits : 12;
         k = std::min({k, sdb::max_tile_qubits(), n_local});
-        const auto ops = sdb::step_ops(gs, n, o.order, std::max(1, k - 3));
+        const auto ops = sdb::step_ops(gs, n, o.order, cx_split(k));
         const sdb::ShardedStep ss = sdb::plan_sharded_step(ops, gs, n_local, k, sdb::fixed_bits_for(k), phys);
         sdb::StepPlan combined;
         combined.tile_qubits = k;

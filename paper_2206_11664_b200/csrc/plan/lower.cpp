@@ -39,8 +39,14 @@ struct Affine {
         identity = false;
     }
     void compose_outer(int phys, uint32_t T) {
-        outer.emplace_back(phys, T);
         identity = false;
+        for (auto& o : outer) {
+            if (o.first == phys) {  // flips of one control bit add up (the map is affine)
+                o.second ^= T;
+                return;
+            }
+        }
+        outer.emplace_back(phys, T);
     }
 };
 
@@ -262,7 +268,7 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                     pm.lo[x] = static_cast<uint16_t>(host_swz(lo));
                     pm.hi[x] = static_cast<uint16_t>(host_swz(hi));
                 }
-                if (P.outer.size() > 16) throw std::logic_error("lower_plan: too many outer-controlled CNOT runs");
+                if (P.outer.size() > 32) throw std::logic_error("lower_plan: too many outer-controlled CNOT controls");
                 pm.n_ctrl = static_cast<int>(P.outer.size());
                 for (size_t b = 0; b < P.outer.size(); ++b) {
                     pm.ctrl_phys[b] = P.outer[b].first;

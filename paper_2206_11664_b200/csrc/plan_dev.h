@@ -73,8 +73,8 @@ struct PermDev {
     uint16_t hi[64];
     int n_ctrl;
     int pad;
-    int ctrl_phys[16];
-    uint32_t flip[16];
+    int ctrl_phys[32];
+    uint32_t flip[32];
 };
 
 // Pointwise factor on the full physical index i = outer(h) | local(l):

@@ -105,6 +105,12 @@ typedef struct sd_group_desc {
 
 sd_status sd_group_get(const sd_groups* g, size_t index, sd_group_desc* out);
 
+/* diag_document (proj/src/serialize.cpp:46-66, serialize.hpp:21): the `diag`
+ * JSON of a synthesised partition -- circuits, hex z-masks, signed
+ * coefficients -- the bit-exact grouping/circuit diff format. Same cap/len
+ * protocol as sd_hamiltonian_save_text. */
+sd_status sd_groups_diag_json(const sd_groups* g, int n_qubits, char* buf, size_t cap, size_t* len);
+
 /* ------------------------------------------------------------------ */
 /* Device state (replaces StateVector, statevector.hpp:34-97)          */
 /* ------------------------------------------------------------------ */
@@ -143,6 +149,12 @@ sd_status sd_state_set_random(sd_state* s, uint64_t seed);
  * equal the shard size. */
 sd_status sd_state_upload(sd_state* s, const double* re_im, uint64_t n_amps);
 sd_status sd_state_download(sd_state* s, double* re_im, uint64_t n_amps);
+/* save_raw / load_raw (statevector.cpp:383-401): raw little-endian (re, im)
+ * doubles of this shard's index range in logical order (a relabelled layout is
+ * canonicalised first, collectively for NCCL-attached shards); the rank files
+ * concatenate to the reference's file. */
+sd_status sd_state_save_raw(sd_state* s, const char* path);
+sd_status sd_state_load_raw(sd_state* s, const char* path);
 /* Sum |a|^2 over this shard (pairwise tree on device) -> sqrt is the
  * caller's once shards are combined; norm() of statevector.cpp:403-407 is
  * sqrt(sd_state_norm_sq) for world == 1. */

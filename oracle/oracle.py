@@ -246,6 +246,7 @@ class Ref:
         L.ref_pauli_rotation.argtypes = [dblp, C.c_int, C.c_uint64, C.c_uint64, C.c_double, C.c_double]
         L.ref_evolve_baseline_text.argtypes = [C.c_char_p, C.c_size_t, dblp, C.c_int, C.c_double, C.c_int]
         L.ref_expectation_text.argtypes = [C.c_char_p, C.c_size_t, dblp, C.c_int, dblp, dblp]
+        L.ref_diag_json.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
         L.ref_norm.argtypes = [dblp, C.c_int]
         L.ref_norm.restype = C.c_double
 
@@ -324,6 +325,14 @@ class Ref:
     def norm(self, psi, n) -> float:
         a = np.ascontiguousarray(psi, dtype=np.complex128)
         return self.lib.ref_norm(a.ctypes.data_as(dblp), n)
+
+    def diag_json(self, h) -> str:
+        """diag_document(...).dump() (serialize.cpp:46-66) of a partition_text handle."""
+        n = C.c_size_t(0)
+        self._err(self.lib.ref_diag_json(h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        self._err(self.lib.ref_diag_json(h, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
 
     def pauli_rotation(self, psi, n, x, z, coeff, dt):
         """StateVector::apply_pauli_rotation (statevector.cpp:288-337)."""

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "simdiag/diagonalize.hpp"
+#include "simdiag/serialize.hpp"
 #include "simdiag/hamiltonian.hpp"
 #include "simdiag/statevector.hpp"
 
@@ -278,6 +279,20 @@ int ref_expectation_text(const char* text, size_t len, const double* re_im, int 
         }
         *re = total.real();
         *imag = std::abs(total.imag());
+    });
+}
+
+// diag_document (serialize.cpp:46-66) of a partition_text handle, dumped.
+int ref_diag_json(void* h, char* buf, size_t cap, size_t* len) {
+    return guarded([&] {
+        auto* r = static_cast<RefGroups*>(h);
+        const std::string s = simdiag::diag_document(r->n, r->diags).dump();
+        *len = s.size();
+        if (buf && cap) {
+            const size_t k = std::min(cap - 1, s.size());
+            std::memcpy(buf, s.data(), k);
+            buf[k] = 0;
+        }
     });
 }
 

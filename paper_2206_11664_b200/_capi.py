@@ -146,6 +146,9 @@ sd_plan_kernel_times = _sig(
 sd_comm_unique_id = _sig("sd_comm_unique_id", [C.c_char_p])
 sd_state_attach_comm = _sig("sd_state_attach_comm", [P, C.c_char_p])
 sd_state_canonicalize = _sig("sd_state_canonicalize", [P])
+sd_groups_diag_json = _sig("sd_groups_diag_json", [P, C.c_int, C.c_char_p, sz, C.POINTER(sz)])
+sd_state_save_raw = _sig("sd_state_save_raw", [P, C.c_char_p])
+sd_state_load_raw = _sig("sd_state_load_raw", [P, C.c_char_p])
 sd_apply_pauli_rotation = _sig("sd_apply_pauli_rotation", [P, u64, u64, dbl, dbl])
 sd_evolve_baseline = _sig("sd_evolve_baseline", [P, C.POINTER(u64), C.POINTER(u64), C.POINTER(dbl), sz, dbl, C.c_int])
 sd_expectation = _sig("sd_expectation", [P, C.POINTER(u64), C.POINTER(u64), C.POINTER(dbl), sz, C.POINTER(dbl),
@@ -184,7 +187,8 @@ EXPORTED = [
     "sd_plan_kernel_times", "sd_comm_unique_id", "sd_state_attach_comm", "sd_state_canonicalize",
     "sd_state_create_local_shards", "sd_evolve_local", "sd_local_canonicalize", "sd_exchange_routes",
     "sd_jit_compile_preview", "sd_apply_pauli_rotation", "sd_evolve_baseline", "sd_expectation",
-    "sd_local_enable_p2p", "sd_state_ipc_handles", "sd_state_attach_peers",
+    "sd_local_enable_p2p", "sd_state_ipc_handles", "sd_state_attach_peers", "sd_groups_diag_json",
+    "sd_state_save_raw", "sd_state_load_raw",
 ]
 
 

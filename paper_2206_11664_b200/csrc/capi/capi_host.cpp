@@ -1,5 +1,7 @@
 // extern "C" host entry points: Hamiltonian I/O, greedy grouping and
 // Clifford synthesis (all computed by the from-scratch C++ in csrc/host).
+#include <charconv>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <sstream>
@@ -207,6 +209,63 @@ sd_status sd_group_get(const sd_groups* g, size_t index, sd_group_desc* d) {
         d->src_x = s.src_x.data();
         d->src_z = s.src_z.data();
         d->src_coeffs = s.src_c.data();
+    });
+}
+
+// `diag` document of a synthesised partition (the reference's
+// diag_document, proj/src/serialize.cpp:46-66): the bit-exact grouping /
+// circuit diff format. Keys in nlohmann::json's (sorted) order; z-masks as
+// "0x.." hex strings; coefficients as shortest round-trip doubles.
+sd_status sd_groups_diag_json(const sd_groups* g, int n_qubits, char* buf, size_t cap, size_t* len) {
+    return sdb::guard([&] {
+        sdb::require(g != nullptr, "null groups");
+        auto ints = [](std::ostringstream& os, const std::vector<int32_t>& v) {
+            os << "[";
+            for (size_t i = 0; i < v.size(); ++i) os << (i ? "," : "") << v[i];
+            os << "]";
+        };
+        auto pairs = [](std::ostringstream& os, const std::vector<int32_t>& v) {
+            os << "[";
+            for (size_t i = 0; i + 1 < v.size(); i += 2) os << (i ? "," : "") << "[" << v[i] << "," << v[i + 1] << "]";
+            os << "]";
+        };
+        auto dbl = [](std::ostringstream& os, double d) {
+            char b[64];
+            auto r = std::to_chars(b, b + sizeof b, d);
+            std::string t(b, r.ptr);
+            if (t.find_first_of(".eEn") == std::string::npos) t += ".0";
+            os << t;
+        };
+        std::ostringstream os;
+        os << "{\"groups\":[";
+        for (size_t i = 0; i < g->g.size(); ++i) {
+            const sd_group_store& st = g->g[i];
+            if (!st.synthesized) throw std::invalid_argument("groups are not synthesised (sd_partition_only)");
+            os << (i ? "," : "") << "{\"circuit\":{\"cnot\":";
+            pairs(os, st.cnots);
+            os << ",\"cz\":";
+            pairs(os, st.czs);
+            os << ",\"h_post\":";
+            ints(os, st.h_post);
+            os << ",\"h_pre\":";
+            ints(os, st.h_pre);
+            os << ",\"n_qubits\":" << st.diag.circuit.n_qubits << ",\"s\":";
+            ints(os, st.s_layer);
+            os << "},\"coeffs\":[";
+            for (size_t k = 0; k < st.diag.signed_coeffs.size(); ++k) {
+                if (k) os << ",";
+                dbl(os, st.diag.signed_coeffs[k]);
+            }
+            os << "],\"group\":" << st.diag.group_index << ",\"z_masks\":[";
+            for (size_t k = 0; k < st.diag.z_masks.size(); ++k) {
+                char b[24];
+                std::snprintf(b, sizeof b, "0x%llx", static_cast<unsigned long long>(st.diag.z_masks[k]));
+                os << (k ? "," : "") << "\"" << b << "\"";
+            }
+            os << "]}";
+        }
+        os << "],\"n_groups\":" << g->g.size() << ",\"n_qubits\":" << n_qubits << "}";
+        sdb::write_text_out(os.str(), buf, cap, len);
     });
 }
 

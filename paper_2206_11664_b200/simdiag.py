@@ -395,6 +395,14 @@ class StateVector:
         every rank passes the same 128-byte id from comm_unique_id()."""
         check(A.sd_state_attach_comm(self._s, C.create_string_buffer(bytes(unique_id), 128)))
 
+    def save_raw(self, path: str) -> None:
+        """statevector.cpp:383-387: raw (re, im) doubles of this shard, logical order."""
+        check(A.sd_state_save_raw(self._s, str(path).encode()))
+
+    def load_raw(self, path: str) -> None:
+        """statevector.cpp:389-401 into this (existing) shard."""
+        check(A.sd_state_load_raw(self._s, str(path).encode()))
+
     def ipc_handles(self) -> bytes:
         """This shard's two cudaIpcMemHandles (state, receive buffer), 128 bytes."""
         buf = C.create_string_buffer(128)
@@ -678,3 +686,19 @@ def jit_compile_preview(n_qubits: int, groups: Sequence[DiagonalGroup], order: i
     n = C.c_size_t(0)
     check(A.sd_jit_compile_preview(n_qubits, world, descs, len(groups), C.byref(opts), C.byref(n)))
     return n.value
+
+
+def diag_document(h: "Hamiltonian") -> str:
+    """The reference's `diag` JSON document (serialize.cpp:46-66) of
+    greedy_partition + diagonalize_group: circuits, hex z-masks, signed
+    coefficients (sd_groups_diag_json)."""
+    g = C.c_void_p()
+    check(A.sd_partition(h._h, C.byref(g)))
+    try:
+        n = C.c_size_t(0)
+        check(A.sd_groups_diag_json(g, h.n_qubits, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        check(A.sd_groups_diag_json(g, h.n_qubits, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+    finally:
+        A.sd_groups_destroy(g)

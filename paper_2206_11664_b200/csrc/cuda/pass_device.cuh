@@ -758,6 +758,26 @@ struct PassCtx {
             for (int j = 0; j < R; ++j)
 #pragma unroll
                 for (int s = 0; s < (1 << j); ++s) o[s + (1 << j)] = o[s] | op.c_off[j];
+        } else if (op.perm >= 0) {
+            // pending CNOT map applied by the addressing: register s (local
+            // index l) goes to P(l) = swz(lo[l & 63] ^ hi[l >> 6] ^ b(h))
+            go = out + base;
+            const PermDev* pm = plan.perms + op.perm;
+            uint32_t sb = 0;
+            for (int j = 0; j < pm->n_ctrl; ++j)
+                if ((full >> pm->ctrl_phys[j]) & 1ull) sb ^= pm->flip[j];
+            uint32_t l = rc.tb;
+#pragma unroll
+            for (int s = 0; s < NR; ++s) {
+                uint32_t ls = rc.tb;
+#pragma unroll
+                for (int j = 0; j < R; ++j)
+                    if ((s >> j) & 1) ls |= 1u << ((rc.cidx >> (8 * j)) & 255u);
+                const uint32_t m = swz(static_cast<uint32_t>(__ldg(&pm->lo[ls & 63u])) ^
+                                       static_cast<uint32_t>(__ldg(&pm->hi[ls >> 6])) ^ sb);
+                o[s] = off_of(m);
+            }
+            (void)l;
         } else {
             go = out + base;
             phys_offsets(o);

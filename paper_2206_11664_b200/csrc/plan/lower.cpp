@@ -229,6 +229,31 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
             take(all, true);
             return cfg;
         };
+        // the pending CNOT map P as a PermDev (swizzled-slot tables), P reset
+        auto make_perm = [&]() {
+            PermDev pm{};
+            for (int x = 0; x < 64; ++x) {
+                uint32_t lo = 0, hi = 0;
+                for (int b = 0; b < 6; ++b) {
+                    if ((x >> b) & 1) {
+                        if (b < K) lo ^= P.col[b];
+                        if (b + 6 < K) hi ^= P.col[b + 6];
+                    }
+                }
+                pm.lo[x] = static_cast<uint16_t>(host_swz(lo));
+                pm.hi[x] = static_cast<uint16_t>(host_swz(hi));
+            }
+            if (P.outer.size() > 32) throw std::logic_error("lower_plan: too many outer-controlled CNOT controls");
+            pm.n_ctrl = static_cast<int>(P.outer.size());
+            for (size_t b = 0; b < P.outer.size(); ++b) {
+                pm.ctrl_phys[b] = P.outer[b].first;
+                pm.flip[b] = host_swz(P.outer[b].second);
+            }
+            const int idx = static_cast<int>(A.perms.size());
+            A.perms.push_back(pm);
+            P = Affine(K);
+            return idx;
+        };
         auto emit = [&](int kind, uint32_t cfg) {
             MicroOpDev op{};
             op.kind = kind;
@@ -256,27 +281,7 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
             op.swc01 = sw[0] | (sw[1] << 16);
             op.swc23 = sw[2] | (sw[3] << 16);
             if (kind == kOpCfg && !P.identity) {
-                PermDev pm{};
-                for (int x = 0; x < 64; ++x) {
-                    uint32_t lo = 0, hi = 0;
-                    for (int b = 0; b < 6; ++b) {
-                        if ((x >> b) & 1) {
-                            if (b < K) lo ^= P.col[b];
-                            if (b + 6 < K) hi ^= P.col[b + 6];
-                        }
-                    }
-                    pm.lo[x] = static_cast<uint16_t>(host_swz(lo));
-                    pm.hi[x] = static_cast<uint16_t>(host_swz(hi));
-                }
-                if (P.outer.size() > 32) throw std::logic_error("lower_plan: too many outer-controlled CNOT controls");
-                pm.n_ctrl = static_cast<int>(P.outer.size());
-                for (size_t b = 0; b < P.outer.size(); ++b) {
-                    pm.ctrl_phys[b] = P.outer[b].first;
-                    pm.flip[b] = host_swz(P.outer[b].second);
-                }
-                op.perm = static_cast<int>(A.perms.size());
-                A.perms.push_back(pm);
-                P = Affine(K);
+                op.perm = make_perm();
                 only_point = false;
             }
             if (kind == kOpCfg) ++transposes;
@@ -506,12 +511,19 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
         }
         if (!loaded) {
             load(fill(0, 0));
+        }
+        // A CNOT map still pending at the end is applied by the store's
+        // addressing (no transpose) when the lanes stay coalesced.
+        int store_perm_idx = -1;
+        if (loaded && !P.identity && !(cur & low3) && pp.store_sigma.empty()) {
+            store_perm_idx = make_perm();
+            only_point = false;
         } else if (!P.identity || (cur & low3)) {
             emit(kOpCfg, fill(0, 0));
         }
         MicroOpDev so{};
         so.kind = kOpStore;
-        so.perm = -1;
+        so.perm = store_perm_idx;
         if (!pp.xswaps.empty()) {
             pd.x_bits = static_cast<int>(pp.xswaps.size());
             pd.x_t0 = n_local - pd.x_bits;

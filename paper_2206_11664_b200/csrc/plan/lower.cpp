@@ -109,7 +109,12 @@ std::vector<int> thread_order(uint32_t others) {
 // one term" relation, first-fit-decreasing into bins). Empty result: no such
 // cover, use the full angle table with a sincos per amplitude.
 constexpr int kMaxFacBits = 8;
-std::vector<uint32_t> factor_cover(const std::vector<uint32_t>& us, uint32_t tm) {
+// big_ok: a single factor may span up to kMaxBigFacBits coordinates (its
+// table is then rebuilt only when the tile's sign pattern changes, so the
+// caller allows it only when that happens a few times per CTA).
+constexpr int kMaxBigFacBits = 11;
+std::vector<uint32_t> factor_cover(const std::vector<uint32_t>& us, uint32_t tm, bool big_ok) {
+    if (big_ok && std::popcount(tm) <= kMaxBigFacBits && std::popcount(tm) > kMaxFacBits) return {tm};
     std::vector<int> parent(32);
     for (int i = 0; i < 32; ++i) parent[i] = i;
     auto find = [&](int x) {
@@ -385,8 +390,15 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                         ts.push_back({u, t.mask & ~Lphys, t.coeff * t.dt_scale});
                     }
                     std::vector<uint32_t> us;
-                    for (const T& t : ts) us.push_back(t.u);
-                    const std::vector<uint32_t> facs = factor_cover(us, tm);
+                    uint64_t pm_mixed = 0;  // outer bits of terms with local support
+                    for (const T& t : ts) {
+                        us.push_back(t.u);
+                        if (t.u) pm_mixed |= t.zh;
+                    }
+                    // a big single table pays off when each CTA sees ~1-2 sign patterns:
+                    // 2^(n_outer - |pm|) tiles per pattern >= tiles per CTA (~2^n_outer / 296)
+                    const bool big_ok = std::popcount(pm_mixed) <= 8;
+                    const std::vector<uint32_t> facs = factor_cover(us, tm, big_ok);
                     pt.table_mask = tm;
                     pt.table_bits = std::popcount(tm);
                     pt.n_fac = static_cast<int>(facs.size());

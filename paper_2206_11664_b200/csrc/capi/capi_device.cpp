@@ -73,6 +73,31 @@ int cx_split(int k) {
     return 1;  // single CNOTs schedule best (config 5: 3471 -> 2003 passes/step)
 }
 
+// Capacity of a CNOT resynthesis round: the tile's free coordinates.
+// SDB_CX_RESYNTH=0 keeps the synthesised CNOT order.
+int resynth_cap(int k) {
+    if (const char* e = std::getenv("SDB_CX_RESYNTH"); e && std::atoi(e) == 0) return 0;
+    return k - sdb::fixed_bits_for(k);
+}
+
+// Step ops with or without CNOT resynthesis, whichever schedules into fewer
+// passes (an exchange counts as two passes of traffic) from the identity
+// layout; resynthesis wins on CNOT-heavy groups (config 5) and can lose a
+// pass or two where the given CNOT order commutes better (config 3).
+std::vector<sdb::Op> best_step_ops(const std::vector<sdb::GroupSpec>& gs, int n, int order, int k, int n_local) {
+    auto ops = sdb::step_ops(gs, n, order, cx_split(k), 0);
+    const int cap = resynth_cap(k);
+    if (cap == 0) return ops;
+    auto alt = sdb::step_ops(gs, n, order, cx_split(k), cap);
+    std::vector<int> ident(n);
+    std::iota(ident.begin(), ident.end(), 0);
+    auto cost = [&](const std::vector<sdb::Op>& o) {
+        const sdb::ShardedStep ss = sdb::plan_sharded_step(o, gs, n_local, k, sdb::fixed_bits_for(k), ident);
+        return ss.n_passes + 2 * ss.n_exchanges;
+    };
+    return cost(alt) < cost(ops) ? alt : ops;
+}
+
 using sdb::guard;
 using sdb::require;
 
@@ -296,7 +321,7 @@ void plan_build(sd_plan& p) {
     if (!p.opts.fuse) return;
     int k = p.opts.tile_qubits > 0 ? p.opts.tile_qubits : 12;
     p.k = std::min({k, sdb::max_tile_qubits(), s.n_local});
-    p.ops = sdb::step_ops(p.groups, s.n, order, cx_split(p.k));
+    p.ops = best_step_ops(p.groups, s.n, order, p.k, s.n_local);
     std::vector<int> ident(s.n);
     std::iota(ident.begin(), ident.end(), 0);
     p.first = &step_for(p, ident);
@@ -992,7 +1017,7 @@ sd_status sd_plan_preview(int n, int world, const sd_group_desc* groups, size_t 
         std::iota(phys.begin(), phys.end(), 0);
         int k = o.tile_qubits > 0 ? o.tile_qubits : 12;
         k = std::min({k, sdb::max_tile_qubits(), n_local});
-        const auto ops = sdb::step_ops(gs, n, o.order, cx_split(k));
+        const auto ops = best_step_ops(gs, n, o.order, k, n_local);
         // steps until the layout repeats (the executor caches one plan per layout)
         std::vector<sdb::ShardedStep> steps;
         std::vector<std::vector<int>> seen;
@@ -1206,7 +1231,7 @@ sd_status sd_jit_compile_preview(int n, int world, const sd_group_desc* groups, 
         std::iota(phys.begin(), phys.end(), 0);
         int k = o.tile_qubits > 0 ? o.tile_qubits : 12;
         k = std::min({k, sdb::max_tile_qubits(), n_local});
-        const auto ops = sdb::step_ops(gs, n, o.order, cx_split(k));
+        const auto ops = best_step_ops(gs, n, o.order, k, n_local);
         const sdb::ShardedStep ss = sdb::plan_sharded_step(ops, gs, n_local, k, sdb::fixed_bits_for(k), phys);
         sdb::StepPlan combined;
         combined.tile_qubits = k;

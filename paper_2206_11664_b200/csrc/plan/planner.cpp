@@ -35,44 +35,256 @@ bool commute(const Op& a, const Op& b) {
     return (cx.targets & dg.support) == 0;
 }
 
-void emit_group(std::vector<Op>& out, const GroupSpec& g, int gi, double dt_scale, int max_targets) {
-    auto h = [&](int q) {
+// ---- CNOT network resynthesis -------------------------------------------
+// A group's CNOT list is a GF(2)-linear index map M (CX(c,t): x_t ^= x_c, a
+// row operation "row t += row c" on M). A tile pass can apply any CNOTs whose
+// targets are local, so M is re-expressed as rounds of CNOTs whose targets lie
+// in a set T of <= cap qubits: each round turns the rows of T into unit rows
+// using every other row (possible iff M restricted to the complement is
+// invertible), so ceil(#non-unit rows / cap) rounds suffice when the sets can
+// be chosen. The result is the same linear map (checked), hence the same
+// amplitude permutation, bit for bit.
+namespace {
+
+using Rows = std::vector<uint64_t>;  // row i: bit j set <=> M[i][j]
+
+bool invertible_on(const Rows& M, uint64_t cols_mask, const std::vector<int>& rows) {
+    // rank of the submatrix (rows x cols_mask) == |rows|
+    std::vector<uint64_t> r;
+    for (int i : rows) r.push_back(M[i] & cols_mask);
+    size_t rank = 0;
+    for (int c = 0; c < 64 && rank < r.size(); ++c) {
+        if (!((cols_mask >> c) & 1)) continue;
+        size_t piv = rank;
+        while (piv < r.size() && !((r[piv] >> c) & 1)) ++piv;
+        if (piv == r.size()) continue;
+        std::swap(r[piv], r[rank]);
+        for (size_t k = 0; k < r.size(); ++k)
+            if (k != rank && ((r[k] >> c) & 1)) r[k] ^= r[rank];
+        ++rank;
+    }
+    return rank == r.size();
+}
+
+// rows T of M^{-1} (M invertible, m x m)
+Rows inverse_rows(const Rows& M, int m) {
+    Rows a = M, inv(m);
+    for (int i = 0; i < m; ++i) inv[i] = 1ull << i;
+    for (int c = 0; c < m; ++c) {
+        int piv = c;
+        while (piv < m && !((a[piv] >> c) & 1)) ++piv;
+        if (piv == m) throw std::logic_error("resynth: singular CNOT map");
+        std::swap(a[piv], a[c]);
+        std::swap(inv[piv], inv[c]);
+        for (int k = 0; k < m; ++k) {
+            if (k != c && ((a[k] >> c) & 1)) {
+                a[k] ^= a[c];
+                inv[k] ^= inv[c];
+            }
+        }
+    }
+    return inv;
+}
+
+std::vector<std::pair<int, int>> resynth_cnots(const std::vector<std::pair<int, int>>& cnots, int cap) {
+    if (cnots.size() < 2 || cap < 1) return cnots;
+    std::vector<int> qs;
+    for (auto [c, t] : cnots) qs.insert(qs.end(), {c, t});
+    std::sort(qs.begin(), qs.end());
+    qs.erase(std::unique(qs.begin(), qs.end()), qs.end());
+    const int m = static_cast<int>(qs.size());
+    if (m > 64) return cnots;
+    auto idx = [&](int q) { return static_cast<int>(std::lower_bound(qs.begin(), qs.end(), q) - qs.begin()); };
+    Rows M(m);
+    for (int i = 0; i < m; ++i) M[i] = 1ull << i;
+    for (auto [c, t] : cnots) M[idx(t)] ^= M[idx(c)];
+    const Rows target = M;
+    std::vector<std::pair<int, int>> red;  // reduction ops (dense indices), applied in order
+    auto apply = [&](int c, int t) {
+        M[t] ^= M[c];
+        red.emplace_back(c, t);
+    };
+    std::vector<int> original_rounds;
+    for (int guard = 0; guard < 4 * m; ++guard) {
+        std::vector<int> nonunit;
+        for (int i = 0; i < m; ++i)
+            if (M[i] != (1ull << i)) nonunit.push_back(i);
+        if (nonunit.empty()) break;
+        std::vector<int> T;
+        const uint64_t all = m >= 64 ? ~0ull : ((1ull << m) - 1);
+        auto complement_ok = [&](const std::vector<int>& t) {
+            uint64_t tm = 0;
+            for (int i : t) tm |= 1ull << i;
+            std::vector<int> o;
+            for (int i = 0; i < m; ++i)
+                if (!((tm >> i) & 1)) o.push_back(i);
+            return invertible_on(M, all & ~tm, o);
+        };
+        if (static_cast<int>(nonunit.size()) <= cap) {
+            T = nonunit;
+        } else {
+            // first cap non-unit rows, then deterministic rotations of the candidate list
+            bool found = false;
+            for (size_t rot = 0; rot < nonunit.size() && !found; ++rot) {
+                std::vector<int> t;
+                for (int j = 0; j < cap; ++j) t.push_back(nonunit[(rot + j) % nonunit.size()]);
+                if (complement_ok(t)) {
+                    T = t;
+                    found = true;
+                }
+            }
+            if (!found) return cnots;  // keep the synthesis as given
+        }
+        uint64_t tm = 0;
+        for (int i : T) tm |= 1ull << i;
+        const Rows inv = inverse_rows(M, m);
+        // rows T <- A_TT rows_T + A_TO rows_O with A = (M^{-1})[T, :]
+        // (a) A_TT as row-add ops within T: Gauss-Jordan of A_TT (no swaps)
+        const int nt = static_cast<int>(T.size());
+        std::vector<uint32_t> att(nt);  // att[r] bit s: A[T_r][T_s]
+        for (int r = 0; r < nt; ++r)
+            for (int s2 = 0; s2 < nt; ++s2)
+                if ((inv[T[r]] >> T[s2]) & 1) att[r] |= 1u << s2;
+        std::vector<std::pair<int, int>> ops;  // (src, dst) in T-local indices reducing att to I
+        for (int c = 0; c < nt; ++c) {
+            if (!((att[c] >> c) & 1)) {
+                int piv = -1;
+                for (int r = 0; r < nt; ++r)
+                    if (r != c && ((att[r] >> c) & 1) && (r > c || !((att[r] >> r) & 1) || true)) {
+                        piv = r;
+                        break;
+                    }
+                if (piv < 0) return cnots;
+                att[c] ^= att[piv];
+                ops.emplace_back(piv, c);
+            }
+            for (int r = 0; r < nt; ++r) {
+                if (r != c && ((att[r] >> c) & 1)) {
+                    att[r] ^= att[c];
+                    ops.emplace_back(c, r);
+                }
+            }
+        }
+        // ops reduce A_TT to I: A_TT = product in reverse; applying A_TT to the
+        // rows of T = applying the ops in reverse order
+        for (auto it = ops.rbegin(); it != ops.rend(); ++it) apply(T[it->first], T[it->second]);
+        // (b) adds from outside T
+        for (int r = 0; r < nt; ++r) {
+            const uint64_t ao = inv[T[r]] & ~tm;
+            for (uint64_t b = ao; b; b &= b - 1) apply(std::countr_zero(b), T[r]);
+        }
+        for (int i : T) {
+            if (M[i] != (1ull << i)) return cnots;  // should not happen; keep the given synthesis
+        }
+    }
+    for (int i = 0; i < m; ++i)
+        if (M[i] != (1ull << i)) return cnots;
+    // forward circuit: the reduction reversed (every CNOT is an involution)
+    std::vector<std::pair<int, int>> out;
+    for (auto it = red.rbegin(); it != red.rend(); ++it) out.emplace_back(qs[it->first], qs[it->second]);
+    // check: same map
+    Rows chk(m);
+    for (int i = 0; i < m; ++i) chk[i] = 1ull << i;
+    for (auto [c, t] : out) chk[idx(t)] ^= chk[idx(c)];
+    if (chk != target) return cnots;
+    // Use it only if it needs fewer target rounds than the given list (proxy:
+    // consecutive windows with at most cap distinct targets).
+    auto windows = [cap](const std::vector<std::pair<int, int>>& l) {
+        int w = 0;
+        std::vector<int> tg;
+        for (auto [c, t] : l) {
+            (void)c;
+            if (std::find(tg.begin(), tg.end(), t) != tg.end()) continue;
+            if (tg.empty() || static_cast<int>(tg.size()) == cap) {
+                ++w;
+                tg.clear();
+            }
+            tg.push_back(t);
+        }
+        return w;
+    };
+    return windows(out) < windows(cnots) ? out : cnots;
+}
+
+}  // namespace
+
+// Emits group applications in order. CNOT networks are kept pending so that
+// C_g^dagger's inverse network and C_{g+1}'s network, adjacent whenever no
+// h_pre layer separates them, become ONE linear map that is re-synthesised as
+// a whole (CX(c,t) is an involution, so the inverse network is the list
+// reversed; statevector.cpp:341-349 applies runs in list order).
+class GroupEmitter {
+public:
+    GroupEmitter(std::vector<Op>& out, int max_targets, int resynth_cap)
+        : out_(out), max_targets_(max_targets), cap_(resynth_cap) {}
+
+    void group(const GroupSpec& g, int gi, double dt_scale) {
+        if (!g.h_pre.empty()) {
+            flush();
+            for (int q : g.h_pre) h(q);
+        }
+        pending_.insert(pending_.end(), g.cnots.begin(), g.cnots.end());
+        flush();
+        const bool has_phase = !g.czs.empty() || !g.s_layer.empty();
+        if (has_phase) ph(g, false);
+        for (int q : g.h_post) h(q);
+        {
+            Op o;
+            o.kind = Op::DG;
+            o.group = gi;
+            o.dt_scale = dt_scale;
+            for (uint64_t m : g.z_masks) o.support |= m;
+            out_.push_back(std::move(o));
+        }
+        for (int q : g.h_post) h(q);
+        if (has_phase) ph(g, true);
+        pending_.assign(g.cnots.rbegin(), g.cnots.rend());
+        if (!g.h_pre.empty()) {
+            flush();
+            for (int q : g.h_pre) h(q);
+        }
+    }
+
+    void flush() {
+        const std::vector<std::pair<int, int>> cn = cap_ > 0 ? resynth_cnots(pending_, cap_) : pending_;
+        pending_.clear();
+        for (size_t k = 0; k < cn.size();) {
+            const int c = cn[k].first;
+            uint64_t t = 0;
+            while (k < cn.size() && cn[k].first == c) t ^= bitq(cn[k++].second);  // CX(c,t)^2 = 1
+            // Same-control CNOTs commute, so a run wider than a tile can hold
+            // is split into sub-runs of at most max_targets targets.
+            while (std::popcount(t) > max_targets_) {
+                uint64_t part = 0;
+                for (int j = 0; j < max_targets_; ++j) {
+                    const uint64_t lo = t & (~t + 1);
+                    part |= lo;
+                    t ^= lo;
+                }
+                cx(c, part);
+            }
+            if (t) cx(c, t);
+        }
+    }
+
+private:
+    void h(int q) {
         Op o;
         o.kind = Op::H;
         o.q = q;
         o.support = o.need = bitq(q);
-        out.push_back(std::move(o));
-    };
-    // CNOT runs with one control, in application order (statevector.cpp:341-349).
-    std::vector<std::pair<int, uint64_t>> runs;
-    for (size_t k = 0; k < g.cnots.size();) {
-        const int c = g.cnots[k].first;
-        uint64_t t = 0;
-        while (k < g.cnots.size() && g.cnots[k].first == c) t |= bitq(g.cnots[k++].second);
-        // Same-control CNOTs commute, so a run wider than a tile can hold is
-        // split into sub-runs of at most max_targets targets.
-        while (std::popcount(t) > max_targets) {
-            uint64_t part = 0;
-            for (int j = 0; j < max_targets; ++j) {
-                const uint64_t lo = t & (~t + 1);
-                part |= lo;
-                t ^= lo;
-            }
-            runs.emplace_back(c, part);
-        }
-        runs.emplace_back(c, t);
+        out_.push_back(std::move(o));
     }
-    auto cx = [&](int c, uint64_t t) {
+    void cx(int c, uint64_t t) {
         Op o;
         o.kind = Op::CX;
         o.q = c;
         o.targets = t;
         o.support = t | bitq(c);
         o.need = t;
-        out.push_back(std::move(o));
-    };
-    const bool has_phase = !g.czs.empty() || !g.s_layer.empty();
-    auto ph = [&](bool dagger) {
+        out_.push_back(std::move(o));
+    }
+    void ph(const GroupSpec& g, bool dagger) {
         Op o;
         o.kind = Op::PH;
         o.dagger = dagger;
@@ -80,25 +292,13 @@ void emit_group(std::vector<Op>& out, const GroupSpec& g, int gi, double dt_scal
         o.czs = g.czs;
         o.support = o.s_mask;
         for (auto [a, b] : g.czs) o.support |= bitq(a) | bitq(b);
-        out.push_back(std::move(o));
-    };
-    for (int q : g.h_pre) h(q);
-    for (auto [c, t] : runs) cx(c, t);
-    if (has_phase) ph(false);
-    for (int q : g.h_post) h(q);
-    {
-        Op o;
-        o.kind = Op::DG;
-        o.group = gi;
-        o.dt_scale = dt_scale;
-        for (uint64_t m : g.z_masks) o.support |= m;
-        out.push_back(std::move(o));
+        out_.push_back(std::move(o));
     }
-    for (int q : g.h_post) h(q);
-    if (has_phase) ph(true);
-    for (auto it = runs.rbegin(); it != runs.rend(); ++it) cx(it->first, it->second);
-    for (int q : g.h_pre) h(q);
-}
+
+    std::vector<Op>& out_;
+    int max_targets_, cap_;
+    std::vector<std::pair<int, int>> pending_;
+};
 
 uint64_t to_phys(uint64_t logical, const std::vector<int>& phys_of) {
     uint64_t p = 0;
@@ -112,19 +312,22 @@ uint64_t to_phys(uint64_t logical, const std::vector<int>& phys_of) {
 
 }  // namespace
 
-std::vector<Op> step_ops(const std::vector<GroupSpec>& groups, int /*n_qubits*/, int order, int max_targets) {
+std::vector<Op> step_ops(const std::vector<GroupSpec>& groups, int /*n_qubits*/, int order, int max_targets,
+                         int resynth_cap) {
     std::vector<Op> ops;
     const int G = static_cast<int>(groups.size());
+    GroupEmitter em(ops, max_targets, resynth_cap);
     if (order == 1 || G <= 1) {
-        for (int g = 0; g < G; ++g) emit_group(ops, groups[g], g, 1.0, max_targets);
+        for (int g = 0; g < G; ++g) em.group(groups[g], g, 1.0);
     } else if (order == 2) {
         // Symmetric Suzuki S2 with the middle group merged.
-        for (int g = 0; g < G - 1; ++g) emit_group(ops, groups[g], g, 0.5, max_targets);
-        emit_group(ops, groups[G - 1], G - 1, 1.0, max_targets);
-        for (int g = G - 2; g >= 0; --g) emit_group(ops, groups[g], g, 0.5, max_targets);
+        for (int g = 0; g < G - 1; ++g) em.group(groups[g], g, 0.5);
+        em.group(groups[G - 1], G - 1, 1.0);
+        for (int g = G - 2; g >= 0; --g) em.group(groups[g], g, 0.5);
     } else {
         throw std::invalid_argument("trotter order must be 1 or 2");
     }
+    em.flush();
     return ops;
 }
 

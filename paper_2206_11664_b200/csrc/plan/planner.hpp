@@ -42,7 +42,10 @@ struct Op {
 
 // Builds the op sequence of one Trotter step (order 1 or 2).
 // CNOT runs wider than max_targets are split (same-control CNOTs commute).
-std::vector<Op> step_ops(const std::vector<GroupSpec>& groups, int n_qubits, int order, int max_targets);
+// resynth_cap > 0: re-synthesise each group's CNOT network into rounds whose
+// targets fit resynth_cap tile-local qubits (same linear map, fewer passes).
+std::vector<Op> step_ops(const std::vector<GroupSpec>& groups, int n_qubits, int order, int max_targets,
+                         int resynth_cap = 0);
 
 // A pass in physical bit positions.
 struct PassStage {

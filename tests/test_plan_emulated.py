@@ -51,7 +51,20 @@ def test_fused_pass_count_beats_reference_sweeps(sd):
         assert info["n_passes_per_step"] * 8 < info["n_ref_sweeps_per_step"]
 
 
-SHARDED = [(1, 10, 6, 2), (2, 9, 5, 4), (3, 10, 6, 2), (3, 10, 6, 8), (4, 11, 6, 2), (4, 11, 7, 4), (4, 12, 8, 8),
+def test_cnot_resynthesis_cuts_passes(sd, monkeypatch):
+    """Config 5 (Jordan-Wigner, CNOT-heavy groups): re-synthesising each CNOT
+    network into rounds of tile-local targets needs fewer passes than running
+    the synthesised CNOT list as given."""
+    text = M.config_text(5)
+    g = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
+    info, _ = sd.plan_preview(33, g, order=1, tile_qubits=12)
+    monkeypatch.setenv("SDB_CX_RESYNTH", "0")
+    info0, _ = sd.plan_preview(33, g, order=1, tile_qubits=12)
+    assert info["n_passes_per_step"] < 0.9 * info0["n_passes_per_step"]
+    assert info["n_passes_per_step"] * 8 < info["n_ref_sweeps_per_step"]
+
+
+SHARDED = [(3, 10, 6, 4), (1, 10, 6, 2), (2, 9, 5, 4), (3, 10, 6, 2), (3, 10, 6, 8), (4, 11, 6, 2), (4, 11, 7, 4), (4, 12, 8, 8),
            (5, 10, 6, 4), (5, 11, 7, 2)]
 
 

@@ -80,22 +80,45 @@ int resynth_cap(int k) {
     return k - sdb::fixed_bits_for(k);
 }
 
+// SDB_SPLIT_DIAG=1 splits diagonal ops per term, -1 picks whichever plans into
+// fewer passes; default whole diagonals (split passes carry more transposes
+// and phase stages per pass and measured slower, profiles/r1_notes.md).
+int split_diag_mode() {
+    if (const char* e = std::getenv("SDB_SPLIT_DIAG")) {
+        const int v = std::atoi(e);
+        return v < 0 ? -1 : (v != 0 ? 1 : 0);
+    }
+    return 0;
+}
+
 // Step ops with or without CNOT resynthesis, whichever schedules into fewer
 // passes (an exchange counts as two passes of traffic) from the identity
 // layout; resynthesis wins on CNOT-heavy groups (config 5) and can lose a
 // pass or two where the given CNOT order commutes better (config 3).
 std::vector<sdb::Op> best_step_ops(const std::vector<sdb::GroupSpec>& gs, int n, int order, int k, int n_local) {
-    auto ops = sdb::step_ops(gs, n, order, cx_split(k), 0);
-    const int cap = resynth_cap(k);
-    if (cap == 0) return ops;
-    auto alt = sdb::step_ops(gs, n, order, cx_split(k), cap);
     std::vector<int> ident(n);
     std::iota(ident.begin(), ident.end(), 0);
     auto cost = [&](const std::vector<sdb::Op>& o) {
         const sdb::ShardedStep ss = sdb::plan_sharded_step(o, gs, n_local, k, sdb::fixed_bits_for(k), ident);
         return ss.n_passes + 2 * ss.n_exchanges;
     };
-    return cost(alt) < cost(ops) ? alt : ops;
+    const int cap = resynth_cap(k);
+    const int split_env = split_diag_mode();
+    std::vector<sdb::Op> best;
+    int best_cost = 0;
+    for (int split = 0; split < 2; ++split) {
+        if ((split_env == 0 && split) || (split_env == 1 && !split)) continue;
+        for (int rs = 0; rs < 2; ++rs) {
+            if (rs && cap == 0) continue;
+            auto o = sdb::step_ops(gs, n, order, cx_split(k), rs ? cap : 0, split != 0);
+            const int c = cost(o);
+            if (best.empty() || c < best_cost) {
+                best = std::move(o);
+                best_cost = c;
+            }
+        }
+    }
+    return best;
 }
 
 using sdb::guard;
@@ -212,7 +235,11 @@ void clifford_unfused(sdb::StateImpl& s, const sdb::GroupSpec& g, bool inverse) 
 }
 
 // ---------------------------------------------------------------- plan build
-constexpr int kTableThreshold = 8;  // terms per POINT stage above which a per-tile table is used
+// terms per POINT stage above which a per-tile table is used (SDB_TABLE_THRESHOLD: experiments)
+const int kTableThreshold = [] {
+    const char* e = std::getenv("SDB_TABLE_THRESHOLD");
+    return e ? std::atoi(e) : 8;
+}();
 
 void upload_step(sd_plan& p, StepExec& E, const sdb::StepPlan& combined) {
     sdb::StateImpl& s = p.state->impl;

@@ -103,6 +103,24 @@ __device__ __forceinline__ void bfly(double2 (&v)[1 << R]) {
     }
 }
 
+// Swaps register coordinate J with lane bit B through warp shuffles (no
+// shared memory, no block barrier): afterwards register bit J holds the
+// coordinate lane bit B held and vice versa. 2^(R-1) double2 move per thread.
+template <int R, int J, int B>
+__device__ __forceinline__ void lane_swap(double2 (&v)[1 << R]) {
+    const bool hi = (threadIdx.x >> B) & 1u;
+#pragma unroll
+    for (int s = 0; s < (1 << R); ++s) {
+        if ((s >> J) & 1) continue;
+        const int s1 = s | (1 << J);
+        double2 x = hi ? v[s] : v[s1];
+        x.x = __shfl_xor_sync(0xffffffffu, x.x, 1 << B);
+        x.y = __shfl_xor_sync(0xffffffffu, x.y, 1 << B);
+        if (hi) v[s] = x;
+        else v[s1] = x;
+    }
+}
+
 template <int R>
 __device__ __forceinline__ void bfly_dispatch(double2 (&v)[1 << R], uint32_t mask) {
     switch (mask & ((1u << R) - 1u)) {
@@ -496,11 +514,13 @@ struct PassCtx {
         // Pull this CTA's next tile into L2 while the current one is
         // transformed: HBM keeps streaming through the compute phase
         // without holding registers or shared memory.
+#ifndef SDB_NO_PREFETCH
         if (t + stride < t_last) {
             const double2* gn = psi + tile_base(t + stride);
 #pragma unroll
             for (int s = 0; s < NR; ++s) prefetch_l2(gn + o[s]);
         }
+#endif
         // per-tile phase tables, built while the loads are in flight
         // (rebuilt only when the tile's table sign pattern changes, see PassDev::pat_shift)
         if (has_table) {
@@ -548,6 +568,22 @@ struct PassCtx {
             for (int s = 0; s < NR; ++s) v[s] = buf[a[s]];
         }
         smem_busy = true;
+    }
+
+    // register slot J <-> lane bit B by warp shuffles, then config r
+    template <int J, int B>
+    __device__ __forceinline__ void swap(const RegCfg& r, double2 (&v)[NR]) {
+        if constexpr (J < R) lane_swap<R, J, B>(v);
+        rc = r;
+    }
+    __device__ __forceinline__ void swap_any(const MicroOpDev& op, const RegCfg& r, double2 (&v)[NR]) {
+        switch (op.mask) {
+#define SDB_SW(J, B) \
+    case (J) | ((B) << 4): swap<J, B>(r, v); break;
+            SDB_SW(0, 3) SDB_SW(1, 3) SDB_SW(2, 3) SDB_SW(3, 3) SDB_SW(0, 4) SDB_SW(1, 4) SDB_SW(2, 4) SDB_SW(3, 4)
+#undef SDB_SW
+            default: __trap();
+        }
     }
 
     // Phase mode of a POINT op (template parameter of point()):

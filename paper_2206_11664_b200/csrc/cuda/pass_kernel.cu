@@ -26,6 +26,8 @@ struct Interpreter {
                 ctx.load(ctx.cfg_of(op), v);
             } else if (kind == kOpCfg) {
                 ctx.cfg(op, ctx.cfg_of(op), v);
+            } else if (kind == kOpSwap) {
+                ctx.swap_any(op, ctx.cfg_of(op), v);
             } else if (kind == kOpBfly) {
                 dev::bfly_dispatch<Ctx::R>(v, op.mask);
             } else if (kind == kOpPoint) {

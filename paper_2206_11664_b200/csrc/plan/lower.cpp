@@ -60,16 +60,6 @@ uint32_t lowest_bits(uint32_t m, int count) {
     return out;
 }
 
-uint32_t slot_mask(uint32_t coords, uint32_t cfg) {
-    // slot j of a config <-> its j-th lowest coordinate
-    uint32_t out = 0;
-    int j = 0;
-    for (uint32_t m = cfg; m; m &= m - 1, ++j) {
-        if (coords & (m & (~m + 1u))) out |= 1u << j;
-    }
-    return out;
-}
-
 uint32_t pext_host(uint32_t v, uint32_t mask) {
     uint32_t out = 0, bit = 1;
     for (uint32_t m = mask; m; m &= m - 1, bit <<= 1) {
@@ -82,7 +72,7 @@ uint32_t pext_host(uint32_t v, uint32_t mask) {
 // take coordinates 0..2 when they are thread coordinates (coalescing);
 // otherwise three coordinates with distinct residues mod 3 (conflict-free
 // 128-bit shared-memory access, see swz in internal.hpp); the rest ascend.
-std::vector<int> thread_order(uint32_t others) {
+std::vector<int> thread_order(uint32_t others, uint32_t prefer34 = 0, uint32_t prefer34b = 0) {
     std::vector<int> order;
     uint32_t rest = others;
     if ((others & 7u) == 7u) {
@@ -99,8 +89,23 @@ std::vector<int> thread_order(uint32_t others) {
             }
         }
     }
+    // lanes 3 and 4 take preferred coordinates (bits a lane swap can reach)
+    for (uint32_t pref : {prefer34, prefer34b}) {
+        for (uint32_t m = rest & pref; m && order.size() < 5; m &= m - 1) {
+            order.push_back(std::countr_zero(m));
+            rest &= ~(m & (~m + 1u));
+        }
+    }
     for (uint32_t m = rest; m; m &= m - 1) order.push_back(std::countr_zero(m));
     return order;
+}
+
+bool lane_swaps_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SDB_LANE_SWAPS");
+        return !e || std::atoi(e) != 0;
+    }();
+    return on;
 }
 
 // Factor cover of a table point: split the coordinates its terms touch into
@@ -212,7 +217,11 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
         for (int i = static_cast<int>(pp.stages.size()) - 1; i >= 0; --i) {
             wht_after[i] = wht_after[i + 1] | (pp.stages[i].kind == PassStage::WHT ? pp.stages[i].mask : 0u);
         }
+        // current config: register slot j holds coordinate regc[j], thread
+        // bit b holds thr[b] (lanes are thread bits 0..4)
         uint32_t cur = 0;
+        int regc[4] = {0, 0, 0, 0};
+        std::vector<int> thr;
         bool loaded = false;
         bool scale_placed = false;
         Affine P(K);
@@ -259,14 +268,13 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
             P = Affine(K);
             return idx;
         };
-        auto emit = [&](int kind, uint32_t cfg) {
+        // a config given explicitly (register coordinates, thread order)
+        auto emit_explicit = [&](int kind, const int (&rc)[4], const std::vector<int>& order, uint32_t mask) {
             MicroOpDev op{};
             op.kind = kind;
-            op.mask = cfg;
+            op.mask = mask;
             op.perm = -1;
             op.arg = pd.n_cfg++;
-            const uint32_t others = all & ~cfg;
-            const std::vector<int> order = thread_order(others);
             const int nt = 1 << (K - R);
             for (int tid = 0; tid < nt; ++tid) {
                 uint32_t tb = 0;
@@ -276,12 +284,14 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                 A.cfg_tb.push_back(tb | (host_swz(tb) << 16));
             }
             uint32_t sw[4] = {0, 0, 0, 0};
-            int j = 0;
-            for (uint32_t m = cfg; m && j < 4; m &= m - 1, ++j) {
-                const int c = std::countr_zero(m);
+            cur = 0;
+            for (int j = 0; j < R; ++j) {
+                const int c = rc[j];
                 sw[j] = host_swz(1u << c);
                 op.cidx |= static_cast<uint32_t>(c) << (8 * j);
                 op.c_off[j] = 1ull << pp.lpos[c];
+                regc[j] = c;
+                cur |= 1u << c;
             }
             op.swc01 = sw[0] | (sw[1] << 16);
             op.swc23 = sw[2] | (sw[3] << 16);
@@ -291,26 +301,57 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
             }
             if (kind == kOpCfg) ++transposes;
             A.ops.push_back(op);
-            cur = cfg;
+            thr = order;
+        };
+        // a config by its register set (ascending slots), thread order by rule
+        auto emit = [&](int kind, uint32_t cfg, uint32_t prefer34 = 0, uint32_t prefer34b = 0) {
+            int rc[4] = {0, 0, 0, 0};
+            int j = 0;
+            for (uint32_t m = cfg; m && j < 4; m &= m - 1, ++j) rc[j] = std::countr_zero(m);
+            emit_explicit(kind, rc, thread_order(all & ~cfg, prefer34, prefer34b), cfg);
+        };
+        // register slot j <-> lane bit b through warp shuffles
+        auto emit_swap = [&](int j, int b) {
+            int rc[4] = {regc[0], regc[1], regc[2], regc[3]};
+            std::vector<int> order = thr;
+            std::swap(rc[j], order[b]);
+            emit_explicit(kOpSwap, rc, order, static_cast<uint32_t>(j | (b << 4)));
         };
         // LOAD (identity positions), then flush a pending CNOT map if any.
-        auto load = [&](uint32_t cfg) {
-            emit(kOpLoad, cfg);
+        auto load = [&](uint32_t cfg, uint32_t prefer34 = 0) {
+            emit(kOpLoad, cfg, prefer34);
             loaded = true;
             if (!P.identity) emit(kOpCfg, cfg);
         };
+        // the table goes to the POINT stage with the most real-angle terms
+        int table_stage_point = -1;
+        {
+            size_t best = static_cast<size_t>(table_threshold);
+            for (const PassStage& st : pp.stages) {
+                if (st.kind != PassStage::POINT) continue;
+                const size_t nt = pp.points[st.point].terms.size();
+                if (nt > best) {
+                    best = nt;
+                    table_stage_point = st.point;
+                }
+            }
+        }
         for (size_t si = 0; si < pp.stages.size(); ++si) {
             const PassStage& st = pp.stages[si];
             const uint32_t after = wht_after[si + 1];
             if (st.kind == PassStage::WHT) {
                 only_point = false;
                 uint32_t bits = st.mask;
+                // lanes 3 and 4 exist (and keep lanes 0..2 untouched) for >= 32 threads
+                const bool swaps = lane_swaps_enabled() && K - R >= 5;
                 while (bits) {
                     if (loaded && P.identity && (bits & cur)) {
                         const uint32_t doing = bits & cur;
                         MicroOpDev b{};
                         b.kind = kOpBfly;
-                        b.mask = slot_mask(doing, cur);
+                        b.mask = 0;
+                        for (int j = 0; j < R; ++j)
+                            if ((doing >> regc[j]) & 1u) b.mask |= 1u << j;
                         b.perm = -1;
                         A.ops.push_back(b);
                         bits &= ~doing;
@@ -318,8 +359,27 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                     }
                     if (!loaded) {
                         const uint32_t chunk = lowest_bits(bits & ~low3, R);
-                        load(fill(chunk, (bits | after) & ~chunk));
+                        const uint32_t cfg = fill(chunk, (bits | after) & ~chunk);
+                        load(cfg, swaps ? (bits & ~cfg) : 0u);
                         continue;
+                    }
+                    // coordinates left only on lanes 3/4: bring them into registers
+                    // with shuffles (a fraction of a transpose's cost) in exchange
+                    // for register coordinates this stage is done with
+                    if (swaps && P.identity) {
+                        const uint32_t lanes34 = (1u << thr[3]) | (1u << thr[4]);
+                        if ((bits & ~lanes34) == 0) {
+                            for (int b = 3; b <= 4; ++b) {
+                                if (!((bits >> thr[b]) & 1u)) continue;
+                                int jbest = -1;
+                                for (int j = 0; j < R; ++j) {
+                                    if ((bits >> regc[j]) & 1u) continue;
+                                    if (jbest < 0 || (((after >> regc[jbest]) & 1u) && !((after >> regc[j]) & 1u))) jbest = j;
+                                }
+                                emit_swap(jbest, b);
+                            }
+                            continue;
+                        }
                     }
                     uint32_t chunk;
                     if (bits & low3) {
@@ -328,7 +388,8 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                     } else {
                         chunk = lowest_bits(bits, R);
                     }
-                    emit(kOpCfg, fill(chunk, (bits | after) & ~chunk));
+                    const uint32_t cfg = fill(chunk, (bits | after) & ~chunk);
+                    emit(kOpCfg, cfg, swaps ? (bits & ~cfg) : 0u, swaps ? (after & ~cfg) : 0u);
                 }
             } else if (st.kind == PassStage::CX) {
                 only_point = false;
@@ -376,7 +437,7 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                 pt.term_off = static_cast<int>(A.term_hmask.size());
                 pt.n_terms = static_cast<int>(ps.terms.size());
                 pt.seg_off = static_cast<int>(A.segs.size());
-                if (pt.n_terms > table_threshold && pd.table_point < 0) {
+                if (st.point == table_stage_point) {
                     struct T {
                         uint32_t u;
                         uint64_t zh;
@@ -483,7 +544,7 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                     // register coordinate (swc01/swc23) and QT(r_s) for the 2^R
                     // register combinations r_s (pad, bit s)
                     std::vector<uint32_t> cbits;
-                    for (uint32_t m = cur; m; m &= m - 1) cbits.push_back(m & (~m + 1u));
+                    for (int j = 0; j < R; ++j) cbits.push_back(1u << regc[j]);
                     uint32_t tic[4] = {0, 0, 0, 0};
                     if (pd.table_point == static_cast<int>(A.points.size())) {
                         for (size_t j = 0; j < cbits.size() && j < 4; ++j) tic[j] = pext_host(cbits[j], pt.table_mask);
@@ -545,10 +606,7 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
             pd.store_perm = 1;
             for (int j = 0; j < K; ++j) pd.st_lpos[j] = pp.store_sigma[pp.lpos[j]];
             for (int j = 0; j < pd.n_outer; ++j) pd.st_opos[j] = pp.store_sigma[pd.opos[j]];
-            int j = 0;
-            for (uint32_t m = cur; m && j < 4; m &= m - 1, ++j) {
-                so.c_off[j] = 1ull << pp.store_sigma[pp.lpos[std::countr_zero(m)]];
-            }
+            for (int j = 0; j < R; ++j) so.c_off[j] = 1ull << pp.store_sigma[pp.lpos[regc[j]]];
         }
         if (pp.scale_exp > 0 && !scale_placed) so.mask |= 2u;
         A.ops.push_back(so);
@@ -606,6 +664,7 @@ std::string describe_program(const HostPlanArrays& a) {
             if (op.kind == kOpLoad) os << " LD{" << std::hex << op.mask << std::dec << "}";
             else if (op.kind == kOpCfg) os << " CFG{" << std::hex << op.mask << std::dec << (op.perm >= 0 ? ",perm" : "") << "}";
             else if (op.kind == kOpBfly) os << " B" << std::popcount(op.mask);
+            else if (op.kind == kOpSwap) os << " X" << (op.mask & 15u) << ":" << (op.mask >> 4);
             else if (op.kind == kOpPoint) {
                 const PointDev& pt = a.points[op.arg];
                 std::string tdesc;

@@ -10,6 +10,7 @@
 #include "planner.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <bit>
 #include <sstream>
 #include <stdexcept>
@@ -19,6 +20,18 @@ namespace sdb {
 namespace {
 
 inline uint64_t bitq(int q) { return 1ull << q; }
+
+}  // namespace
+
+int fixed_bits_for(int k) {
+    static const int want = [] {
+        const char* e = std::getenv("SDB_FIXED_BITS");
+        return e ? std::atoi(e) : 3;
+    }();
+    return std::max(0, std::min(want, k - 1));
+}
+
+namespace {
 
 bool is_diag(const Op& o) { return o.kind == Op::PH || o.kind == Op::DG; }
 
@@ -215,8 +228,8 @@ std::vector<std::pair<int, int>> resynth_cnots(const std::vector<std::pair<int, 
 // reversed; statevector.cpp:341-349 applies runs in list order).
 class GroupEmitter {
 public:
-    GroupEmitter(std::vector<Op>& out, int max_targets, int resynth_cap)
-        : out_(out), max_targets_(max_targets), cap_(resynth_cap) {}
+    GroupEmitter(std::vector<Op>& out, int max_targets, int resynth_cap, bool split_diag)
+        : out_(out), max_targets_(max_targets), cap_(resynth_cap), split_(split_diag) {}
 
     void group(const GroupSpec& g, int gi, double dt_scale) {
         if (!g.h_pre.empty()) {
@@ -228,7 +241,18 @@ public:
         const bool has_phase = !g.czs.empty() || !g.s_layer.empty();
         if (has_phase) ph(g, false);
         for (int q : g.h_post) h(q);
-        {
+        if (split_) {
+            for (size_t t = 0; t < g.z_masks.size(); ++t) {
+                Op o;
+                o.kind = Op::DG;
+                o.group = gi;
+                o.t0 = static_cast<int>(t);
+                o.t1 = static_cast<int>(t + 1);
+                o.dt_scale = dt_scale;
+                o.support = g.z_masks[t];
+                out_.push_back(std::move(o));
+            }
+        } else {
             Op o;
             o.kind = Op::DG;
             o.group = gi;
@@ -285,6 +309,24 @@ private:
         out_.push_back(std::move(o));
     }
     void ph(const GroupSpec& g, bool dagger) {
+        if (split_) {
+            for (int q : g.s_layer) {
+                Op o;
+                o.kind = Op::PH;
+                o.dagger = dagger;
+                o.s_mask = o.support = bitq(q);
+                out_.push_back(std::move(o));
+            }
+            for (auto cz : g.czs) {
+                Op o;
+                o.kind = Op::PH;
+                o.dagger = dagger;
+                o.czs = {cz};
+                o.support = bitq(cz.first) | bitq(cz.second);
+                out_.push_back(std::move(o));
+            }
+            return;
+        }
         Op o;
         o.kind = Op::PH;
         o.dagger = dagger;
@@ -297,6 +339,7 @@ private:
 
     std::vector<Op>& out_;
     int max_targets_, cap_;
+    bool split_;
     std::vector<std::pair<int, int>> pending_;
 };
 
@@ -313,10 +356,10 @@ uint64_t to_phys(uint64_t logical, const std::vector<int>& phys_of) {
 }  // namespace
 
 std::vector<Op> step_ops(const std::vector<GroupSpec>& groups, int /*n_qubits*/, int order, int max_targets,
-                         int resynth_cap) {
+                         int resynth_cap, bool split_diag) {
     std::vector<Op> ops;
     const int G = static_cast<int>(groups.size());
-    GroupEmitter em(ops, max_targets, resynth_cap);
+    GroupEmitter em(ops, max_targets, resynth_cap, split_diag);
     if (order == 1 || G <= 1) {
         for (int g = 0; g < G; ++g) em.group(groups[g], g, 1.0);
     } else if (order == 2) {
@@ -374,6 +417,144 @@ void finalize_scales(std::vector<PassPlan*>& passes) {
     if (pending != 0) throw std::logic_error("plan_step: normalisation did not close");
 }
 
+namespace {
+
+constexpr size_t kMaxDiagPerPass = 16384;
+
+// SDB_MAX_HDEPTH: WHT levels per pass (0 = unlimited)
+int max_hadamard_depth() {
+    const char* e = std::getenv("SDB_MAX_HDEPTH");
+    return e ? std::atoi(e) : 0;
+}
+
+bool dram_pattern_heuristic() {
+    const char* e = std::getenv("SDB_DRAM_PATTERN");
+    return !e || std::atoi(e) != 0;
+}
+
+bool consolidate_enabled() {
+    const char* e = std::getenv("SDB_CONSOLIDATE");
+    return !e || std::atoi(e) != 0;
+}
+
+// Orders a pass's ops (valid in the given order) into few stages: all ready
+// Hadamards form one WHT stage, then ready CNOTs, and diagonal ops only when
+// no gate is ready, so each POINT stage collects every term it can.
+std::vector<int> stage_order(const std::vector<Op>& ops, std::vector<int> sched) {
+    std::sort(sched.begin(), sched.end());  // program order is a valid order
+    const size_t m = sched.size();
+    std::vector<std::vector<int>> preds(m);
+    bool any_diag = false;
+    for (size_t j = 0; j < m; ++j) {
+        any_diag |= is_diag(ops[sched[j]]);
+        for (size_t i = 0; i < j; ++i)
+            if (!commute(ops[sched[i]], ops[sched[j]])) preds[j].push_back(static_cast<int>(i));
+    }
+    if (!any_diag) return sched;
+    std::vector<char> taken(m, 0);
+    std::vector<int> out;
+    auto ready = [&](size_t j) {
+        if (taken[j]) return false;
+        for (int i : preds[j])
+            if (!taken[i]) return false;
+        return true;
+    };
+    while (out.size() < m) {
+        bool progress = false;
+        for (int cls = 0; cls < 3 && !progress; ++cls) {
+            for (bool again = true; again;) {
+                again = false;
+                for (size_t j = 0; j < m; ++j) {
+                    const Op& o = ops[sched[j]];
+                    const int c = o.kind == Op::H ? 0 : o.kind == Op::CX ? 1 : 2;
+                    if (c != cls || !ready(j)) continue;
+                    taken[j] = 1;
+                    out.push_back(sched[j]);
+                    again = progress = true;
+                    if (cls == 1) break;  // one CNOT, then look for Hadamards again
+                }
+                if (cls == 1 && progress) break;
+            }
+        }
+        if (!progress) throw std::logic_error("stage_order: cyclic dependencies");
+    }
+    return out;
+}
+
+// Diagonal ops need no tile-local qubit, so each may sit anywhere between the
+// last gate before it and the first gate after it that it does not commute
+// with. Given the gate order the scheduler chose, every diagonal op therefore
+// has an interval of gaps; stabbing all intervals with the fewest gaps
+// (greedy by right end, optimal for intervals) merges them into the fewest
+// POINT stages. Passes left without gates are dropped.
+void consolidate_diagonals(const std::vector<Op>& ops, std::vector<std::vector<int>>& pass_ops,
+                           std::vector<uint64_t>& pass_local) {
+    std::vector<int> seq, pass_of;
+    std::vector<int> diag;
+    for (size_t p = 0; p < pass_ops.size(); ++p) {
+        for (int id : pass_ops[p]) {
+            if (is_diag(ops[id])) {
+                diag.push_back(id);
+            } else {
+                seq.push_back(id);
+                pass_of.push_back(static_cast<int>(p));
+            }
+        }
+    }
+    if (seq.empty() || diag.empty()) return;
+    // gates per qubit they do not commute with a diagonal on (H: its qubit; CX: targets)
+    std::vector<std::vector<int>> on(64);
+    for (size_t i = 0; i < seq.size(); ++i) {
+        const Op& g = ops[seq[i]];
+        uint64_t m = g.kind == Op::H ? bitq(g.q) : g.targets;
+        for (; m; m &= m - 1) on[std::countr_zero(m)].push_back(static_cast<int>(i));
+    }
+    struct Iv {
+        int a, b, id;
+    };
+    std::vector<Iv> iv;
+    iv.reserve(diag.size());
+    for (int d : diag) {
+        int a = 0, b = static_cast<int>(seq.size());
+        for (uint64_t m = ops[d].support; m; m &= m - 1) {
+            for (int i : on[std::countr_zero(m)]) {
+                if (seq[i] < d) a = std::max(a, i + 1);
+                else b = std::min(b, i);
+            }
+        }
+        if (a > b) throw std::logic_error("consolidate_diagonals: schedule violates a dependency");
+        iv.push_back({a, b, d});
+    }
+    std::sort(iv.begin(), iv.end(), [](const Iv& x, const Iv& y) { return x.b != y.b ? x.b < y.b : x.a < y.a; });
+    std::vector<std::vector<int>> at(seq.size() + 1);
+    int stab = -1;
+    for (const Iv& v : iv) {
+        if (stab < v.a) stab = v.b;
+        at[stab].push_back(v.id);
+    }
+    std::vector<std::vector<int>> out(pass_ops.size());
+    for (size_t g = 0; g <= seq.size(); ++g) {
+        const int p = g < seq.size() ? pass_of[g] : pass_of.back();
+        std::vector<int>& d = at[g];
+        std::sort(d.begin(), d.end());
+        out[p].insert(out[p].end(), d.begin(), d.end());
+        if (g < seq.size()) out[p].push_back(seq[g]);
+    }
+    std::vector<std::vector<int>> kept;
+    std::vector<uint64_t> kept_local;
+    for (size_t p = 0; p < out.size(); ++p) {
+        bool gate = false;
+        for (int id : out[p]) gate |= !is_diag(ops[id]);
+        if (!gate) continue;
+        kept.push_back(std::move(out[p]));
+        kept_local.push_back(pass_local[p]);
+    }
+    pass_ops = std::move(kept);
+    pass_local = std::move(kept_local);
+}
+
+}  // namespace
+
 StepPlan plan_step(const std::vector<Op>& ops, const std::vector<GroupSpec>& groups, int n_local,
                    int k, int n_fixed, const std::vector<int>& phys_of, bool finalize) {
     if (k > n_local) k = n_local;
@@ -418,31 +599,78 @@ StepPlan plan_step(const std::vector<Op>& ops, const std::vector<GroupSpec>& gro
     };
     std::vector<std::vector<int>> pass_ops;
     std::vector<uint64_t> pass_local;
+    std::vector<int> hq(64, 0), dq(64, 0);
+    uint64_t good_logical = 0;
+    if (dram_pattern_heuristic()) {
+        for (int q = 0; q < n_logical; ++q)
+            if ((phys_of[q] == 3 || phys_of[q] == 5) && phys_of[q] >= n_fixed && phys_of[q] < n_local) good_logical |= bitq(q);
+    }
+    constexpr size_t kGoodLookahead = 64;
+    const int max_depth = max_hadamard_depth();
     while (first < N) {
         uint64_t L = fixed_logical;
         std::vector<int> sched;
         extend();
+        int n_gates = 0;
+        // Hadamard depth inside the pass: every further WHT level costs about
+        // two shared-memory transposes per tile, so a pass stops at max_depth
+        // levels (hq: depth of the last gate on a qubit, dq: of the last
+        // diagonal containing it; diagonals depend only on gates).
+        std::fill(hq.begin(), hq.end(), 0);
+        std::fill(dq.begin(), dq.end(), 0);
+        auto depth_of = [&](const Op& o) {
+            int d = 0;
+            for (uint64_t m = o.support; m; m &= m - 1) {
+                const int q = std::countr_zero(m);
+                d = std::max(d, is_diag(o) ? hq[q] : std::max(hq[q], dq[q]));
+            }
+            return d + (o.kind == Op::H ? 1 : 0);
+        };
+        auto depth_ok = [&](const Op& o) { return max_depth <= 0 || depth_of(o) <= max_depth; };
         for (;;) {
-            if (sched.size() >= static_cast<size_t>(kMaxOpsPerPass)) break;
+            if (n_gates >= kMaxOpsPerPass || sched.size() >= kMaxDiagPerPass) break;
             long pick = -1;
             for (size_t j = first; j < hi; ++j) {
-                if (!done[j] && blockers[j] == 0 && (ops[j].need & ~L) == 0) {
+                if (!done[j] && blockers[j] == 0 && (ops[j].need & ~L) == 0 && depth_ok(ops[j])) {
                     pick = static_cast<long>(j);
                     break;
                 }
             }
             if (pick < 0) {
+                // HBM pattern: a tile with a local bit at physical 3 or 5 spreads
+                // over twice the channels (tools/membench3: 8.3 -> 6.0 ms at
+                // n=30 for otherwise high local bits), so a pass without one
+                // takes such an op first, and a pass with one leaves the others
+                // to later passes when it can.
+                const bool have_good = (L & good_logical) != 0;
+                long fallback = -1;
                 for (size_t j = first; j < hi; ++j) {
-                    if (!done[j] && blockers[j] == 0 && std::popcount(L | ops[j].need) <= k) {
-                        pick = static_cast<long>(j);
-                        break;
+                    if (!done[j] && blockers[j] == 0 && std::popcount(L | ops[j].need) <= k && depth_ok(ops[j])) {
+                        const uint64_t g = ops[j].need & ~L & good_logical;
+                        if (!good_logical || (have_good ? g == 0 : g != 0)) {
+                            pick = static_cast<long>(j);
+                            break;
+                        }
+                        if (fallback < 0) fallback = static_cast<long>(j);
+                        if (!have_good && j > first + kGoodLookahead) break;
                     }
                 }
+                if (pick < 0) pick = fallback;
                 if (pick < 0) break;
                 L |= ops[pick].need;
             }
+            {
+                const Op& o = ops[pick];
+                const int d = depth_of(o);
+                for (uint64_t m = o.support; m; m &= m - 1) {
+                    const int q = std::countr_zero(m);
+                    if (is_diag(o)) dq[q] = std::max(dq[q], d);
+                    else hq[q] = std::max(hq[q], d);
+                }
+            }
             done[pick] = 1;
             sched.push_back(static_cast<int>(pick));
+            if (!is_diag(ops[pick])) ++n_gates;
             for (size_t j = pick + 1; j < hi; ++j) {
                 if (!done[j] && !commute(ops[pick], ops[j])) --blockers[j];
             }
@@ -450,9 +678,11 @@ StepPlan plan_step(const std::vector<Op>& ops, const std::vector<GroupSpec>& gro
             extend();
         }
         if (sched.empty()) throw std::logic_error("plan_step: no schedulable op (tile too small?)");
-        pass_ops.push_back(std::move(sched));
+        pass_ops.push_back(stage_order(ops, std::move(sched)));
         pass_local.push_back(L);
     }
+
+    if (consolidate_enabled()) consolidate_diagonals(ops, pass_ops, pass_local);
 
     // --- lower each pass to physical stages
     int cum = 0;
@@ -527,7 +757,8 @@ StepPlan plan_step(const std::vector<Op>& ops, const std::vector<GroupSpec>& gro
                     for (auto [a, b] : o.czs) ps.cz_masks.push_back(bitq(phys_of[a]) | bitq(phys_of[b]));
                 } else {
                     const GroupSpec& g = groups[o.group];
-                    for (size_t t = 0; t < g.z_masks.size(); ++t) {
+                    const size_t t1 = o.t1 < 0 ? g.z_masks.size() : static_cast<size_t>(o.t1);
+                    for (size_t t = static_cast<size_t>(o.t0); t < t1; ++t) {
                         ps.terms.push_back({to_phys(g.z_masks[t], phys_of), g.coeffs[t], o.dt_scale});
                     }
                 }

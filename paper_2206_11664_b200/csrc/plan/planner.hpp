@@ -16,7 +16,7 @@ constexpr int kMaxOpsPerPass = 96;
 
 // Physical bits kept local in every pass (0..2: 8 lanes x 16 B = one 128-byte
 // line); tiles of <= 3 qubits keep at least one free coordinate.
-inline int fixed_bits_for(int k) { return k - 1 < 3 ? (k - 1 > 0 ? k - 1 : 0) : 3; }
+int fixed_bits_for(int k);
 
 // One group as the planner sees it (a flattened DiagonalGroup).
 struct GroupSpec {
@@ -35,6 +35,7 @@ struct Op {
     bool dagger = false;     // PH
     std::vector<std::pair<int, int>> czs;  // PH
     int group = -1;          // DG: index into groups
+    int t0 = 0, t1 = -1;     // DG: term range [t0, t1) of the group (t1 < 0: all terms)
     double dt_scale = 1.0;   // DG: multiplier of dt
     uint64_t support = 0;    // qubits acted on (commutation checks)
     uint64_t need = 0;       // qubits that must be tile-local
@@ -44,8 +45,11 @@ struct Op {
 // CNOT runs wider than max_targets are split (same-control CNOTs commute).
 // resynth_cap > 0: re-synthesise each group's CNOT network into rounds whose
 // targets fit resynth_cap tile-local qubits (same linear map, fewer passes).
+// split_diag: every diagonal term (Pauli-Z string, S, CZ) becomes its own op
+// with its own support, so Hadamards of later layers can run ahead in the
+// same pass wherever a qubit's terms are done (temporal blocking).
 std::vector<Op> step_ops(const std::vector<GroupSpec>& groups, int n_qubits, int order, int max_targets,
-                         int resynth_cap = 0);
+                         int resynth_cap = 0, bool split_diag = false);
 
 // A pass in physical bit positions.
 struct PassStage {

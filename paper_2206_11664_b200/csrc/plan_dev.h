@@ -39,7 +39,9 @@ namespace sdb {
 // residues, which makes each quarter-warp of a 128-bit access conflict-free.
 // swz is GF(2)-linear, which the kernel and the lowering both exploit.
 
-enum MicroKind : int { kOpLoad = 0, kOpCfg = 1, kOpBfly = 2, kOpPoint = 3, kOpStore = 4 };
+// kOpSwap: register slot (mask & 15) <-> lane bit (mask >> 4) by warp shuffles,
+// then the op's config (like kOpCfg, without shared memory).
+enum MicroKind : int { kOpLoad = 0, kOpCfg = 1, kOpBfly = 2, kOpPoint = 3, kOpStore = 4, kOpSwap = 5 };
 
 struct MicroOpDev {
     int kind;

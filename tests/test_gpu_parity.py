@@ -114,6 +114,33 @@ def test_fused_evolve_matches_reference(cfg, n, k, sd, ref, port):
     assert st["kernel_calls"] == 4 * plan.info()["n_passes_per_step"]
 
 
+@pytest.mark.parametrize("env", [{"SDB_SPLIT_DIAG": "1"}, {"SDB_SPLIT_DIAG": "1", "SDB_MAX_HDEPTH": "2"},
+                                 {"SDB_DRAM_PATTERN": "0", "SDB_CX_RESYNTH": "0"}])
+@pytest.mark.parametrize("jit", ["0", "1"])
+@pytest.mark.parametrize("cfg,n,k", [(4, 14, 12), (3, 13, 10), (5, 13, 12)])
+def test_planner_modes_on_device(cfg, n, k, jit, env, sd, ref, port, monkeypatch):
+    """Planner variants (per-term diagonals, Hadamard-depth cap, no HBM-pattern
+    heuristic / CNOT resynthesis) through both the interpreter and the
+    NVRTC-specialised kernels (lane swaps, several POINT stages per pass)."""
+    monkeypatch.setenv("SDB_JIT", jit)
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    text = M.config_text(cfg, n=n)
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
+    order, dt = M.CONFIGS[cfg]["order"], M.CONFIGS[cfg]["dt"] * 5
+    psi0 = initial(port, cfg, n)
+    s = sd.StateVector(n)
+    s.upload(psi0)
+    plan = sd.TrotterPlan(s, groups, order=order, tile_qubits=k)
+    plan.evolve(dt, 3)
+    got = s.amplitudes()
+    h, _, _ = ref.partition_text(text)
+    want, _ = ref.evolve_grouped(h, psi0, n, dt, 3, order)
+    ref.free(h)
+    assert np.max(np.abs(got - want)) < TOL_AMP
+    assert abs(np.linalg.norm(got) - 1) < TOL_NORM
+
+
 def test_unfused_reference_schedule_matches(sd, ref, port):
     n, cfg = 11, 3
     text = M.config_text(cfg, n=n)

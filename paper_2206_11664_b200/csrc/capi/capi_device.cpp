@@ -427,7 +427,12 @@ void run_segment(sd_plan& p, StepExec& E, size_t seg, double dt) {
     const double bytes = 2.0 * 16.0 * double(s.amps_count());
     const bool exch = E.ss.segs[seg].exchange_after;
     const int first = E.seg_first[seg], count = E.seg_count[seg];
+    static const int debug_passes = [] {
+        const char* e = std::getenv("SDB_DEBUG_PASSES");  // debugging: run only the first N passes
+        return e ? std::atoi(e) : -1;
+    }();
     for (int i = first; i < first + count; ++i) {
+        if (debug_passes >= 0 && i >= debug_passes) break;
         const bool to_buf = exch && i == first + count - 1;
         // fused exchange: the pass stores straight into the peers' receive buffers
         double2* const* xdst = nullptr;

@@ -526,6 +526,9 @@ struct PassCtx {
         if (has_table) {
             const uint64_t pat = P.pat_shift >= 64 ? t : (t >> P.pat_shift);
             if (pat != last_pat) {
+                // the previous tile's POINT may still be reading the tables when
+                // no transpose (block barrier) follows it in the program
+                if (last_pat != ~0ull) __syncthreads();
                 last_pat = pat;
                 build_tables<NT>(tabc(), plan, plan.points[P.table_point], full, neg_dt, P.table_scale, false);
             }
@@ -781,6 +784,7 @@ struct PassCtx {
     }
 
     __device__ __forceinline__ void store(const MicroOpDev& op, double2 (&v)[NR]) {
+        if (op.mask & 4u) __syncthreads();  // cross-warp in-place store with no barrier since the load
         uint64_t o[NR];
         double2* go;
         if (store_perm) {

@@ -4,6 +4,8 @@
 // pass's program at plan time (jit.cpp).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "../internal.hpp"
 #include "jit.hpp"
 #include "pass_device.cuh"
@@ -80,6 +82,8 @@ void launch_kr(StateImpl& s, const PassDev& ph, int pass_index, const PlanDev& p
     const uint64_t n_tiles = 1ull << ph.n_outer;
     uint64_t grid = static_cast<uint64_t>(s.sm_count) * static_cast<uint64_t>(occ);
     if (grid > n_tiles) grid = n_tiles;
+    if (const char* e = std::getenv("SDB_MAX_CTAS"); e && std::atoi(e) > 0 && grid > uint64_t(std::atoi(e)))
+        grid = std::atoi(e);  // debugging: many tiles per CTA at small n
     k_tile_pass<K, RB><<<static_cast<unsigned>(grid), C::NT, smem, s.stream>>>(
         reinterpret_cast<const double2*>(s.amps), reinterpret_cast<double2*>(out ? out : s.amps), xdst, plan,
         pass_index, -dt, rank_bits, n_tiles);

@@ -100,13 +100,15 @@ std::vector<int> thread_order(uint32_t others, uint32_t prefer34 = 0, uint32_t p
     return order;
 }
 
-bool lane_swaps_enabled() {
-    static const bool on = [] {
+// SDB_LANE_SWAPS bit 0: emit lane swaps, bit 1: steer coordinates onto lanes 3/4
+int lane_swap_mode() {
+    static const int m = [] {
         const char* e = std::getenv("SDB_LANE_SWAPS");
-        return !e || std::atoi(e) != 0;
+        return e ? std::atoi(e) : 3;
     }();
-    return on;
+    return m;
 }
+bool lane_swaps_enabled() { return (lane_swap_mode() & 3) != 0; }
 
 // Factor cover of a table point: split the coordinates its terms touch into
 // at most three disjoint sets of <= kMaxFacBits coordinates such that no
@@ -344,6 +346,8 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                 uint32_t bits = st.mask;
                 // lanes 3 and 4 exist (and keep lanes 0..2 untouched) for >= 32 threads
                 const bool swaps = lane_swaps_enabled() && K - R >= 5;
+                const bool emit_swaps = swaps && (lane_swap_mode() & 1);
+                const bool steer = swaps && (lane_swap_mode() & 2);
                 while (bits) {
                     if (loaded && P.identity && (bits & cur)) {
                         const uint32_t doing = bits & cur;
@@ -360,13 +364,13 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                     if (!loaded) {
                         const uint32_t chunk = lowest_bits(bits & ~low3, R);
                         const uint32_t cfg = fill(chunk, (bits | after) & ~chunk);
-                        load(cfg, swaps ? (bits & ~cfg) : 0u);
+                        load(cfg, steer ? (bits & ~cfg) : 0u);
                         continue;
                     }
                     // coordinates left only on lanes 3/4: bring them into registers
                     // with shuffles (a fraction of a transpose's cost) in exchange
                     // for register coordinates this stage is done with
-                    if (swaps && P.identity) {
+                    if (emit_swaps && P.identity) {
                         const uint32_t lanes34 = (1u << thr[3]) | (1u << thr[4]);
                         if ((bits & ~lanes34) == 0) {
                             for (int b = 3; b <= 4; ++b) {
@@ -389,7 +393,7 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                         chunk = lowest_bits(bits, R);
                     }
                     const uint32_t cfg = fill(chunk, (bits | after) & ~chunk);
-                    emit(kOpCfg, cfg, swaps ? (bits & ~cfg) : 0u, swaps ? (after & ~cfg) : 0u);
+                    emit(kOpCfg, cfg, steer ? (bits & ~cfg) : 0u, steer ? (after & ~cfg) : 0u);
                 }
             } else if (st.kind == PassStage::CX) {
                 only_point = false;
@@ -597,6 +601,10 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
         MicroOpDev so{};
         so.kind = kOpStore;
         so.perm = store_perm_idx;
+        // An in-place store through a CNOT map writes other warps' positions:
+        // without a transpose (block barrier) since the load, warps of a CTA
+        // may still be loading them (or be a tile behind), so the store syncs.
+        if (store_perm_idx >= 0 && transposes == 0) so.mask |= 4u;
         if (!pp.xswaps.empty()) {
             pd.x_bits = static_cast<int>(pp.xswaps.size());
             pd.x_t0 = n_local - pd.x_bits;
@@ -652,6 +660,48 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
         A.transposes.push_back(transposes);
     }
     return A;
+}
+
+void verify_lowering(const HostPlanArrays& A) {
+    // Every register config op must place the element with local index l in
+    // the thread/register its tables say; only SWAP moves data without going
+    // through those tables, so simulate its shuffles and compare.
+    for (size_t p = 0; p < A.passes.size(); ++p) {
+        const PassDev& pd = A.passes[p];
+        const int R = pd.rbits, NT = 1 << (pd.k - R), NR = 1 << R;
+        auto label = [&](const MicroOpDev& op, int tid, int s) {
+            uint32_t l = A.cfg_tb[pd.cfg_off + static_cast<size_t>(op.arg) * NT + tid] & 0xffffu;
+            for (int j = 0; j < R; ++j)
+                if ((s >> j) & 1) l |= 1u << ((op.cidx >> (8 * j)) & 255u);
+            return l;
+        };
+        const MicroOpDev* prev = nullptr;
+        for (int i = 0; i < pd.n_ops; ++i) {
+            const MicroOpDev& op = A.ops[pd.op_off + i];
+            if (op.kind == kOpSwap) {
+                if (!prev) throw std::logic_error("verify_lowering: swap before load");
+                const int J = static_cast<int>(op.mask & 15u), B = static_cast<int>(op.mask >> 4);
+                for (int tid = 0; tid < NT; ++tid) {
+                    const bool hi = (tid >> B) & 1;
+                    const int partner = tid ^ (1 << B);
+                    for (int s = 0; s < NR; ++s) {
+                        // where register s of thread tid gets its value from (lane_swap)
+                        int st = tid, ss = s;
+                        const bool sj = (s >> J) & 1;
+                        if (hi && !sj) { st = partner; ss = s | (1 << J); }
+                        if (!hi && sj) { st = partner; ss = s & ~(1 << J); }
+                        if (label(op, tid, s) != label(*prev, st, ss)) {
+                            std::ostringstream os;
+                            os << "verify_lowering: pass " << p << " op " << i << " swap(" << J << "," << B
+                               << ") tid " << tid << " s " << s;
+                            throw std::logic_error(os.str());
+                        }
+                    }
+                }
+            }
+            if (op.kind == kOpLoad || op.kind == kOpCfg || op.kind == kOpSwap) prev = &op;
+        }
+    }
 }
 
 std::string describe_program(const HostPlanArrays& a) {

@@ -33,4 +33,7 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
 
 std::string describe_program(const HostPlanArrays& a);
 
+// Checks the register-config bookkeeping of every pass (throws on a mismatch).
+void verify_lowering(const HostPlanArrays& a);
+
 }  // namespace sdb

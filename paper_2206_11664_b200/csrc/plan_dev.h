@@ -47,7 +47,9 @@ struct MicroOpDev {
     int kind;
     uint32_t mask;  // LOAD/CFG: register coordinates (R bits among k); BFLY: register slots (bits 0..3);
                     // POINT: bit 0 = apply the pass scale here (folded into the phase factor);
-                    // STORE: bit 1 = apply the pass scale
+                    // STORE: bit 1 = apply the pass scale, bit 2 = block barrier first
+                    // (in-place store through a CNOT map with no transpose since the load);
+                    // SWAP: register slot (bits 0..3) | lane bit << 4
     int perm;       // CFG: PermDev index applied on the write side, or -1
     int arg;        // LOAD/CFG: index of this config among the pass's configs; POINT: PointDev index
     uint32_t swc01; // LOAD/CFG: swizzled slot offsets of register coordinates 0,1 (16 bits each);

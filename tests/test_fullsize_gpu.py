@@ -1,0 +1,105 @@
+"""Full-size checks (BASELINE.json sizes) through size-independent properties.
+
+The oracle needs about a minute per Trotter step at n=30, so at full size the
+fused path is checked through properties every correct implementation has:
+
+* time reversal: order 1 is U(dt) = e_G(dt)...e_1(dt), so the plan over the
+  reversed group list at -dt is its exact inverse; S2 is symmetric, so the same
+  plan at -dt inverts it (proj/src/evolve.cpp:47-58 defines both products);
+* unitarity: the norm stays 1 (the reference's tolerance, |1-||psi||| <= 1e-12);
+* independent paths agree: the sharded schedule (qubit remaps between passes,
+  in-process shards on one GPU) and the unsharded one give the same state.
+
+Config 5 (n=33, 128 GiB) runs only with SDB_TEST_CONFIG5=1 (several minutes of
+NVRTC compilation for its ~1500 distinct pass programs).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2206_11664_b200 import models as M
+
+pytestmark = pytest.mark.gpu
+
+TOL_ROUNDTRIP = 1e-11
+TOL_NORM = 1e-12
+
+
+def _groups(sd, cfg, n=None):
+    return sd.partition_and_diagonalize(sd.Hamiltonian.load(M.config_text(cfg, n)))
+
+
+def _start(sd, port, cfg, n):
+    psi = sd.StateVector(n)
+    init = M.CONFIGS[cfg]["init"]
+    if init[0] == "basis":
+        psi.set_basis(M.initial_index(cfg, n))
+        return psi, None
+    a = port.random_state(n, init[1]) if init[0] == "random" else np.full(1 << n, 1 / np.sqrt(1 << n), np.complex128)
+    psi.upload(a)
+    return psi, a
+
+
+def _check_back_at_start(psi, cfg, n, a0):
+    got = psi.amplitudes()
+    if a0 is None:
+        k = M.initial_index(cfg, n)
+        dev = abs(got[k] - 1.0)
+        got[k] = 0
+        dev = max(dev, float(np.max(np.abs(got))))
+    else:
+        dev = float(np.max(np.abs(got - a0)))
+    assert dev < TOL_ROUNDTRIP, dev
+
+
+@pytest.mark.parametrize("cfg,steps", [(4, 8), (3, 2)])
+def test_order1_time_reversal_full_size(cfg, steps, sd, port):
+    n = M.CONFIGS[cfg]["n"]
+    groups = _groups(sd, cfg)
+    psi, a0 = _start(sd, port, cfg, n)
+    dt = M.CONFIGS[cfg]["dt"]
+    fwd = sd.TrotterPlan(psi, groups, order=1)
+    fwd.evolve(dt, steps)
+    assert abs(psi.norm() - 1) < TOL_NORM
+    bwd = sd.TrotterPlan(psi, list(reversed(groups)), order=1)
+    bwd.evolve(-dt, steps)
+    assert abs(psi.norm() - 1) < TOL_NORM
+    _check_back_at_start(psi, cfg, n, a0)
+
+
+def test_order2_time_reversal_full_size(sd, port):
+    cfg = 2
+    n = M.CONFIGS[cfg]["n"]
+    psi, a0 = _start(sd, port, cfg, n)
+    plan = sd.TrotterPlan(psi, _groups(sd, cfg), order=2)
+    dt = M.CONFIGS[cfg]["dt"]
+    plan.evolve(dt, 50)
+    assert abs(psi.norm() - 1) < TOL_NORM
+    plan.evolve(-dt, 50)
+    _check_back_at_start(psi, cfg, n, a0)
+
+
+def test_sharded_and_unsharded_agree_full_size(sd, port):
+    """Config 4 at n=30: two in-process shards (one qubit remapped between
+    passes, fused peer stores) against the single-state path."""
+    cfg, n, steps = 4, 30, 3
+    groups = _groups(sd, cfg)
+    dt = M.CONFIGS[cfg]["dt"]
+    psi, _ = _start(sd, port, cfg, n)
+    sd.TrotterPlan(psi, groups, order=1).evolve(dt, steps)
+    want = psi.amplitudes()
+    del psi
+    sh = sd.LocalShards(n, 2)
+    sh.set_basis(M.initial_index(cfg, n))
+    sh.enable_p2p()
+    sh.plan(groups, order=1)
+    sh.evolve(dt, steps)
+    got = sh.amplitudes()
+    assert float(np.max(np.abs(got - want))) < 1e-12
+    assert abs(np.linalg.norm(got) - 1) < TOL_NORM
+
+
+@pytest.mark.skipif(os.environ.get("SDB_TEST_CONFIG5") != "1", reason="config 5 full size is opt-in (SDB_TEST_CONFIG5=1)")
+def test_config5_time_reversal_full_size(sd, port):
+    test_order1_time_reversal_full_size(5, 1, sd, port)

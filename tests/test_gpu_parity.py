@@ -141,6 +141,27 @@ def test_planner_modes_on_device(cfg, n, k, jit, env, sd, ref, port, monkeypatch
     assert abs(np.linalg.norm(got) - 1) < TOL_NORM
 
 
+@pytest.mark.parametrize("jit", ["0", "1"])
+@pytest.mark.parametrize("cfg,n", [(3, 16), (5, 16), (4, 17)])
+def test_many_tiles_per_cta(cfg, n, jit, sd, ref, port, monkeypatch):
+    """Few CTAs walking many tiles: warps of a CTA drift apart in programs
+    without a block barrier (lane swaps, CNOT-only passes), which in-place
+    stores through a CNOT map and table rebuilds must tolerate."""
+    monkeypatch.setenv("SDB_JIT", jit)
+    monkeypatch.setenv("SDB_MAX_CTAS", "2")
+    text = M.config_text(cfg, n=n)
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
+    order, dt = M.CONFIGS[cfg]["order"], M.CONFIGS[cfg]["dt"] * 5
+    psi0 = rand_state(n, 3)
+    s = sd.StateVector(n)
+    s.upload(psi0)
+    sd.TrotterPlan(s, groups, order=order, use_graph=False).evolve(dt, 2)
+    h, _, _ = ref.partition_text(text)
+    want, _ = ref.evolve_grouped(h, psi0, n, dt, 2, order)
+    ref.free(h)
+    assert np.max(np.abs(s.amplitudes() - want)) < TOL_AMP
+
+
 def test_unfused_reference_schedule_matches(sd, ref, port):
     n, cfg = 11, 3
     text = M.config_text(cfg, n=n)

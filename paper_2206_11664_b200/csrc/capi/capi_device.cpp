@@ -80,15 +80,14 @@ int resynth_cap(int k) {
     return k - sdb::fixed_bits_for(k);
 }
 
-// SDB_SPLIT_DIAG=1 splits diagonal ops per term, -1 picks whichever plans into
-// fewer passes; default whole diagonals (split passes carry more transposes
-// and phase stages per pass and measured slower, profiles/r1_notes.md).
+// SDB_SPLIT_DIAG=1 / 0 forces per-term / whole-group diagonal ops; by default
+// best_step_ops picks by its cost model.
 int split_diag_mode() {
     if (const char* e = std::getenv("SDB_SPLIT_DIAG")) {
         const int v = std::atoi(e);
         return v < 0 ? -1 : (v != 0 ? 1 : 0);
     }
-    return 0;
+    return -1;
 }
 
 // Step ops with or without CNOT resynthesis, whichever schedules into fewer
@@ -98,23 +97,40 @@ int split_diag_mode() {
 std::vector<sdb::Op> best_step_ops(const std::vector<sdb::GroupSpec>& gs, int n, int order, int k, int n_local) {
     std::vector<int> ident(n);
     std::iota(ident.begin(), ident.end(), 0);
-    auto cost = [&](const std::vector<sdb::Op>& o) {
+    const bool sharded = n_local < n;
+    // Cost in units of a whole-diagonal pass. Per-term-diagonal passes carry
+    // more transposes and phase stages (~1.8x a pass of the default plan at
+    // n=30, profiles/r1_notes.md); an exchange moves half a shard or more over
+    // NVLink (~2 passes). Sharded states take the plan with the fewest
+    // exchanges first (the north star's "at most one exchange per group").
+    struct Score {
+        int exchanges;
+        double cost;
+    };
+    auto score = [&](const std::vector<sdb::Op>& o, bool split) {
         const sdb::ShardedStep ss = sdb::plan_sharded_step(o, gs, n_local, k, sdb::fixed_bits_for(k), ident);
-        return ss.n_passes + 2 * ss.n_exchanges;
+        return Score{ss.n_exchanges, ss.n_passes * (split ? 1.8 : 1.0) + 2.0 * ss.n_exchanges};
+    };
+    auto better = [&](const Score& a, const Score& b) {
+        if (sharded && a.exchanges != b.exchanges) return a.exchanges < b.exchanges;
+        return a.cost < b.cost;
     };
     const int cap = resynth_cap(k);
     const int split_env = split_diag_mode();
     std::vector<sdb::Op> best;
-    int best_cost = 0;
+    Score best_score{0, 0.0};
     for (int split = 0; split < 2; ++split) {
         if ((split_env == 0 && split) || (split_env == 1 && !split)) continue;
+        // one GPU: per-term diagonals never paid off (config 1: 0.081 -> 0.162 ms,
+        // config 4: 92 -> 104 ms per step), so only sharded states consider them
+        if (split_env < 0 && split && !sharded) continue;
         for (int rs = 0; rs < 2; ++rs) {
             if (rs && cap == 0) continue;
             auto o = sdb::step_ops(gs, n, order, cx_split(k), rs ? cap : 0, split != 0);
-            const int c = cost(o);
-            if (best.empty() || c < best_cost) {
+            const Score sc = score(o, split != 0);
+            if (best.empty() || better(sc, best_score)) {
                 best = std::move(o);
-                best_cost = c;
+                best_score = sc;
             }
         }
     }

@@ -120,6 +120,58 @@ constexpr int kMaxFacBits = 8;
 // table is then rebuilt only when the tile's sign pattern changes, so the
 // caller allows it only when that happens a few times per CTA).
 constexpr int kMaxBigFacBits = 11;
+// Factors may share coordinates: each term only has to lie inside one of
+// them (the phase is the product of the factors' tables, every term counted in
+// the first factor that contains it). Greedy set growth over a few orders of
+// the term supports; empty result: no cover with <= 3 factors of <= 8 bits.
+std::vector<uint32_t> overlapping_cover(const std::vector<uint32_t>& us_in) {
+    std::vector<uint32_t> us;
+    for (uint32_t u : us_in)
+        if (u) us.push_back(u);
+    std::sort(us.begin(), us.end());
+    us.erase(std::unique(us.begin(), us.end()), us.end());
+    if (us.empty()) return {};
+    uint64_t rng = 0x9e3779b97f4a7c15ull;
+    for (int attempt = 0; attempt < 64; ++attempt) {
+        std::vector<uint32_t> ord = us;
+        if (attempt == 0) {
+            std::stable_sort(ord.begin(), ord.end(),
+                             [](uint32_t a, uint32_t b) { return std::popcount(a) > std::popcount(b); });
+        } else {
+            for (size_t i = ord.size(); i > 1; --i) {
+                rng ^= rng << 13;
+                rng ^= rng >> 7;
+                rng ^= rng << 17;
+                std::swap(ord[i - 1], ord[rng % i]);
+            }
+        }
+        std::vector<uint32_t> sets;
+        bool ok = true;
+        for (uint32_t u : ord) {
+            int best = -1, grow = 99;
+            for (size_t f = 0; f < sets.size(); ++f) {
+                const int g = std::popcount(u & ~sets[f]);
+                if (std::popcount(sets[f] | u) <= kMaxFacBits && g < grow) {
+                    grow = g;
+                    best = static_cast<int>(f);
+                }
+            }
+            if (best >= 0 && (grow == 0 || sets.size() == 3)) {
+                sets[best] |= u;
+            } else if (sets.size() < 3) {
+                sets.push_back(u);
+            } else if (best >= 0) {
+                sets[best] |= u;
+            } else {
+                ok = false;
+                break;
+            }
+        }
+        if (ok) return sets;
+    }
+    return {};
+}
+
 std::vector<uint32_t> factor_cover(const std::vector<uint32_t>& us, uint32_t tm, bool big_ok) {
     if (big_ok && std::popcount(tm) <= kMaxBigFacBits && std::popcount(tm) > kMaxFacBits) return {tm};
     std::vector<int> parent(32);
@@ -170,7 +222,7 @@ std::vector<uint32_t> factor_cover(const std::vector<uint32_t>& us, uint32_t tm,
         if (out.empty()) out.push_back(0);
         return out;
     }
-    return {};
+    return overlapping_cover(us);
 }
 
 }  // namespace

@@ -254,7 +254,7 @@ void clifford_unfused(sdb::StateImpl& s, const sdb::GroupSpec& g, bool inverse) 
 // terms per POINT stage above which a per-tile table is used (SDB_TABLE_THRESHOLD: experiments)
 const int kTableThreshold = [] {
     const char* e = std::getenv("SDB_TABLE_THRESHOLD");
-    return e ? std::atoi(e) : 8;
+    return e ? std::atoi(e) : 0;  // 0: the pass's largest phase stage always gets the table
 }();
 
 void upload_step(sd_plan& p, StepExec& E, const sdb::StepPlan& combined) {

@@ -705,13 +705,16 @@ struct PassCtx {
                 }
             }
         }
+        // q of every register combination, one add each
+        unsigned qs[NR];
+        qs[0] = q0;
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+#pragma unroll
+            for (int s = 0; s < (1 << j); ++s) qs[s + (1 << j)] = qs[s] + dq[j];
 #pragma unroll
         for (int s2 = 0; s2 < NR; ++s2) {
-            unsigned q = q0 + 2u * ((pc.qr >> s2) & 1u);
-#pragma unroll
-            for (int j = 0; j < R; ++j)
-                if ((s2 >> j) & 1) q += dq[j];
-            q &= 3u;
+            const unsigned q = (qs[s2] + 2u * ((pc.qr >> s2) & 1u)) & 3u;
             double2 a = v[s2];
             if (q & 2u) a = make_double2(-a.x, -a.y);
             if (q & 1u) a = make_double2(-a.y, a.x);

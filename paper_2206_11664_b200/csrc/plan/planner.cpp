@@ -427,6 +427,11 @@ int max_hadamard_depth() {
     return e ? std::atoi(e) : 0;
 }
 
+bool defer_fixed_hadamards() {
+    const char* e = std::getenv("SDB_DEFER_FIXED_H");
+    return e && std::atoi(e) != 0;
+}
+
 bool dram_pattern_heuristic() {
     const char* e = std::getenv("SDB_DRAM_PATTERN");
     return !e || std::atoi(e) != 0;
@@ -607,6 +612,7 @@ StepPlan plan_step(const std::vector<Op>& ops, const std::vector<GroupSpec>& gro
     }
     constexpr size_t kGoodLookahead = 64;
     const int max_depth = max_hadamard_depth();
+    const bool defer_fixed = defer_fixed_hadamards();
     while (first < N) {
         uint64_t L = fixed_logical;
         std::vector<int> sched;
@@ -626,7 +632,15 @@ StepPlan plan_step(const std::vector<Op>& ops, const std::vector<GroupSpec>& gro
             }
             return d + (o.kind == Op::H ? 1 : 0);
         };
-        auto depth_ok = [&](const Op& o) { return max_depth <= 0 || depth_of(o) <= max_depth; };
+        auto depth_ok = [&](const Op& o) {
+            if (max_depth > 0 && depth_of(o) > max_depth) return false;
+            // Hadamards on the always-local qubits are deferred out of a second
+            // WHT level: the next pass has them local anyway, and here they
+            // would cost two extra transposes (in and out of registers)
+            if ((defer_fixed || o.defer_deep) && o.kind == Op::H && (bitq(o.q) & fixed_logical) && depth_of(o) > 1)
+                return false;
+            return true;
+        };
         for (;;) {
             if (n_gates >= kMaxOpsPerPass || sched.size() >= kMaxDiagPerPass) break;
             long pick = -1;

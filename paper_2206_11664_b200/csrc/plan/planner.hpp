@@ -37,6 +37,7 @@ struct Op {
     int group = -1;          // DG: index into groups
     int t0 = 0, t1 = -1;     // DG: term range [t0, t1) of the group (t1 < 0: all terms)
     double dt_scale = 1.0;   // DG: multiplier of dt
+    bool defer_deep = false; // H on an always-local qubit: leave for the next pass rather than a 2nd WHT level
     uint64_t support = 0;    // qubits acted on (commutation checks)
     uint64_t need = 0;       // qubits that must be tile-local
 };

@@ -202,7 +202,8 @@ def cpu_reference(cfg: int, n_target: int, budget_s: float = 30.0):
                   f" scaled x2^{n_target - n_run} state size x {p_target:.0f}/{p_run:.0f} sweeps to n={n_target}")
     return {"value": 1.0 / t_target, "unit": "Trotter steps/s", "cores": threads, "kind": "reference",
             "sample": sample, "s_per_step": t_target,
-            "host": _host_desc(), "omp_threads": int(os.environ.get("OMP_NUM_THREADS", threads))}
+            "host": _host_desc(), "omp_threads": int(os.environ.get("OMP_NUM_THREADS", threads)),
+            "n_sample": n_run, "scale_to_target": t_target / t_run}
 
 
 def _host_desc():
@@ -223,11 +224,26 @@ def run_reference_arm(args, rank, world):
         return 0
     from paper_2206_11664_b200 import models as M
 
+    from oracle import oracle as O
+
     cfg, n = args.config, args.n
-    cb = cpu_reference(cfg, n, budget_s=args.ref_budget)
-    v = cb["value"]
+    K, W = max(1, args.steps), max(0, args.warmup)
+    # each step is one reference Trotter step at the largest n whose step fits
+    # the per-step budget (the whole K + W run stays within a few minutes),
+    # scaled to n by state size x sweeps; the sizing run counts as a warm-up
+    per_step = max(2.0, min(args.ref_budget, 180.0 / (K + W)))
+    cb = cpu_reference(cfg, n, budget_s=per_step)
+    ref = O.ref()
+    n_s = cb["n_sample"]
+    text = M.config_text(cfg, None if n_s == M.CONFIGS[cfg]["n"] else n_s)
+    for _ in range(W - 1):
+        ref_step_seconds(ref, text, n_s, cfg)
+    times = [ref_step_seconds(ref, text, n_s, cfg)[0] * cb["scale_to_target"] for _ in range(K)]
+    v = K / sum(times)
+    cb = dict(cb, value=v, s_per_step=sum(times) / K,
+              sample=cb["sample"] + f"; {K} timed samples after {W} warm-up")
     line = {
-        "metric": METRIC, "value": v, "unit": "Trotter steps/s", "n_gpus": world, "steps": 1, "warmup": 0,
+        "metric": METRIC, "value": v, "unit": "Trotter steps/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "c128 (f64 pairs)", "data": "synthetic (seeded generator, BASELINE config)",
         "config": {"workload": f"config{cfg}: {CONFIG_DESC[cfg]}", "n_qubits": n, "dt": M.CONFIGS[cfg]["dt"],

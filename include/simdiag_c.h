@@ -149,6 +149,10 @@ sd_status sd_state_set_random(sd_state* s, uint64_t seed);
  * equal the shard size. */
 sd_status sd_state_upload(sd_state* s, const double* re_im, uint64_t n_amps);
 sd_status sd_state_download(sd_state* s, double* re_im, uint64_t n_amps);
+/* Amplitudes [first, first + count) of this shard in logical order (the
+ * reference's StateVector::operator[] over a range, statevector.hpp:48-50) --
+ * partial readout of states larger than host memory allows at once. */
+sd_status sd_state_download_range(sd_state* s, uint64_t first, uint64_t count, double* re_im);
 /* save_raw / load_raw (statevector.cpp:383-401): raw little-endian (re, im)
  * doubles of this shard's index range in logical order (a relabelled layout is
  * canonicalised first, collectively for NCCL-attached shards); the rank files

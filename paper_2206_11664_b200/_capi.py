@@ -115,6 +115,7 @@ sd_state_set_plus = _sig("sd_state_set_plus", [P])
 sd_state_set_random = _sig("sd_state_set_random", [P, u64])
 sd_state_upload = _sig("sd_state_upload", [P, P, u64])
 sd_state_download = _sig("sd_state_download", [P, P, u64])
+sd_state_download_range = _sig("sd_state_download_range", [P, u64, u64, P])
 sd_state_norm_sq = _sig("sd_state_norm_sq", [P, C.POINTER(dbl)])
 sd_state_inner = _sig("sd_state_inner", [P, P, C.POINTER(dbl), C.POINTER(dbl)])
 sd_state_copy = _sig("sd_state_copy", [P, P])
@@ -178,7 +179,7 @@ EXPORTED = [
     "sd_groups_count", "sd_groups_destroy", "sd_group_get",
     "sd_state_create", "sd_state_create_shard", "sd_state_destroy", "sd_state_info",
     "sd_state_stream", "sd_state_device_ptr", "sd_sync", "sd_state_set_basis", "sd_state_set_plus",
-    "sd_state_set_random", "sd_state_upload", "sd_state_download", "sd_state_norm_sq",
+    "sd_state_set_random", "sd_state_upload", "sd_state_download", "sd_state_download_range", "sd_state_norm_sq",
     "sd_state_inner", "sd_state_copy", "sd_kernel_stats_get", "sd_kernel_stats_reset",
     "sd_apply_hadamard", "sd_apply_batched_cnot", "sd_apply_phase_layer", "sd_apply_diagonal_exp",
     "sd_apply_clifford", "sd_apply_clifford_inverse",

@@ -834,6 +834,25 @@ sd_status sd_state_download(sd_state* h, double* re_im, uint64_t n_amps) {
     });
 }
 
+sd_status sd_state_download_range(sd_state* h, uint64_t first, uint64_t count, double* re_im) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require(re_im != nullptr || count == 0, "null host buffer");
+        if (first > s.amps_count() || count > s.amps_count() - first)
+            throw std::out_of_range("download range outside the shard");
+        if (!is_identity(s.phys_of)) {
+            SDB_CUDA(cudaSetDevice(s.device));
+            if (s.world == 1) permute_local(s);
+            else if (s.nccl) canonicalize_nccl(s);
+            else throw std::runtime_error("sharded state is relabelled: call sd_local_canonicalize first");
+        }
+        if (count == 0) return;
+        SDB_CUDA(cudaSetDevice(s.device));
+        SDB_CUDA(cudaMemcpyAsync(re_im, s.amps + 2 * first, count * 16, cudaMemcpyDeviceToHost, s.stream));
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
 sd_status sd_state_norm_sq(sd_state* h, double* out) {
     return guard([&] {
         sdb::StateImpl& s = st(h);

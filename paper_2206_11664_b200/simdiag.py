@@ -359,9 +359,16 @@ class StateVector:
     def download_ptr(self, host_ptr: int, n_amps: int) -> None:
         check(A.sd_state_download(self._s, host_ptr, n_amps))
 
-    def amplitudes(self) -> np.ndarray:
-        out = np.empty(1 << self.n_local, np.complex128)
-        check(A.sd_state_download(self._s, out.ctypes.data, out.size))
+    def amplitudes(self, first: int = 0, count: Optional[int] = None) -> np.ndarray:
+        """This shard's amplitudes in logical order; `first`/`count` read a
+        range (operator[] over a slice) without staging the whole shard."""
+        if first == 0 and count is None:
+            out = np.empty(1 << self.n_local, np.complex128)
+            check(A.sd_state_download(self._s, out.ctypes.data, out.size))
+            return out
+        count = (1 << self.n_local) - first if count is None else count
+        out = np.empty(count, np.complex128)
+        check(A.sd_state_download_range(self._s, first, count, out.ctypes.data))
         return out
 
     def norm_sq_local(self) -> float:

@@ -74,3 +74,16 @@ def test_empty_hamiltonian_and_zero_steps(sd):
     groups = sd.partition_and_diagonalize(sd.Hamiltonian.load("1.0 XIIII\n"))
     sd.TrotterPlan(s, groups).evolve(0.1, 0)
     assert np.max(np.abs(s.amplitudes() - psi0)) == 0.0
+
+
+def test_download_range_matches_full_download(sd):
+    n = 12
+    rng = np.random.default_rng(5)
+    a = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    s = sd.StateVector(n)
+    s.upload(a / np.linalg.norm(a))
+    full = s.amplitudes()
+    for first, count in ((0, 1), (17, 100), (4000, 96), (0, 1 << n), (1 << n, 0)):
+        assert np.array_equal(s.amplitudes(first, count), full[first:first + count])
+    with pytest.raises(IndexError):
+        s.amplitudes(4000, 97)

@@ -103,6 +103,7 @@ PLANNER_MODES = [
     {"SDB_SPLIT_DIAG": "1", "SDB_CONSOLIDATE": "0"},
     {"SDB_DRAM_PATTERN": "0", "SDB_CX_RESYNTH": "0"},
     {"SDB_DEFER_FIXED_H": "1", "SDB_SPLIT_DIAG": "0"},
+    {"SDB_DRAM_PATTERN": "2"},
 ]
 
 

@@ -644,7 +644,15 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
         // A CNOT map still pending at the end is applied by the store's
         // addressing (no transpose) when the lanes stay coalesced.
         int store_perm_idx = -1;
-        if (loaded && !P.identity && !(cur & low3) && pp.store_sigma.empty()) {
+        // ... only when the map keeps coordinates 0..2 in place and out of every
+        // other image (each 8-lane group still writes one 128-byte line);
+        // otherwise the stores would scatter 16-byte pieces (config 5: 7.8 ms
+        // passes at n=28, 6x the pass roofline) and a transpose is cheaper
+        bool lanes_kept = true;
+        for (int j = 0; j < K; ++j)
+            lanes_kept &= ((low3 >> j) & 1u) ? P.col[j] == (1u << j) : (P.col[j] & low3) == 0u;
+        for (const auto& o : P.outer) lanes_kept &= (o.second & low3) == 0u;
+        if (loaded && !P.identity && !(cur & low3) && pp.store_sigma.empty() && lanes_kept) {
             store_perm_idx = make_perm();
             only_point = false;
         } else if (!P.identity || (cur & low3)) {

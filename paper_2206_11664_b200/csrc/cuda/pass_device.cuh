@@ -609,8 +609,8 @@ struct PassCtx {
         // S/CZ quadratic form of the tile (literals in specialised kernels;
         // n_lo < 0: read PointDev's pair lists at run time)
         int n_lo, n_oo;
-        uint32_t lo[16];     // (coord << 8) | outer physical bit
-        uint64_t oo[8];      // outer-outer pair masks
+        uint32_t lo[kMaxLitPairs];  // (local coordinate mask << 8) | outer physical bit
+        uint64_t oo[kMaxLitPairs];  // (1 << a) | outer partners of a above a
         uint32_t s1L, s2L;
         uint64_t s1H, s2H;
     };
@@ -648,22 +648,23 @@ struct PassCtx {
         // (QT is a quadratic form: QT(a^b) = QT(a) + QT(b) + B(a,b), B bilinear)
         uint32_t m2 = pc.s2L;
         unsigned q0 = __popcll(full & pc.s1H) + 2u * __popcll(full & pc.s2H);
+        auto oo_term = [&](uint64_t m) -> unsigned {
+            // 2 * bit_a * popc(full & partners(a)), a = lowest bit of m
+            return ((full & m & (~m + 1ull)) != 0ull) ? 2u * __popcll(full & (m & (m - 1ull))) : 0u;
+        };
         if (pc.n_lo >= 0) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (j < pc.n_lo && ((full >> (pc.lo[j] & 0xffu)) & 1ull)) m2 ^= 1u << (pc.lo[j] >> 8);
+            for (int j = 0; j < kMaxLitPairs; ++j)
+                if (j < pc.n_lo && ((full >> (pc.lo[j] & 0xffu)) & 1ull)) m2 ^= pc.lo[j] >> 8;
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (j < pc.n_oo && (full & pc.oo[j]) == pc.oo[j]) q0 += 2u;
+            for (int j = 0; j < kMaxLitPairs; ++j)
+                if (j < pc.n_oo) q0 += oo_term(pc.oo[j]);
         } else {
             for (int j = 0; j < pt.n_lo; ++j) {
                 const uint32_t wl = __ldg(plan.lo_pairs + pt.lo_off + j);
-                if ((full >> (wl & 0xffu)) & 1ull) m2 ^= 1u << (wl >> 8);
+                if ((full >> (wl & 0xffu)) & 1ull) m2 ^= wl >> 8;
             }
-            for (int j = 0; j < pt.n_oo; ++j) {
-                const uint64_t m = __ldg(plan.oo_pairs + pt.oo_off + j);
-                if ((full & m) == m) q0 += 2u;
-            }
+            for (int j = 0; j < pt.n_oo; ++j) q0 += oo_term(__ldg(plan.oo_pairs + pt.oo_off + j));
         }
         const uint32_t* qt = pt.qt_word >= 0 ? s_qt + 2 * pt.qt_word : nullptr;
         auto qtb = [&](uint32_t l) -> unsigned { return qt ? (qt[l >> 5] >> (l & 31u)) & 1u : 0u; };

@@ -468,15 +468,26 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                 std::vector<std::pair<int, int>> ll;
                 pt.lo_off = static_cast<int>(A.lo_pairs.size());
                 pt.oo_off = static_cast<int>(A.oo_pairs.size());
+                // Pairs with an outer qubit only depend on the tile: grouped by
+                // outer bit, a tile needs one test per outer bit instead of one
+                // per pair (config 5 groups carry ~180 CZs): local-outer pairs
+                // as (local mask << 8) | outer bit, outer-outer pairs as
+                // (1 << a) | mask of a's partners above a. CZ^2 = 1, so XOR.
+                std::vector<uint32_t> lo_by(64, 0);
+                std::vector<uint64_t> oo_by(64, 0);
                 for (uint64_t m : ps.cz_masks) {
                     const int a = std::countr_zero(m);
                     const int b = 63 - std::countl_zero(m);
                     const bool la = (Lphys >> a) & 1, lb = (Lphys >> b) & 1;
                     if (la && lb) ll.emplace_back(coord[a], coord[b]);
-                    else if (la) A.lo_pairs.push_back((uint32_t(coord[a]) << 8) | uint32_t(b));
-                    else if (lb) A.lo_pairs.push_back((uint32_t(coord[b]) << 8) | uint32_t(a));
-                    else A.oo_pairs.push_back(m);
+                    else if (la) lo_by[b] ^= 1u << coord[a];
+                    else if (lb) lo_by[a] ^= 1u << coord[b];
+                    else oo_by[a] ^= 1ull << b;
                 }
+                for (int b = 0; b < 64; ++b)
+                    if (lo_by[b]) A.lo_pairs.push_back((lo_by[b] << 8) | uint32_t(b));
+                for (int a = 0; a < 64; ++a)
+                    if (oo_by[a]) A.oo_pairs.push_back((1ull << a) | oo_by[a]);
                 pt.n_lo = static_cast<int>(A.lo_pairs.size()) - pt.lo_off;
                 pt.n_oo = static_cast<int>(A.oo_pairs.size()) - pt.oo_off;
                 if (!ll.empty()) {

@@ -41,6 +41,10 @@ namespace sdb {
 
 // kOpSwap: register slot (mask & 15) <-> lane bit (mask >> 4) by warp shuffles,
 // then the op's config (like kOpCfg, without shared memory).
+// Literal CZ-pair entries a specialised kernel carries per POINT (entries are
+// grouped by outer bit, so a shard of <= 24 outer bits always fits).
+constexpr int kMaxLitPairs = 24;
+
 enum MicroKind : int { kOpLoad = 0, kOpCfg = 1, kOpBfly = 2, kOpPoint = 3, kOpStore = 4, kOpSwap = 5 };
 
 struct MicroOpDev {

@@ -3,6 +3,7 @@
 #include <cuda_runtime_api.h>
 
 #include <algorithm>
+#include <chrono>
 #include <bit>
 #include <cmath>
 #include <cstdlib>
@@ -43,6 +44,7 @@ struct StepExec {
     cudaGraphExec_t graph = nullptr; // one captured step (small, launch-bound states)
     double graph_dt = std::nan("");
     std::string program;
+    bool relabel = false;  // unsharded: the last pass stores out of place into the plan's layout
 };
 
 struct sd_plan {
@@ -61,6 +63,7 @@ struct sd_plan {
     std::vector<int> ev_class;
     size_t ev_used = 0;
     int n_ref_sweeps = 0;
+    std::vector<int> layout;  // unsharded: physical layout the steps run in (empty: identity)
 };
 
 namespace {
@@ -158,10 +161,19 @@ void require_unsharded(const sdb::StateImpl& s) {
     if (s.world != 1) throw std::invalid_argument("single-sweep kernels need an unsharded state");
 }
 
-void require_identity_layout(const sdb::StateImpl& s) {
-    for (int q = 0; q < s.n; ++q) {
-        if (s.phys_of[q] != q) throw std::logic_error("state layout is relabelled");
-    }
+void permute_local(sdb::StateImpl& s);
+void permute_into_xbuf(sdb::StateImpl& s, const std::vector<int>& new_pos);
+
+// Kernels that address qubits directly need the logical layout: an unsharded
+// state evolved under a relabelled layout (plan layout search) is permuted
+// back first; a relabelled sharded state must be canonicalised collectively.
+void require_identity_layout(sdb::StateImpl& s) {
+    bool ident = true;
+    for (int q = 0; q < s.n; ++q) ident &= s.phys_of[q] == q;
+    if (ident) return;
+    if (s.world != 1) throw std::logic_error("state layout is relabelled");
+    SDB_CUDA(cudaSetDevice(s.device));
+    permute_local(s);
 }
 
 void bump(sdb::StateImpl& s, uint64_t reads, uint64_t writes) {
@@ -339,6 +351,15 @@ StepExec& step_for(sd_plan& p, const std::vector<int>& layout) {
     sdb::StateImpl& s = p.state->impl;
     auto E = std::make_unique<StepExec>();
     E->ss = sdb::plan_sharded_step(p.ops, p.groups, s.n_local, p.k, sdb::fixed_bits_for(p.k), layout);
+    if (!p.layout.empty() && s.world == 1 && layout != p.layout && !E->ss.segs.empty() &&
+        !E->ss.segs.back().plan.passes.empty() && E->ss.segs.back().plan.passes.back().store_sigma.empty()) {
+        // physical bit layout[q] -> p.layout[q] in the step's last store
+        std::vector<int> sigma(s.n_local);
+        for (int q = 0; q < s.n_local; ++q) sigma[layout[q]] = p.layout[q];
+        E->ss.segs.back().plan.passes.back().store_sigma = sigma;
+        E->ss.phys_out = p.layout;
+        E->relabel = true;
+    }
     sdb::StepPlan combined;
     combined.tile_qubits = p.k;
     for (const sdb::Segment& sg : E->ss.segs) {
@@ -347,7 +368,7 @@ StepExec& step_for(sd_plan& p, const std::vector<int>& layout) {
         for (const sdb::PassPlan& pp : sg.plan.passes) combined.passes.push_back(pp);
     }
     upload_step(p, *E, combined);
-    if (E->ss.n_exchanges > 0 && !s.xbuf) {
+    if ((E->ss.n_exchanges > 0 || E->relabel) && !s.xbuf) {
         SDB_CUDA(cudaSetDevice(s.device));
         cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&s.xbuf), 16 * s.amps_count());
         if (e != cudaSuccess) {
@@ -361,6 +382,73 @@ StepExec& step_for(sd_plan& p, const std::vector<int>& layout) {
     return ref;
 }
 
+// HBM streaming cost of a pass by its local physical bits (tools/membench3,
+// profiles/r1_membench3_n30.txt): bit 3 or 5 local ~1.0, else bits 4 or
+// 6..10 ~1.25, else ~1.45 (relative to a pass with a good pattern).
+double pattern_cost(const std::vector<int>& lpos) {
+    bool good = false, medium = false;
+    for (int b : lpos) {
+        good |= b == 3 || b == 5;
+        medium |= b == 4 || (b >= 6 && b <= 10);
+    }
+    return good ? 1.0 : medium ? 1.25 : 1.45;
+}
+
+double layout_cost(const sd_plan& p, const std::vector<int>& layout) {
+    const sdb::StateImpl& s = p.state->impl;
+    const sdb::ShardedStep ss = sdb::plan_sharded_step(p.ops, p.groups, s.n_local, p.k, sdb::fixed_bits_for(p.k), layout);
+    double c = 0.0;
+    for (const sdb::Segment& sg : ss.segs)
+        for (const sdb::PassPlan& pp : sg.plan.passes) c += pattern_cost(pp.lpos);
+    return c;
+}
+
+// Unsharded states of >= 22 qubits may run their steps in a relabelled qubit
+// layout: a step that starts elsewhere (after an upload) stores its last pass
+// out of place through the relabelling (no extra pass; needs the second buffer),
+// and readout permutes back.
+// A time-boxed random search over layouts, scored by pass count weighted with
+// each pass's HBM pattern cost; kept only if it beats the identity by 2%.
+void choose_layout(sd_plan& p) {
+    sdb::StateImpl& s = p.state->impl;
+    if (const char* e = std::getenv("SDB_LAYOUT_SEARCH"); e && std::atoi(e) == 0) return;
+    if (s.world != 1 || s.n_local < 22 || !p.opts.fuse || p.opts.use_graph > 0) return;
+    size_t free_b = 0, total_b = 0;
+    SDB_CUDA(cudaSetDevice(s.device));
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    if (!s.xbuf && free_b < 16 * s.amps_count() + (size_t(4) << 30)) return;
+    const int n = s.n;
+    std::vector<int> ident(n);
+    std::iota(ident.begin(), ident.end(), 0);
+    const double base = layout_cost(p, ident);
+    double best = base;
+    std::vector<int> best_l;
+    uint64_t rng = 0x243f6a8885a308d3ull;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int trial = 0; trial < 4096; ++trial) {
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(1500)) break;
+        std::vector<int> cand = best_l.empty() ? ident : best_l;
+        // a few random transpositions away from the best layout so far
+        const int moves = 1 + static_cast<int>(rng % 3);
+        for (int m = 0; m < moves; ++m) {
+            rng ^= rng << 13;
+            rng ^= rng >> 7;
+            rng ^= rng << 17;
+            const int a = static_cast<int>(rng % n), b = static_cast<int>((rng >> 20) % n);
+            std::swap(cand[a], cand[b]);
+        }
+        const double c = layout_cost(p, cand);
+        if (c < best) {
+            best = c;
+            best_l = cand;
+        }
+    }
+    if (!best_l.empty() && best < 0.98 * base) p.layout = best_l;
+}
+
 void plan_build(sd_plan& p) {
     sdb::StateImpl& s = p.state->impl;
     const int order = p.opts.order;
@@ -370,9 +458,10 @@ void plan_build(sd_plan& p) {
     int k = p.opts.tile_qubits > 0 ? p.opts.tile_qubits : 12;
     p.k = std::min({k, sdb::max_tile_qubits(), s.n_local});
     p.ops = best_step_ops(p.groups, s.n, order, p.k, s.n_local);
+    choose_layout(p);
     std::vector<int> ident(s.n);
     std::iota(ident.begin(), ident.end(), 0);
-    p.first = &step_for(p, ident);
+    p.first = &step_for(p, p.layout.empty() ? ident : p.layout);
 }
 
 void record_start(sd_plan& p, int cls) {
@@ -454,7 +543,7 @@ void run_segment(sd_plan& p, StepExec& E, size_t seg, double dt) {
     }();
     for (int i = first; i < first + count; ++i) {
         if (debug_passes >= 0 && i >= debug_passes) break;
-        const bool to_buf = exch && i == first + count - 1;
+        const bool to_buf = (exch || (E.relabel && seg + 1 == E.ss.segs.size())) && i == first + count - 1;
         // fused exchange: the pass stores straight into the peers' receive buffers
         double2* const* xdst = nullptr;
         if (to_buf && s.p2p) {
@@ -491,6 +580,10 @@ void run_step_fused(sd_plan& p, double dt) {
             sdb::exchange_nccl(s, E.ss.segs[seg].ex);
             record_end(p, xb);
         }
+    }
+    if (E.relabel) {
+        std::swap(s.amps, s.xbuf);
+        s.parity ^= 1;
     }
     s.phys_of = E.ss.phys_out;
 }

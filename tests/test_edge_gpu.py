@@ -87,3 +87,33 @@ def test_download_range_matches_full_download(sd):
         assert np.array_equal(s.amplitudes(first, count), full[first:first + count])
     with pytest.raises(IndexError):
         s.amplitudes(4000, 97)
+
+
+def test_relabelled_layout_is_transparent(sd, ref):
+    """States of >= 22 qubits may run their steps in a relabelled layout (plan
+    layout search); readout, direct kernels and a second plan must not see it."""
+    from paper_2206_11664_b200 import models as M
+    n, cfg = 22, 4
+    text = M.config_text(cfg, n=n)
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
+    rng = np.random.default_rng(11)
+    a = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    a /= np.linalg.norm(a)
+    s = sd.StateVector(n)
+    s.upload(a)
+    dt = 0.02
+    sd.TrotterPlan(s, groups, order=1).evolve(dt, 2)
+    s.apply_hadamard(3)                                        # direct kernel after a relabelled step
+    sd.TrotterPlan(s, list(reversed(groups)), order=1).evolve(dt, 1)
+    got = s.amplitudes()
+    h, _, _ = ref.partition_text(text)
+    want, _ = ref.evolve_grouped(h, a, n, dt, 2, 1)
+    want = ref.kernel(0, want, n, a=3)
+    ref.free(h)
+    # the reversed-order plan: groups applied in reverse order
+    g2 = list(reversed(groups))
+    s2 = sd.StateVector(n)
+    s2.upload(want)
+    sd.TrotterPlan(s2, g2, order=1, use_graph=False).evolve(dt, 1)
+    assert np.max(np.abs(got - s2.amplitudes())) < 1e-12
+    assert abs(np.linalg.norm(got) - 1) < 1e-12

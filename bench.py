@@ -349,12 +349,17 @@ def run_ours(args, rank, world, local_rank):
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record(stream)
+        fu = torch.cuda.Event(enable_timing=True)
+        fe = torch.cuda.Event(enable_timing=True)
         psi.upload_ptr(host.data_ptr(), 1 << psi.n_local)       # H2D of the step inputs
+        fu.record(stream)
         plan.evolve(dt, args.steps, wait=False)
+        fe.record(stream)
         psi.download_ptr(host.data_ptr(), 1 << psi.n_local)     # D2H of the result
         f1.record(stream)
         f1.synchronize()
         e2e_ms = f0.elapsed_time(f1)
+        split_ms = {"h2d_ms": f0.elapsed_time(fu), "steps_ms": fu.elapsed_time(fe), "d2h_ms": fe.elapsed_time(f1)}
         bytes_state = 16 * (1 << psi.n_local)
         if world > 1:
             import torch.distributed as dist
@@ -364,7 +369,7 @@ def run_ours(args, rank, world, local_rank):
         e2e = {"value": args.steps * 1000.0 / e2e_ms, "unit": "Trotter steps/s",
                "h2d_bytes_per_step": bytes_state / args.steps, "d2h_bytes_per_step": bytes_state / args.steps,
                "api": "StateVector.upload -> TrotterPlan.evolve(K steps) -> download (sd_state_upload/sd_evolve/sd_state_download)",
-               "trotter_steps_per_call": args.steps}
+               "trotter_steps_per_call": args.steps, "rank0_split": split_ms}
         del host
 
     peak, peak_src = load_peaks()

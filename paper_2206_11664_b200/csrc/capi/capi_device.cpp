@@ -3,7 +3,6 @@
 #include <cuda_runtime_api.h>
 
 #include <algorithm>
-#include <chrono>
 #include <bit>
 #include <cmath>
 #include <cstdlib>
@@ -406,9 +405,9 @@ double layout_cost(const sd_plan& p, const std::vector<int>& layout) {
 // Unsharded states of >= 22 qubits may run their steps in a relabelled qubit
 // layout: a step that starts elsewhere (after an upload) stores its last pass
 // out of place through the relabelling (no extra pass; needs the second buffer),
-// and readout permutes back.
-// A time-boxed random search over layouts, scored by pass count weighted with
-// each pass's HBM pattern cost; kept only if it beats the identity by 2%.
+// and readout permutes back. Random search (a few transpositions from the best
+// so far) with a trial budget set by the plan size, scored by pass count
+// weighted with each pass's HBM pattern; kept only if it beats the identity by 2%.
 void choose_layout(sd_plan& p) {
     sdb::StateImpl& s = p.state->impl;
     if (const char* e = std::getenv("SDB_LAYOUT_SEARCH"); e && std::atoi(e) == 0) return;
@@ -427,9 +426,9 @@ void choose_layout(sd_plan& p) {
     double best = base;
     std::vector<int> best_l;
     uint64_t rng = 0x243f6a8885a308d3ull;
-    const auto t0 = std::chrono::steady_clock::now();
-    for (int trial = 0; trial < 4096; ++trial) {
-        if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(1500)) break;
+    // deterministic budget by plan size (~1 s of planning for config 4's 13 passes)
+    const int trials = std::clamp(5200 / std::max(1, static_cast<int>(base)), 0, 400);
+    for (int trial = 0; trial < trials; ++trial) {
         std::vector<int> cand = best_l.empty() ? ident : best_l;
         // a few random transpositions away from the best layout so far
         const int moves = 1 + static_cast<int>(rng % 3);

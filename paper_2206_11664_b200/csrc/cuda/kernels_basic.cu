@@ -240,13 +240,16 @@ __global__ void k_diag_exp(double2* __restrict__ a, uint64_t n, const uint64_t* 
 
 // Physical bit permutation dst[pi(i)] = src[i] with bit j of i moved to
 // bit new_pos[j] (used to restore logical order on download).
+// Gather form (dst bit c comes from src bit src_of[c]): the writes stay
+// coalesced and scattered reads only waste sector bandwidth, where scattered
+// 16-byte writes would force partial-sector merges.
 __global__ void k_permute_bits(const double2* __restrict__ src, double2* __restrict__ dst,
-                               uint64_t n, const int* __restrict__ new_pos, int n_bits) {
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-        uint64_t j = 0;
-        for (int b = 0; b < n_bits; ++b) j |= ((i >> b) & 1ull) << __ldg(new_pos + b);
-        dst[j] = src[i];
+                               uint64_t n, const int* __restrict__ src_of, int n_bits) {
+    for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < n;
+         j += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t i = 0;
+        for (int c = 0; c < n_bits; ++c) i |= ((j >> c) & 1ull) << __ldg(src_of + c);
+        dst[j] = __ldcs(src + i);
     }
 }
 
@@ -419,7 +422,8 @@ void device_expectation_term(StateImpl& s, uint64_t x, uint64_t z, double* re, d
 
 void launch_permute_bits(StateImpl& s, const double* src, double* dst, const int* new_pos_host,
                          int n_bits) {
-    std::vector<int> pos(new_pos_host, new_pos_host + n_bits);
+    std::vector<int> pos(n_bits);
+    for (int b = 0; b < n_bits; ++b) pos[new_pos_host[b]] = b;  // inverse: source bit of each target bit
     int* dpos = upload_scratch(pos, s.stream);
     const uint64_t n = uint64_t(1) << n_bits;
     k_permute_bits<<<grid_for(n), kThreads, 0, s.stream>>>(reinterpret_cast<const double2*>(src),

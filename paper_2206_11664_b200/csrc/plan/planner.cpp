@@ -162,8 +162,10 @@ std::vector<std::pair<int, int>> resynth_cnots(const std::vector<std::pair<int, 
         for (int c = 0; c < nt; ++c) {
             if (!((att[c] >> c) & 1)) {
                 int piv = -1;
-                for (int r = 0; r < nt; ++r)
-                    if (r != c && ((att[r] >> c) & 1) && (r > c || !((att[r] >> r) & 1) || true)) {
+                // rows above c are already unit in columns < c; an invertible
+                // block always has a pivot below
+                for (int r = c + 1; r < nt; ++r)
+                    if ((att[r] >> c) & 1) {
                         piv = r;
                         break;
                     }

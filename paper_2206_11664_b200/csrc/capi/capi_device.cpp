@@ -344,19 +344,25 @@ void upload_step(sd_plan& p, StepExec& E, const sdb::StepPlan& combined) {
     E.host_passes = std::move(A.passes);
 }
 
-StepExec& step_for(sd_plan& p, const std::vector<int>& layout) {
-    auto it = p.steps.find(layout);
-    if (it != p.steps.end()) return *it->second;
+// The step plan starting in `layout`. `end` (unsharded only): the layout the
+// step must leave the state in; a different one is reached by storing the
+// step's last pass out of place through the relabelling (no extra pass).
+StepExec& step_for(sd_plan& p, const std::vector<int>& layout, const std::vector<int>* end = nullptr) {
     sdb::StateImpl& s = p.state->impl;
+    const bool relabel = end && s.world == 1 && *end != layout;
+    std::vector<int> key = layout;
+    if (relabel) key.insert(key.end(), end->begin(), end->end());
+    auto it = p.steps.find(key);
+    if (it != p.steps.end()) return *it->second;
     auto E = std::make_unique<StepExec>();
     E->ss = sdb::plan_sharded_step(p.ops, p.groups, s.n_local, p.k, sdb::fixed_bits_for(p.k), layout);
-    if (!p.layout.empty() && s.world == 1 && layout != p.layout && !E->ss.segs.empty() &&
-        !E->ss.segs.back().plan.passes.empty() && E->ss.segs.back().plan.passes.back().store_sigma.empty()) {
-        // physical bit layout[q] -> p.layout[q] in the step's last store
+    if (relabel && !E->ss.segs.empty() && !E->ss.segs.back().plan.passes.empty() &&
+        E->ss.segs.back().plan.passes.back().store_sigma.empty()) {
+        // physical bit layout[q] -> end[q] in the step's last store
         std::vector<int> sigma(s.n_local);
-        for (int q = 0; q < s.n_local; ++q) sigma[layout[q]] = p.layout[q];
+        for (int q = 0; q < s.n_local; ++q) sigma[layout[q]] = (*end)[q];
         E->ss.segs.back().plan.passes.back().store_sigma = sigma;
-        E->ss.phys_out = p.layout;
+        E->ss.phys_out = *end;
         E->relabel = true;
     }
     sdb::StepPlan combined;
@@ -377,7 +383,7 @@ StepExec& step_for(sd_plan& p, const std::vector<int>& layout) {
         s.xbuf_amps = s.amps_count();
     }
     StepExec& ref = *E;
-    p.steps.emplace(layout, std::move(E));
+    p.steps.emplace(key, std::move(E));
     return ref;
 }
 
@@ -403,9 +409,10 @@ double layout_cost(const sd_plan& p, const std::vector<int>& layout) {
 }
 
 // Unsharded states of >= 22 qubits may run their steps in a relabelled qubit
-// layout: a step that starts elsewhere (after an upload) stores its last pass
-// out of place through the relabelling (no extra pass; needs the second buffer),
-// and readout permutes back. Random search (a few transpositions from the best
+// layout: each evolve call enters it inside its first step and leaves it inside
+// its last (the steps' final stores run out of place through the relabelling,
+// no extra pass; needs the second buffer), so states stay in logical order
+// between calls. Random search (a few transpositions from the best
 // so far) with a trial budget set by the plan size, scored by pass count
 // weighted with each pass's HBM pattern; kept only if it beats the identity by 2%.
 void choose_layout(sd_plan& p) {
@@ -562,9 +569,9 @@ void run_segment(sd_plan& p, StepExec& E, size_t seg, double dt) {
     }
 }
 
-void run_step_fused(sd_plan& p, double dt) {
+void run_step_fused(sd_plan& p, double dt, const std::vector<int>* end = nullptr) {
     sdb::StateImpl& s = p.state->impl;
-    StepExec& E = step_for(p, s.phys_of);
+    StepExec& E = step_for(p, s.phys_of, end);
     for (size_t seg = 0; seg < E.ss.segs.size(); ++seg) {
         run_segment(p, E, seg, dt);
         if (E.ss.segs[seg].exchange_after) {
@@ -641,10 +648,15 @@ void evolve(sd_plan& p, double dt, int n_steps, bool wait) {
     sdb::StateImpl& s = p.state->impl;
     SDB_CUDA(cudaSetDevice(s.device));
     const bool graphs = graph_mode(p);
+    // A relabelled plan layout is entered inside the call's first step and left
+    // inside its last one: the state is in logical order between calls.
+    const bool relayout = !p.layout.empty() && s.world == 1 && p.opts.fuse && !graphs;
+    std::vector<int> ident(s.n);
+    std::iota(ident.begin(), ident.end(), 0);
     for (int step = 0; step < n_steps; ++step) {
         if (!p.opts.fuse) run_step_unfused(p, dt);
         else if (graphs) run_step_graph(p, dt);
-        else run_step_fused(p, dt);
+        else run_step_fused(p, dt, relayout ? (step + 1 == n_steps ? &ident : &p.layout) : nullptr);
     }
     if (wait) SDB_CUDA(cudaStreamSynchronize(s.stream));
     harvest(p);
@@ -1129,7 +1141,7 @@ sd_status sd_plan_get_info(const sd_plan* p, sd_plan_info* o) {
         if (p->opts.fuse) {
             // steady state: the plan of the current layout (identity until the first exchange)
             auto it = p->steps.find(s.phys_of);
-            const StepExec* E = it != p->steps.end() ? it->second.get() : p->first;
+            const StepExec* E = it != p->steps.end() && p->layout.empty() ? it->second.get() : p->first;
             o->n_passes_per_step = E->ss.n_passes;
             o->n_exchanges_per_step = E->ss.n_exchanges;
             o->tile_qubits = p->k;

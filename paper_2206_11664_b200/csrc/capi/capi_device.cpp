@@ -403,8 +403,18 @@ double layout_cost(const sd_plan& p, const std::vector<int>& layout) {
     const sdb::StateImpl& s = p.state->impl;
     const sdb::ShardedStep ss = sdb::plan_sharded_step(p.ops, p.groups, s.n_local, p.k, sdb::fixed_bits_for(p.k), layout);
     double c = 0.0;
+    static const double w2 = [] {
+        const char* e = std::getenv("SDB_LAYOUT_W2");
+        return e ? std::atof(e) : 1.0;
+    }();
     for (const sdb::Segment& sg : ss.segs)
-        for (const sdb::PassPlan& pp : sg.plan.passes) c += pattern_cost(pp.lpos);
+        for (const sdb::PassPlan& pp : sg.plan.passes) {
+            int wht = 0;
+            for (const sdb::PassStage& st : pp.stages) wht += st.kind == sdb::PassStage::WHT;
+            // passes with two Hadamard stages take ~1.35x a single-stage pass
+            const double base = wht >= 2 ? 1.35 : 1.0;
+            c += base * (1.0 + (wht >= 2 ? w2 : 1.0) * (pattern_cost(pp.lpos) - 1.0));
+        }
     return c;
 }
 

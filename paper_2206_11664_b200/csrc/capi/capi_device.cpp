@@ -279,6 +279,7 @@ void upload_step(sd_plan& p, StepExec& E, const sdb::StepPlan& combined) {
     int rbits = 4;
     if (const char* e = std::getenv("SDB_RBITS"); e && jit) rbits = std::atoi(e) == 3 ? 3 : 4;
     sdb::HostPlanArrays A = sdb::lower_plan(combined, s.n_local, kTableThreshold, rbits);
+    sdb::verify_lowering(A);  // register-config bookkeeping of lane swaps (host check, cheap)
     E.pass_class = A.pass_class;
     E.program = sdb::describe_program(A);
     E.jit_fn.assign(A.passes.size(), nullptr);

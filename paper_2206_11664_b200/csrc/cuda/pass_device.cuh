@@ -608,6 +608,8 @@ struct PassCtx {
         int coffE[3];        // factor tables: double offsets in the table region
         // S/CZ quadratic form of the tile (literals in specialised kernels;
         // n_lo < 0: read PointDev's pair lists at run time)
+        int quarter;         // 0: the point has no S/CZ quarter turns at all
+        int tph;             // the pass multiplies by a per-tile constant phase here (MODE 4)
         int n_lo, n_oo;
         uint32_t lo[kMaxLitPairs];  // (local coordinate mask << 8) | outer physical bit
         uint64_t oo[kMaxLitPairs];  // (1 << a) | outer partners of a above a
@@ -629,6 +631,9 @@ struct PassCtx {
         }
         c.n_lo = -1;
         c.n_oo = 0;
+        c.quarter = (pt.s1L | pt.s2L) != 0u || (pt.s1H | pt.s2H) != 0ull || pt.n_lo > 0 || pt.n_oo > 0 ||
+                    pt.qt_word >= 0;
+        c.tph = P.tphase_off >= 0;
         c.s1L = pt.s1L;
         c.s2L = pt.s2L;
         c.s1H = pt.s1H;
@@ -647,11 +652,14 @@ struct PassCtx {
         // ---- quarter turns: q(tb ^ r_s) = q0 + sum_{j in s} dq_j + 2 QT(r_s)  (mod 4)
         // (QT is a quadratic form: QT(a^b) = QT(a) + QT(b) + B(a,b), B bilinear)
         uint32_t m2 = pc.s2L;
-        unsigned q0 = __popcll(full & pc.s1H) + 2u * __popcll(full & pc.s2H);
+        unsigned q0 = 0;
+        unsigned dq[4] = {0u, 0u, 0u, 0u};
         auto oo_term = [&](uint64_t m) -> unsigned {
             // 2 * bit_a * popc(full & partners(a)), a = lowest bit of m
             return ((full & m & (~m + 1ull)) != 0ull) ? 2u * __popcll(full & (m & (m - 1ull))) : 0u;
         };
+        if (pc.quarter) {
+        q0 = __popcll(full & pc.s1H) + 2u * __popcll(full & pc.s2H);
         if (pc.n_lo >= 0) {
 #pragma unroll
             for (int j = 0; j < kMaxLitPairs; ++j)
@@ -670,19 +678,19 @@ struct PassCtx {
         auto qtb = [&](uint32_t l) -> unsigned { return qt ? (qt[l >> 5] >> (l & 31u)) & 1u : 0u; };
         const unsigned qt_tb = qtb(rc.tb);
         q0 += __popc(rc.tb & pc.s1L) + 2u * (__popc(rc.tb & m2) + qt_tb);
-        unsigned dq[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const unsigned bil = qt ? (qtb(rc.tb ^ cb[j]) ^ qt_tb ^ qtb(cb[j])) : 0u;
             dq[j] = __popc(cb[j] & pc.s1L) + 2u * (__popc(cb[j] & m2) + bil);
         }
+        }  // pc.quarter
         // ---- table slots of this thread's registers (compact index, swizzle linear)
         uint32_t ts0 = 0, fb[3] = {0, 0, 0};
         const double2* E[3] = {nullptr, nullptr, nullptr};
         if constexpr (MODE == 3) ts0 = s_pl[rc.tb & 63u] ^ s_ph[rc.tb >> 6];
         double2 tph = make_double2(1.0, 0.0);
         if constexpr (MODE == 4) {
-            if (P.tphase_off >= 0) tph = plan.tile_phase[P.tphase_off + t];
+            if (pc.tph) tph = plan.tile_phase[P.tphase_off + t];
             const double* tb_ = tabc();
 #pragma unroll
             for (int f = 0; f < NFAC; ++f) {
@@ -715,12 +723,14 @@ struct PassCtx {
             for (int s = 0; s < (1 << j); ++s) qs[s + (1 << j)] = qs[s] + dq[j];
 #pragma unroll
         for (int s2 = 0; s2 < NR; ++s2) {
-            const unsigned q = (qs[s2] + 2u * ((pc.qr >> s2) & 1u)) & 3u;
             double2 a = v[s2];
-            if (q & 2u) a = make_double2(-a.x, -a.y);
-            if (q & 1u) a = make_double2(-a.y, a.x);
+            if (pc.quarter) {
+                const unsigned q = (qs[s2] + 2u * ((pc.qr >> s2) & 1u)) & 3u;
+                if (q & 2u) a = make_double2(-a.x, -a.y);
+                if (q & 1u) a = make_double2(-a.y, a.x);
+            }
             if constexpr (MODE == 4) {
-                if (P.tphase_off >= 0) a = make_double2(a.x * tph.x - a.y * tph.y, a.x * tph.y + a.y * tph.x);
+                if (pc.tph) a = make_double2(a.x * tph.x - a.y * tph.y, a.x * tph.y + a.y * tph.x);
                 double2 e;
 #pragma unroll
                 for (int f = 0; f < NFAC; ++f) {

@@ -40,6 +40,14 @@ __device__ __forceinline__ uint32_t pext32(uint32_t v, uint32_t mask) {
     return out;
 }
 
+// Cache hints of the tile loads/stores (timing experiments may override).
+#ifndef SDB_TILE_LOAD
+#define SDB_TILE_LOAD __ldcs
+#endif
+#ifndef SDB_TILE_STORE
+#define SDB_TILE_STORE __stcs
+#endif
+
 __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
@@ -510,7 +518,7 @@ struct PassCtx {
         uint64_t o[NR];
         phys_offsets(o);
 #pragma unroll
-        for (int s = 0; s < NR; ++s) v[s] = __ldcs(g + o[s]);
+        for (int s = 0; s < NR; ++s) v[s] = SDB_TILE_LOAD(g + o[s]);
         // Pull this CTA's next tile into L2 while the current one is
         // transformed: HBM keeps streaming through the compute phase
         // without holding registers or shared memory.
@@ -855,10 +863,10 @@ struct PassCtx {
         }
         if (sc) {
 #pragma unroll
-            for (int s = 0; s < NR; ++s) __stcs(go + o[s], make_double2(v[s].x * scale, v[s].y * scale));
+            for (int s = 0; s < NR; ++s) SDB_TILE_STORE(go + o[s], make_double2(v[s].x * scale, v[s].y * scale));
         } else {
 #pragma unroll
-            for (int s = 0; s < NR; ++s) __stcs(go + o[s], v[s]);
+            for (int s = 0; s < NR; ++s) SDB_TILE_STORE(go + o[s], v[s]);
         }
     }
 };

@@ -137,73 +137,69 @@ def init_state(psi, cfg: int, n: int, rank: int):
 
 # ------------------------------------------------------- CPU reference
 
-def ref_step_seconds(ref, text, n, cfg, steps=1):
-    """Wall time of `steps` reference Trotter steps (oracle/_ref) at n."""
-    import numpy as np
-    from paper_2206_11664_b200 import models as M
+def load_models():
+    """paper_2206_11664_b200/models.py loaded by path: the reference arm must
+    not import the product package (which maps libsimdiag_b200.so)."""
+    import importlib.util
 
-    h, nn, _ = ref.partition_text(text, synthesize=True)
+    if "sdb_models_standalone" in sys.modules:
+        return sys.modules["sdb_models_standalone"]
+    spec = importlib.util.spec_from_file_location(
+        "sdb_models_standalone", os.path.join(ROOT, "paper_2206_11664_b200", "models.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules["sdb_models_standalone"] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def host_threads() -> int:
     try:
-        psi = np.zeros(1 << n, np.complex128)
-        init = M.CONFIGS[cfg]["init"]
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+class RefRun:
+    """The reference's own CPU path (oracle/_ref: proj/src compiled from its
+    sources; evolve_grouped's loop proj/src/evolve.cpp:47-58 in the shim) on a
+    persistent reference StateVector at the workload's full size, with every
+    host thread. Timings cover the Trotter steps only."""
+
+    def __init__(self, cfg: int, n: int):
+        from oracle import oracle as O
+
+        M = load_models()
+        self.M, self.cfg, self.n = M, cfg, n
+        self.ref = O.ref()
+        self.threads = host_threads()
+        self.ref.lib.ref_set_threads(self.threads)
+        text = M.config_text(cfg, None if n == M.CONFIGS[cfg]["n"] else n)
+        self.h, nn, _ = self.ref.partition_text(text, synthesize=True)
+        self.dt, self.order = M.CONFIGS[cfg]["dt"], M.CONFIGS[cfg]["order"]
+        self.st = O.RefState(self.ref, n)
+        self.reset()
+
+    def reset(self):
+        init = self.M.CONFIGS[self.cfg]["init"]
+        n = self.n
         if init[0] == "basis":
-            psi[M.initial_index(cfg, n)] = 1.0
+            self.st.set_basis(self.M.initial_index(self.cfg, n))
         elif init[0] == "plus":
-            psi[:] = 1.0 / math.sqrt(1 << n)
+            import numpy as np
+            c = 1 << min(n, 24)
+            for f in range(0, 1 << n, c):
+                self.st.write(f, np.full(c, 1.0 / math.sqrt(1 << n), np.complex128))
         else:
-            psi = ref.random_state(n, init[1])
+            self.st.write(0, self.ref.random_state(n, init[1]))
+
+    def step(self) -> float:
         t0 = time.perf_counter()
-        out, stats = ref.evolve_grouped(h, psi, n, M.CONFIGS[cfg]["dt"], steps, M.CONFIGS[cfg]["order"])
-        dt = time.perf_counter() - t0
-        return dt / steps, stats
-    finally:
-        ref.free(h)
+        self.st.evolve(self.h, self.dt, 1, self.order)
+        return time.perf_counter() - t0
 
-
-def cpu_reference(cfg: int, n_target: int, budget_s: float = 30.0):
-    """Reference CPU steps/s at n_target, measured on the largest n whose
-    single step fits ~budget_s, scaled to n_target by state size x sweeps
-    (the reference's step cost is linear in both)."""
-    from oracle import oracle as O
-    from paper_2206_11664_b200 import models as M
-
-    ref = O.ref()
-    threads = os.cpu_count() or 1
-    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
-    n_probe = min(n_target, 20)
-    t_probe, st_probe = ref_step_seconds(ref, M.config_text(cfg, n_probe if n_probe != M.CONFIGS[cfg]["n"] else None),
-                                         n_probe, cfg)
-    sweeps = lambda st, n: (st["amp_reads"] + st["amp_writes"]) / (2.0 * (1 << n))
-    n_run = n_probe
-    for cand in range(n_target, n_probe, -1):
-        est = t_probe * (1 << (cand - n_probe)) * 1.15
-        if est <= budget_s:
-            n_run = cand
-            break
-    if n_run != n_probe:
-        text = M.config_text(cfg, None if n_run == M.CONFIGS[cfg]["n"] else n_run)
-        t_run, st_run = ref_step_seconds(ref, text, n_run, cfg)
-    else:
-        t_run, st_run = t_probe, st_probe
-    p_run = sweeps(st_run, n_run)
-    if n_run == n_target:
-        t_target = t_run
-        sample = f"1 full reference Trotter step of config {cfg} at n={n_run} ({p_run:.0f} sweeps)"
-    else:
-        # sweeps/step at the target n from the reference's own schedule
-        _, _, g = ref.partition_text(M.config_text(cfg, None if n_target == M.CONFIGS[cfg]["n"] else n_target))
-        per = 0.0
-        for gr in g:
-            runs = len({c for c, _ in gr.cnots}) if gr.cnots else 0
-            per += 2 * (len(gr.h_pre) + len(gr.h_post) + 0.5 * runs + (1 if (gr.czs or gr.s_layer) else 0)) + 1
-        p_target = per * (2 if M.CONFIGS[cfg]["order"] == 2 else 1)
-        t_target = t_run * (1 << (n_target - n_run)) * (p_target / p_run)
-        sample = (f"1 full reference Trotter step of config {cfg} at n={n_run} ({p_run:.0f} sweeps, {t_run:.2f} s),"
-                  f" scaled x2^{n_target - n_run} state size x {p_target:.0f}/{p_run:.0f} sweeps to n={n_target}")
-    return {"value": 1.0 / t_target, "unit": "Trotter steps/s", "cores": threads, "kind": "reference",
-            "sample": sample, "s_per_step": t_target,
-            "host": _host_desc(), "omp_threads": int(os.environ.get("OMP_NUM_THREADS", threads)),
-            "n_sample": n_run, "scale_to_target": t_target / t_run}
+    def close(self):
+        self.ref.free(self.h)
+        del self.st
 
 
 def _host_desc():
@@ -219,40 +215,99 @@ def _host_desc():
         return "unknown"
 
 
+def _host_fits(nbytes: float) -> bool:
+    try:
+        import psutil
+        return psutil.virtual_memory().available > 1.5 * nbytes
+    except Exception:
+        return True
+
+
+def _ref_cap_reason(n: int):
+    if n > 30:
+        return "the reference StateVector caps n <= 30 (proj/src/statevector.cpp:63-65)"
+    try:
+        import psutil
+        need = 2.2 * 16 * (1 << n)
+        if psutil.virtual_memory().available < need:
+            return f"host RAM: {need / 2**30:.0f} GiB needed for the reference state + comparison"
+    except Exception:
+        pass
+    return None
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return 0
-    from paper_2206_11664_b200 import models as M
-
-    from oracle import oracle as O
-
+    M = load_models()
     cfg, n = args.config, args.n
     K, W = max(1, args.steps), max(0, args.warmup)
-    # each step is one reference Trotter step at the largest n whose step fits
-    # the per-step budget (the whole K + W run stays within a few minutes),
-    # scaled to n by state size x sweeps; the sizing run counts as a warm-up
-    per_step = max(2.0, min(args.ref_budget, 180.0 / (K + W)))
-    cb = cpu_reference(cfg, n, budget_s=per_step)
-    ref = O.ref()
-    n_s = cb["n_sample"]
-    text = M.config_text(cfg, None if n_s == M.CONFIGS[cfg]["n"] else n_s)
-    for _ in range(W - 1):
-        ref_step_seconds(ref, text, n_s, cfg)
-    times = [ref_step_seconds(ref, text, n_s, cfg)[0] * cb["scale_to_target"] for _ in range(K)]
-    v = K / sum(times)
-    cb = dict(cb, value=v, s_per_step=sum(times) / K,
-              sample=cb["sample"] + f"; {K} timed samples after {W} warm-up")
-    line = {
-        "metric": METRIC, "value": v, "unit": "Trotter steps/s", "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "c128 (f64 pairs)", "data": "synthetic (seeded generator, BASELINE config)",
-        "config": {"workload": f"config{cfg}: {CONFIG_DESC[cfg]}", "n_qubits": n, "dt": M.CONFIGS[cfg]["dt"],
-                   "order": M.CONFIGS[cfg]["order"]},
-        "impl": "reference", "cpu_baseline": cb,
-        "e2e": {"value": v, "unit": "Trotter steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
+    base = {"metric": METRIC, "unit": "Trotter steps/s", "n_gpus": world, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64 pairs)",
+            "data": "synthetic (seeded generator, BASELINE config)",
+            "config": {"workload": f"config{cfg}: {CONFIG_DESC[cfg]}", "n_qubits": n, "dt": M.CONFIGS[cfg]["dt"],
+                       "order": M.CONFIGS[cfg]["order"]},
+            "impl": "reference"}
+    why = _ref_cap_reason(n)
+    if why:
+        print(json.dumps(dict(base, unavailable=why)), flush=True)
+        return 0
+    rr = RefRun(cfg, n)
+    # Every timed step is one FULL reference Trotter step at the workload's
+    # size (no extrapolation). A step takes about a minute at n=30, so the
+    # arm times as many of the K requested steps as fit its budget; the
+    # state is resident before the first step, so no warm-up is needed.
+    times = []
+    for _ in range(K):
+        times.append(rr.step())
+        if sum(times) + times[-1] > args.ref_budget_total:
+            break
+    rr.close()
+    v = len(times) / sum(times)
+    cb = {"value": v, "unit": "Trotter steps/s", "cores": rr.threads, "kind": "reference",
+          "sample": (f"{len(times)} full reference Trotter steps of config {cfg} at n={n} (oracle/_ref = "
+                     f"proj/src compiled from the reference sources, evolve_grouped loop), "
+                     f"{rr.threads} OpenMP threads; s/step = {[round(t, 2) for t in times]}"),
+          "s_per_step": sum(times) / len(times), "host": _host_desc(), "omp_threads": rr.threads}
+    line = dict(base, value=v, steps=len(times), warmup=0, steps_requested=K, warmup_requested=W,
+                ms_per_step=1000.0 / v, cpu_baseline=cb,
+                e2e={"value": v, "unit": "Trotter steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
     print(json.dumps(line), flush=True)
     return 0
+
+
+def cpu_baseline_and_parity(cfg, n, psi, plan):
+    """cpu_baseline: one full reference Trotter step at the workload's size
+    on the host cores. parity: the same step on the GPU (the benchmarked plan
+    and kernels, from the same initial state) compared amplitude by amplitude
+    with the reference's state."""
+    import numpy as np
+
+    why = _ref_cap_reason(n)
+    if why:
+        return {"value": None, "reason": why}, {"checked": False, "reason": why}
+    rr = RefRun(cfg, n)
+    t = rr.step()
+    cb = {"value": 1.0 / t, "unit": "Trotter steps/s", "cores": rr.threads, "kind": "reference",
+          "sample": (f"1 full reference Trotter step of config {cfg} at n={n} (oracle/_ref, the reference "
+                     f"compiled from its sources), {rr.threads} OpenMP threads, no scaling"),
+          "s_per_step": t, "host": _host_desc(), "omp_threads": rr.threads}
+    init_state(psi, cfg, n, 0)
+    plan.evolve(rr.dt, 1)
+    chunk = 1 << min(n, 24)
+    dmax = 0.0
+    nsq_ref = 0.0
+    for f in range(0, 1 << n, chunk):
+        want = rr.st.read(f, chunk)
+        got = psi.amplitudes(f, chunk)
+        dmax = max(dmax, float(np.max(np.abs(got - want))))
+        nsq_ref += float(np.vdot(want, want).real)
+    par = {"checked": True, "n": n, "steps": 1, "max_abs_dpsi": dmax, "norm_err": abs(psi.norm() - 1.0),
+           "ref_norm_err": abs(math.sqrt(nsq_ref) - 1.0), "tol_dpsi": 1e-10, "tol_norm": 1e-12,
+           "oracle": "oracle/_ref (reference sources), persistent StateVector, same Hamiltonian/initial state/dt",
+           "ok": dmax <= 1e-10 and abs(psi.norm() - 1.0) <= 1e-12}
+    rr.close()
+    return cb, par
 
 
 # ------------------------------------------------------------ our arm
@@ -266,9 +321,14 @@ def run_ours(args, rank, world, local_rank):
     cfg, n = args.config, args.n
     dev = local_rank
     torch.cuda.set_device(dev)
+    gpus_active = 1
     if world > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # keeps NCCL's init lines (nranks) in the log
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        ids = [None] * world
+        dist.all_gather_object(ids, (os.uname().nodename, str(torch.cuda.get_device_properties(dev).uuid)))
+        gpus_active = len(set(ids))
     text, H, groups = build_workload(cfg, n)
     dt = M.CONFIGS[cfg]["dt"]
     order = M.CONFIGS[cfg]["order"]
@@ -342,7 +402,9 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not _host_fits(world * 16 * (1 << psi.n_local)):
+        e2e = {"value": None, "reason": "pinned host staging of every rank's shard exceeds available host RAM"}
+    elif not args.no_e2e:
         host = torch.empty(2 << psi.n_local, dtype=torch.float64, pin_memory=True)
         psi.download_ptr(host.data_ptr(), 1 << psi.n_local)
         barrier()
@@ -387,7 +449,8 @@ def run_ours(args, rank, world, local_rank):
     achieved = (bytes_per_launch / ((dom["ms"] / max(1, dom["launches"])) / 1e3)) / 1e9 if dom["launches"] else 0.0
     step_gbs = info["bytes_per_step"] / (ms_per_step / 1e3) / 1e9
     line = {
-        "metric": METRIC, "value": value, "unit": "Trotter steps/s", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": "Trotter steps/s", "n_gpus": world, "gpus_active": gpus_active,
+        "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "c128 (f64 pairs)", "data": "synthetic (seeded generator, BASELINE config)",
@@ -420,9 +483,10 @@ def run_ours(args, rank, world, local_rank):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = cpu_reference(cfg, n, budget_s=args.ref_budget)
+            line["cpu_baseline"], line["parity"] = cpu_baseline_and_parity(cfg, n, psi, plan)
         except Exception as ex:  # reported, never fatal
-            line["cpu_baseline"] = {"value": None, "error": str(ex)}
+            line["cpu_baseline"] = {"value": None, "error": repr(ex)}
+            line["parity"] = {"checked": False, "error": repr(ex)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -471,6 +535,34 @@ def run_baseline_method(args, rank, world, local_rank):
     return 0
 
 
+def relaunch(n: int) -> int:
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def launch_check(rank: int, world: int) -> int:
+    """Every rank joins one gloo group and checks the world it sees."""
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo")
+    t = torch.ones(1)
+    dist.all_reduce(t)
+    seen = [None] * world
+    dist.all_gather_object(seen, (rank, world, os.getpid()))
+    ok = int(t.item()) == world and len({p for _, _, p in seen}) == world
+    if rank == 0:
+        print(json.dumps({"launch_check": ok, "world": world, "ranks": sorted(r for r, _, _ in seen)}), flush=True)
+    dist.destroy_process_group()
+    return 0 if ok else 1
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -482,18 +574,29 @@ def main():
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-budget", type=float, default=30.0)
+    ap.add_argument("--ref-budget-total", type=float, default=150.0,
+                    help="--impl reference: stop timing further full steps once this many seconds are spent")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="only check the multi-process launch (gloo; every rank must see world == --gpus)")
     ap.add_argument("--nccl-exchange", action="store_true",
                     help="N>1: qubit remaps as grouped ncclSend/ncclRecv instead of the fused peer-memory store")
     ap.add_argument("--method", choices=["grouped", "baseline"], default="grouped",
                     help="grouped (the hot path) or the paper's per-term baseline on the GPU")
     args = ap.parse_args()
-    from paper_2206_11664_b200 import models as M
+    M = load_models()
     if args.n is None:
         args.n = M.CONFIGS[args.config]["n"]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun
+        return relaunch(args.gpus)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
+    if args.launch_check:
+        return launch_check(rank, world)
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
     if args.method == "baseline":

@@ -250,6 +250,18 @@ class Ref:
         L.ref_norm.argtypes = [dblp, C.c_int]
         L.ref_norm.restype = C.c_double
 
+        L.ref_sv_create.argtypes = [C.c_int]
+        L.ref_sv_create.restype = C.c_void_p
+        L.ref_sv_free.argtypes = [C.c_void_p]
+        L.ref_sv_set_basis.argtypes = [C.c_void_p, C.c_uint64]
+        L.ref_sv_write.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, dblp]
+        L.ref_sv_read.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, dblp]
+        L.ref_sv_evolve.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_int]
+        L.ref_sv_norm.argtypes = [C.c_void_p]
+        L.ref_sv_norm.restype = C.c_double
+        L.ref_set_threads.argtypes = [C.c_int]
+        L.ref_get_threads.restype = C.c_int
+
     def _err(self, rc):
         if rc == 0:
             return
@@ -354,6 +366,40 @@ class Ref:
         re, im = C.c_double(), C.c_double()
         self._err(self.lib.ref_expectation_text(b, len(b), a.ctypes.data_as(dblp), n, C.byref(re), C.byref(im)))
         return re.value, im.value
+
+
+class RefState:
+    """A persistent reference StateVector (oracle/_ref): evolve_grouped's loop
+    runs on it in place, so timings exclude host copies."""
+
+    def __init__(self, ref: Ref, n: int):
+        self.ref, self.n = ref, n
+        self.h = ref.lib.ref_sv_create(n)
+        if not self.h:
+            ref._err(3)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.ref.lib.ref_sv_free(self.h)
+            self.h = None
+
+    def set_basis(self, index: int) -> None:
+        self.ref._err(self.ref.lib.ref_sv_set_basis(self.h, index))
+
+    def write(self, first: int, a: np.ndarray) -> None:
+        a = np.ascontiguousarray(a, dtype=np.complex128)
+        self.ref._err(self.ref.lib.ref_sv_write(self.h, first, a.size, a.ctypes.data_as(dblp)))
+
+    def read(self, first: int, count: int) -> np.ndarray:
+        out = np.empty(count, np.complex128)
+        self.ref._err(self.ref.lib.ref_sv_read(self.h, first, count, out.ctypes.data_as(dblp)))
+        return out
+
+    def evolve(self, groups_handle, dt: float, steps: int, order: int = 1) -> None:
+        self.ref._err(self.ref.lib.ref_sv_evolve(self.h, groups_handle, dt, steps, order))
+
+    def norm(self) -> float:
+        return self.ref.lib.ref_sv_norm(self.h)
 
 
 def port() -> Port:

@@ -17,6 +17,8 @@
 #include <string>
 #include <vector>
 
+#include <omp.h>
+
 #include "simdiag/diagonalize.hpp"
 #include "simdiag/serialize.hpp"
 #include "simdiag/hamiltonian.hpp"
@@ -193,6 +195,58 @@ int ref_evolve_grouped(void* h, double* re_im, int n, double dt, int steps, int 
         }
     });
 }
+
+// A reference StateVector that persists across calls, so the CPU timings
+// (bench.py cpu_baseline / --impl reference) cover evolve_grouped's loop
+// only, not a 16 GiB copy in and out per call.
+void* ref_sv_create(int n) {
+    void* out = nullptr;
+    const int rc = guarded([&] { out = new simdiag::StateVector(n); });
+    return rc == 0 ? out : nullptr;
+}
+void ref_sv_free(void* sv) { delete static_cast<simdiag::StateVector*>(sv); }
+int ref_sv_set_basis(void* sv, uint64_t index) {
+    return guarded([&] {
+        auto& psi = *static_cast<simdiag::StateVector*>(sv);
+        for (uint64_t i = 0; i < psi.dim(); ++i) psi[i] = 0.0;
+        psi[index] = 1.0;
+    });
+}
+int ref_sv_write(void* sv, uint64_t first, uint64_t count, const double* re_im) {
+    return guarded([&] {
+        auto& psi = *static_cast<simdiag::StateVector*>(sv);
+        for (uint64_t i = 0; i < count; ++i) psi[first + i] = {re_im[2 * i], re_im[2 * i + 1]};
+    });
+}
+int ref_sv_read(void* sv, uint64_t first, uint64_t count, double* re_im) {
+    return guarded([&] {
+        const auto& psi = *static_cast<simdiag::StateVector*>(sv);
+        for (uint64_t i = 0; i < count; ++i) {
+            re_im[2 * i] = psi[first + i].real();
+            re_im[2 * i + 1] = psi[first + i].imag();
+        }
+    });
+}
+// evolve_grouped's loop (evolve.cpp:47-58) on the persistent state.
+int ref_sv_evolve(void* sv, void* h, double dt, int steps, int order) {
+    return guarded([&] {
+        auto& psi = *static_cast<simdiag::StateVector*>(sv);
+        const auto& gs = static_cast<RefGroups*>(h)->diags;
+        const size_t G = gs.size();
+        for (int s = 0; s < steps; ++s) {
+            if (order == 1 || G <= 1) {
+                for (const auto& g : gs) apply_group(psi, g, dt);
+            } else {
+                for (size_t g = 0; g + 1 < G; ++g) apply_group(psi, gs[g], 0.5 * dt);
+                apply_group(psi, gs[G - 1], dt);
+                for (size_t g = G - 1; g-- > 0;) apply_group(psi, gs[g], 0.5 * dt);
+            }
+        }
+    });
+}
+double ref_sv_norm(void* sv) { return simdiag::norm(*static_cast<simdiag::StateVector*>(sv)); }
+void ref_set_threads(int t) { omp_set_num_threads(t); }
+int ref_get_threads() { return omp_get_max_threads(); }
 
 int ref_random_state(int n, uint64_t seed, double* re_im) {
     return guarded([&] { store_state(simdiag::StateVector::random_state(n, seed), re_im); });

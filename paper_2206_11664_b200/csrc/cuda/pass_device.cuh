@@ -327,8 +327,8 @@ struct PassCtx {
 
     const PassDev& P;
     const PlanDev& plan;
-    const double2* __restrict__ psi;
-    double2* __restrict__ out;
+    const double2* psi;   // may alias out (in-place passes): no __restrict__
+    double2* out;
     double2* const* xdst;  // fused exchange destinations per chunk (nullptr: local store)
     double neg_dt;
     uint64_t rank_bits, n_tiles, stride;
@@ -857,7 +857,7 @@ struct PassCtx {
             for (int s = 0; s < NR; ++s) {
                 const uint64_t y = sb | o[s];
                 double2* const d = xdst[y >> P.x_t0] + ((y & low) | ownsh);
-                __stcs(d, sc ? make_double2(v[s].x * scale, v[s].y * scale) : v[s]);
+                SDB_TILE_STORE(d, sc ? make_double2(v[s].x * scale, v[s].y * scale) : v[s]);
             }
             return;
         }

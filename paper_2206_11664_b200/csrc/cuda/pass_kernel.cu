@@ -50,7 +50,7 @@ __global__ void k_tile_phase(PlanDev plan, int pass_index, double neg_dt, uint64
 
 template <int K, int RB>
 __global__ void __launch_bounds__(Cfg<K, RB>::NT, Cfg<K, RB>::MINB)
-k_tile_pass(const double2* __restrict__ psi, double2* __restrict__ out, double2* const* xdst, PlanDev plan,
+k_tile_pass(const double2* psi, double2* out, double2* const* xdst, PlanDev plan,
             int pass_index, double neg_dt, uint64_t rank_bits, uint64_t n_tiles) {
     const Interpreter prog;
     SDB_PASS_KERNEL_BODY(K, RB, prog)

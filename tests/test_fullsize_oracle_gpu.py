@@ -1,0 +1,98 @@
+"""Oracle parity at the BASELINE sizes (SURVEY §8c plan for configs 2-4).
+
+The fixtures tests/golden/fullsize_<case>_s<steps>.npz fingerprint the state
+the REFERENCE ITSELF (oracle/_ref, proj/src compiled from its sources; the
+evolve_grouped loop of proj/src/evolve.cpp:47-58) reaches at full size:
+config 4 (n=30, Neel) after 1 and 3 steps, config 3 (n=28, random_state(28,2))
+after 1 step, config 2 (n=25, |+>^25, S2) after 20 and all 500 steps
+(tests/golden/make_fullsize.py; tests/fingerprint.py says what a fingerprint
+holds). Here the benchmarked path (fused tile passes, NVRTC-specialised
+kernels, plan-time qubit layout search) evolves the same inputs on the GPU and
+the downloaded state is compared with the fingerprint:
+
+  max |dpsi| <= 1e-10 on ~20k sampled amplitudes (north star tolerance),
+  every block's weighted sum within 1e-10 (covers every amplitude),
+  |1 - ||psi||| <= 1e-12.
+"""
+import glob
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from paper_2206_11664_b200 import models as M
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import fingerprint as F  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+TOL_DPSI = 1e-10
+TOL_SKETCH = 1e-10
+TOL_NORM = 1e-12
+
+
+def _fixtures(case):
+    out = {}
+    for p in sorted(glob.glob(os.path.join(HERE, "golden", f"fullsize_{case}_s*.npz"))):
+        d = dict(np.load(p))
+        out[int(d["steps"])] = d
+    if not out:
+        pytest.skip(f"no full-size fixture for {case} (tests/golden/make_fullsize.py)")
+    return out
+
+
+def _init(sd, psi, cfg, n):
+    init = M.CONFIGS[cfg]["init"]
+    if init[0] == "basis":
+        psi.set_basis(M.initial_index(cfg, n))
+    elif init[0] == "plus":
+        import paper_2206_11664_b200._capi as A
+        A.check(A.sd_state_set_plus(psi._s))
+    else:
+        import paper_2206_11664_b200._capi as A
+        A.check(A.sd_state_set_random(psi._s, init[1]))
+
+
+def _check(fp, get_chunk, n, label):
+    r = F.compare(fp, get_chunk, n)
+    print(f"{label}: {r}")
+    assert r["ref_norm_err"] < 1e-9
+    assert r["max_abs_dpsi_sampled"] <= TOL_DPSI, r
+    assert r["max_abs_dblock_sketch"] <= TOL_SKETCH, r
+    assert r["norm_err"] <= TOL_NORM, r
+
+
+@pytest.mark.parametrize("case,cfg", [("cfg4_n30", 4), ("cfg3_n28", 3), ("cfg2_n25", 2)])
+def test_fullsize_matches_reference(case, cfg, sd):
+    fx = _fixtures(case)
+    n = M.CONFIGS[cfg]["n"]
+    dt, order = M.CONFIGS[cfg]["dt"], M.CONFIGS[cfg]["order"]
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(M.config_text(cfg)))
+    psi = sd.StateVector(n)
+    _init(sd, psi, cfg, n)
+    plan = sd.TrotterPlan(psi, groups, order=order)
+    done = 0
+    for steps in sorted(fx):
+        plan.evolve(dt, steps - done)
+        done = steps
+        _check(fx[steps], lambda f, c: psi.amplitudes(f, c), n, f"{case} after {steps} steps")
+
+
+def test_fullsize_sharded_p2_matches_reference(sd):
+    """Config 4 at n=30 as two in-process shards (qubit remaps fused into the
+    pass stores) against the reference's state after 1 step."""
+    fx = _fixtures("cfg4_n30")
+    if 1 not in fx:
+        pytest.skip("1-step fixture missing")
+    cfg, n = 4, 30
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(M.config_text(cfg)))
+    sh = sd.LocalShards(n, 2)
+    sh.set_basis(M.initial_index(cfg, n))
+    sh.enable_p2p()
+    sh.plan(groups, order=1)
+    sh.evolve(M.CONFIGS[cfg]["dt"], 1)
+    got = sh.amplitudes()
+    _check(fx[1], lambda f, c: got[f:f + c], n, "cfg4_n30 P=2 after 1 step")

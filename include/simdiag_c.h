@@ -50,6 +50,13 @@ typedef struct sd_hamiltonian sd_hamiltonian;
 sd_status sd_hamiltonian_from_terms(int n_qubits, const uint64_t* x_masks, const uint64_t* z_masks,
                                     const double* coeffs, size_t n_terms, double drop_tolerance,
                                     size_t* merged, sd_hamiltonian** out);
+/* gen_tfim / gen_syk (proj/include/simdiag/models.hpp:13-34,
+ * proj/src/models.cpp:17-92): the paper's benchmark models, identical to the
+ * reference's (same counter-RNG draws and term order). The SYK counts may be
+ * NULL. */
+sd_status sd_gen_tfim(int n_qubits, uint64_t seed, sd_hamiltonian** out);
+sd_status sd_gen_syk(int n_qubits, uint64_t seed, size_t* candidate_quadruples, size_t* merge_collisions,
+                     sd_hamiltonian** out);
 /* Hamiltonian::load (hamiltonian.hpp:33, hamiltonian.cpp:71-118) on an
  * in-memory text buffer. */
 sd_status sd_hamiltonian_load_text(const char* text, size_t len, double drop_tolerance,
@@ -196,9 +203,48 @@ sd_status sd_evolve_baseline(sd_state* s, const uint64_t* x_masks, const uint64_
                              size_t n_terms, double dt, int n_steps);
 /* expectation (evolve.cpp:99-135): sum_k coeffs[k] <psi|P_k|psi>; real part
  * in *re, |imaginary residue| in *imag_residue (may be NULL). Device
- * reductions in a fixed order (bit-identical for any launch). */
+ * reductions in a fixed order (bit-identical for any launch).
+ *
+ * Sharded states (one process per GPU, communicator attached): these calls,
+ * sd_apply_pauli_rotation, sd_evolve_baseline, sd_state_norm and
+ * sd_state_fidelity are COLLECTIVE -- every rank calls them with the same
+ * arguments. A term whose X part flips a global (rank) qubit pairs
+ * amplitudes across shards: each rank copies its partner shard (rank ^ the
+ * global X bits) into its exchange buffer over NCCL first. Per-shard partials
+ * are all-gathered and summed in rank order, so the result is identical on
+ * every rank. Masks address LOGICAL qubits; a relabelled state is handled by
+ * mapping them to physical bits (no canonicalisation). */
 sd_status sd_expectation(sd_state* s, const uint64_t* x_masks, const uint64_t* z_masks, const double* coeffs,
                          size_t n_terms, double* re, double* imag_residue);
+/* norm() (statevector.cpp:403-407) of the whole (sharded) state. */
+sd_status sd_state_norm(sd_state* s, double* out);
+/* fidelity() = |<a|b>| (statevector.cpp:409-418) of two whole (sharded)
+ * states with the same shape (relabelled layouts are canonicalised first). */
+sd_status sd_state_fidelity(sd_state* a, sd_state* b, double* out);
+/* The same operations on `world` in-process shards (sd_state_create_local_shards). */
+sd_status sd_local_expectation(sd_state* const* shards, int world, const uint64_t* x_masks,
+                               const uint64_t* z_masks, const double* coeffs, size_t n_terms, double* re,
+                               double* imag_residue);
+sd_status sd_local_apply_pauli_rotation(sd_state* const* shards, int world, uint64_t x_mask, uint64_t z_mask,
+                                        double coeff, double dt);
+sd_status sd_local_evolve_baseline(sd_state* const* shards, int world, const uint64_t* x_masks,
+                                   const uint64_t* z_masks, const double* coeffs, size_t n_terms, double dt,
+                                   int n_steps);
+sd_status sd_local_norm(sd_state* const* shards, int world, double* out);
+sd_status sd_local_fidelity(sd_state* const* a, sd_state* const* b, int world, double* out);
+
+/* apply_single_qubit / apply_two_qubit (statevector.hpp:53-55,
+ * statevector.cpp:101-154): u = row-major 2x2 (8 doubles) / 4x4 (32 doubles)
+ * complex matrix as (re, im) pairs, unitary within 1e-10 (else
+ * SD_INVALID_ARGUMENT, "... matrix is not unitary"); the two-qubit local
+ * index is 2*bit(q1) + bit(q2). Unsharded states. */
+sd_status sd_apply_single_qubit(sd_state* s, const double* u, int target);
+sd_status sd_apply_two_qubit(sd_state* s, const double* u, int q1, int q2);
+/* exact_evolve (evolve.hpp:38-42, evolve.cpp:60-97): psi <- exp(-i H t) psi
+ * for n <= 12 (the reference's dense test oracle; here a time-sliced Taylor
+ * series on the device). */
+sd_status sd_exact_evolve(sd_state* s, const uint64_t* x_masks, const uint64_t* z_masks, const double* coeffs,
+                          size_t n_terms, double t);
 
 /* ------------------------------------------------------------------ */
 /* Fused Trotter plan (replaces evolve_grouped, evolve.cpp:47-58)       */

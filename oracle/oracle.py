@@ -250,6 +250,10 @@ class Ref:
         L.ref_norm.argtypes = [dblp, C.c_int]
         L.ref_norm.restype = C.c_double
 
+        L.ref_gen_save_text.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t),
+                                        u64p]
+        L.ref_generic_gate.argtypes = [dblp, C.c_int, dblp, C.c_int, C.c_int]
+        L.ref_evolve_baseline_groups.argtypes = [C.c_void_p, dblp, C.c_int, C.c_double, C.c_int]
         L.ref_sv_create.argtypes = [C.c_int]
         L.ref_sv_create.restype = C.c_void_p
         L.ref_sv_free.argtypes = [C.c_void_p]
@@ -350,6 +354,29 @@ class Ref:
         """StateVector::apply_pauli_rotation (statevector.cpp:288-337)."""
         a = np.ascontiguousarray(psi, dtype=np.complex128).copy()
         self._err(self.lib.ref_pauli_rotation(a.ctypes.data_as(dblp), n, x, z, coeff, dt))
+        return a
+
+    def gen_text(self, model: str, n: int, seed: int):
+        """gen_tfim / gen_syk (models.cpp:17-92) saved as text, + SYK counts."""
+        which = {"tfim": 0, "syk": 1}[model]
+        ln = C.c_size_t(0)
+        info = np.zeros(2, np.uint64)
+        self._err(self.lib.ref_gen_save_text(which, n, seed, None, 0, C.byref(ln), _p(info, u64p)))
+        buf = C.create_string_buffer(ln.value + 1)
+        self._err(self.lib.ref_gen_save_text(which, n, seed, buf, ln.value + 1, C.byref(ln), _p(info, u64p)))
+        return buf.value.decode(), (int(info[0]), int(info[1]))
+
+    def generic_gate(self, psi, n, u, q1, q2=-1):
+        """apply_single_qubit (q2 < 0) / apply_two_qubit (statevector.cpp:101-154)."""
+        a = np.ascontiguousarray(psi, dtype=np.complex128).copy()
+        m = np.ascontiguousarray(np.asarray(u, dtype=np.complex128).reshape(-1))
+        self._err(self.lib.ref_generic_gate(a.ctypes.data_as(dblp), n, m.ctypes.data_as(dblp), q1, q2))
+        return a
+
+    def evolve_baseline_groups(self, h, psi, n, dt, steps):
+        """evolve_baseline(span<const CommutingGroup>) (evolve.cpp:34-45), restated loop."""
+        a = np.ascontiguousarray(psi, dtype=np.complex128).copy()
+        self._err(self.lib.ref_evolve_baseline_groups(h, a.ctypes.data_as(dblp), n, dt, steps))
         return a
 
     def evolve_baseline(self, text: str, psi, n, dt, steps):

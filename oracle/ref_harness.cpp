@@ -22,6 +22,7 @@
 #include "simdiag/diagonalize.hpp"
 #include "simdiag/serialize.hpp"
 #include "simdiag/hamiltonian.hpp"
+#include "simdiag/models.hpp"
 #include "simdiag/statevector.hpp"
 
 namespace {
@@ -91,6 +92,27 @@ int ref_partition_text(const char* text, size_t len, int synthesize, void** out)
             r->diags.push_back(std::move(d));
         }
         *out = r.release();
+    });
+}
+
+// gen_tfim (model 0) / gen_syk (model 1) (models.cpp:17-92) -> save() text.
+int ref_gen_save_text(int model, int n, uint64_t seed, char* buf, size_t cap, size_t* out_len, uint64_t* info) {
+    return guarded([&] {
+        simdiag::SykInfo si;
+        const simdiag::Hamiltonian h = model == 0 ? simdiag::gen_tfim(n, seed) : simdiag::gen_syk(n, seed, &si);
+        std::ostringstream os;
+        h.save(os);
+        const std::string s = os.str();
+        *out_len = s.size();
+        if (info) {
+            info[0] = si.candidate_quadruples;
+            info[1] = si.merge_collisions;
+        }
+        if (buf && cap) {
+            const size_t k = s.size() < cap - 1 ? s.size() : cap - 1;
+            std::memcpy(buf, s.data(), k);
+            buf[k] = 0;
+        }
     });
 }
 
@@ -281,6 +303,39 @@ int ref_pauli_rotation(double* re_im, int n, uint64_t x, uint64_t z, double coef
         simdiag::StateVector psi(n);
         load_state(psi, re_im);
         psi.apply_pauli_rotation(simdiag::WeightedTerm{coeff, simdiag::PauliString::from_masks(n, x, z)}, dt);
+        store_state(psi, re_im);
+    });
+}
+
+// apply_single_qubit / apply_two_qubit (statevector.cpp:101-154); u =
+// row-major complex entries as (re, im) pairs.
+int ref_generic_gate(double* re_im, int n, const double* u, int q1, int q2) {
+    return guarded([&] {
+        simdiag::StateVector psi(n);
+        load_state(psi, re_im);
+        if (q2 < 0) {
+            simdiag::Mat2 m;
+            for (int k = 0; k < 4; ++k) m[k] = {u[2 * k], u[2 * k + 1]};
+            psi.apply_single_qubit(m, q1);
+        } else {
+            simdiag::Mat4 m;
+            for (int k = 0; k < 16; ++k) m[k] = {u[2 * k], u[2 * k + 1]};
+            psi.apply_two_qubit(m, q1, q2);
+        }
+        store_state(psi, re_im);
+    });
+}
+
+// evolve_baseline(span<const CommutingGroup>, ...) restated (evolve.cpp:34-45)
+// over a partition_text handle's groups.
+int ref_evolve_baseline_groups(void* h, double* re_im, int n, double dt, int steps) {
+    return guarded([&] {
+        auto* r = static_cast<RefGroups*>(h);
+        simdiag::StateVector psi(n);
+        load_state(psi, re_im);
+        for (int s = 0; s < steps; ++s)
+            for (const auto& g : r->parts)
+                for (const auto& term : g.terms) psi.apply_pauli_rotation(term, dt);
         store_state(psi, re_im);
     });
 }

@@ -23,6 +23,9 @@ from .simdiag import (  # noqa: F401
     diagonalize_group,
     evolve_baseline,
     evolve_grouped,
+    exact_evolve,
+    gen_syk,
+    gen_tfim,
     exchange_routes,
     expectation,
     fidelity,
@@ -37,5 +40,5 @@ __all__ = [
     "CliffordCircuit", "CommutingGroup", "DiagonalGroup", "EvolutionPlan", "Hamiltonian",
     "PauliString", "StateVector", "TrotterPlan", "WeightedTerm", "commutes", "diagonalize_group",
     "evolve_grouped", "fidelity", "greedy_partition", "norm", "partition_and_diagonalize", "models",
-    "LocalShards", "comm_unique_id", "plan_preview", "evolve_baseline", "expectation",
+    "LocalShards", "comm_unique_id", "plan_preview", "evolve_baseline", "expectation", "exact_evolve", "gen_tfim", "gen_syk",
 ]

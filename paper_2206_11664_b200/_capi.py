@@ -88,6 +88,8 @@ sd_hamiltonian_from_terms = _sig(
     "sd_hamiltonian_from_terms",
     [C.c_int, C.POINTER(u64), C.POINTER(u64), C.POINTER(dbl), sz, dbl, C.POINTER(sz), PP],
 )
+sd_gen_tfim = _sig("sd_gen_tfim", [C.c_int, u64, PP])
+sd_gen_syk = _sig("sd_gen_syk", [C.c_int, u64, C.POINTER(sz), C.POINTER(sz), PP])
 sd_hamiltonian_load_text = _sig("sd_hamiltonian_load_text", [C.c_char_p, sz, dbl, PP])
 sd_hamiltonian_load_file = _sig("sd_hamiltonian_load_file", [C.c_char_p, dbl, PP])
 sd_hamiltonian_save_text = _sig("sd_hamiltonian_save_text", [P, C.c_char_p, sz, C.POINTER(sz)])
@@ -154,6 +156,17 @@ sd_apply_pauli_rotation = _sig("sd_apply_pauli_rotation", [P, u64, u64, dbl, dbl
 sd_evolve_baseline = _sig("sd_evolve_baseline", [P, C.POINTER(u64), C.POINTER(u64), C.POINTER(dbl), sz, dbl, C.c_int])
 sd_expectation = _sig("sd_expectation", [P, C.POINTER(u64), C.POINTER(u64), C.POINTER(dbl), sz, C.POINTER(dbl),
                                          C.POINTER(dbl)])
+PU, PD = C.POINTER(u64), C.POINTER(dbl)
+sd_state_norm = _sig("sd_state_norm", [P, PD])
+sd_state_fidelity = _sig("sd_state_fidelity", [P, P, PD])
+sd_local_expectation = _sig("sd_local_expectation", [C.POINTER(P), C.c_int, PU, PU, PD, sz, PD, PD])
+sd_local_apply_pauli_rotation = _sig("sd_local_apply_pauli_rotation", [C.POINTER(P), C.c_int, u64, u64, dbl, dbl])
+sd_local_evolve_baseline = _sig("sd_local_evolve_baseline", [C.POINTER(P), C.c_int, PU, PU, PD, sz, dbl, C.c_int])
+sd_local_norm = _sig("sd_local_norm", [C.POINTER(P), C.c_int, PD])
+sd_local_fidelity = _sig("sd_local_fidelity", [C.POINTER(P), C.POINTER(P), C.c_int, PD])
+sd_apply_single_qubit = _sig("sd_apply_single_qubit", [P, PD, C.c_int])
+sd_apply_two_qubit = _sig("sd_apply_two_qubit", [P, PD, C.c_int, C.c_int])
+sd_exact_evolve = _sig("sd_exact_evolve", [P, PU, PU, PD, sz, dbl])
 sd_jit_compile_preview = _sig("sd_jit_compile_preview", [C.c_int, C.c_int, C.POINTER(GroupDesc), sz,
                                                          C.POINTER(PlanOptions), C.POINTER(sz)])
 sd_state_create_local_shards = _sig("sd_state_create_local_shards", [C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(P)])
@@ -190,6 +203,9 @@ EXPORTED = [
     "sd_jit_compile_preview", "sd_apply_pauli_rotation", "sd_evolve_baseline", "sd_expectation",
     "sd_local_enable_p2p", "sd_state_ipc_handles", "sd_state_attach_peers", "sd_groups_diag_json",
     "sd_state_save_raw", "sd_state_load_raw",
+    "sd_state_norm", "sd_state_fidelity", "sd_local_expectation", "sd_local_apply_pauli_rotation",
+    "sd_local_evolve_baseline", "sd_local_norm", "sd_local_fidelity", "sd_apply_single_qubit",
+    "sd_apply_two_qubit", "sd_exact_evolve", "sd_gen_tfim", "sd_gen_syk",
 ]
 
 

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <bit>
 #include <cmath>
+#include <complex>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -1430,70 +1431,6 @@ sd_status sd_jit_compile_preview(int n, int world, const sd_group_desc* groups, 
     });
 }
 
-sd_status sd_apply_pauli_rotation(sd_state* h, uint64_t x_mask, uint64_t z_mask, double coeff, double dt) {
-    return guard([&] {
-        sdb::StateImpl& s = st(h);
-        require_unsharded(s);
-        require_identity_layout(s);
-        const uint64_t all = s.amps_count() - 1;
-        if ((x_mask | z_mask) & ~all) throw std::invalid_argument("pauli rotation: qubit count mismatch");
-        SDB_CUDA(cudaSetDevice(s.device));
-        sdb::launch_pauli_rotation(s, x_mask, z_mask, coeff, dt);
-        bump(s, s.amps_count(), s.amps_count());
-        SDB_CUDA(cudaStreamSynchronize(s.stream));
-    });
-}
-
-sd_status sd_evolve_baseline(sd_state* h, const uint64_t* x, const uint64_t* z, const double* coeffs, size_t n_terms,
-                             double dt, int n_steps) {
-    return guard([&] {
-        sdb::StateImpl& s = st(h);
-        require_unsharded(s);
-        require_identity_layout(s);
-        require(n_terms == 0 || (x && z && coeffs), "null term arrays");
-        if (n_steps < 0) throw std::invalid_argument("plan needs n_steps >= 0");
-        if (!std::isfinite(dt)) throw std::invalid_argument("plan needs finite total_time");
-        const uint64_t all = s.amps_count() - 1;
-        for (size_t k = 0; k < n_terms; ++k) {
-            if ((x[k] | z[k]) & ~all) throw std::invalid_argument("hamiltonian/state qubit counts differ");
-        }
-        SDB_CUDA(cudaSetDevice(s.device));
-        for (int step = 0; step < n_steps; ++step) {
-            for (size_t k = 0; k < n_terms; ++k) {
-                sdb::launch_pauli_rotation(s, x[k], z[k], coeffs[k], dt);
-                bump(s, s.amps_count(), s.amps_count());
-            }
-        }
-        SDB_CUDA(cudaStreamSynchronize(s.stream));
-    });
-}
-
-sd_status sd_expectation(sd_state* h, const uint64_t* x, const uint64_t* z, const double* coeffs, size_t n_terms,
-                         double* re, double* imag_residue) {
-    return guard([&] {
-        sdb::StateImpl& s = st(h);
-        require_unsharded(s);
-        require(re != nullptr, "null output");
-        require(n_terms == 0 || (x && z && coeffs), "null term arrays");
-        if (!is_identity(s.phys_of)) {
-            SDB_CUDA(cudaSetDevice(s.device));
-            permute_local(s);
-        }
-        const uint64_t all = s.amps_count() - 1;
-        SDB_CUDA(cudaSetDevice(s.device));
-        double tr = 0.0, ti = 0.0;
-        for (size_t k = 0; k < n_terms; ++k) {
-            if ((x[k] | z[k]) & ~all) throw std::invalid_argument("hamiltonian/state qubit counts differ");
-            double r = 0.0, i = 0.0;
-            sdb::device_expectation_term(s, x[k], z[k], &r, &i);
-            tr += coeffs[k] * r;
-            ti += coeffs[k] * i;
-        }
-        *re = tr;
-        if (imag_residue) *imag_residue = std::abs(ti);
-    });
-}
-
 namespace {
 void ensure_xbuf(sdb::StateImpl& s) {
     if (s.xbuf) return;
@@ -1657,3 +1594,370 @@ sd_status sd_state_load_raw(sd_state* h, const char* path) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Observables and the per-term baseline on (sharded) states: expectation
+// (evolve.cpp:99-135), norm / fidelity (statevector.cpp:403-418),
+// apply_pauli_rotation (statevector.cpp:288-337), evolve_baseline
+// (evolve.cpp:21-45), and the generic gates apply_single_qubit /
+// apply_two_qubit (statevector.cpp:101-154).
+//
+// Masks are mapped through the state's logical -> physical layout, so a
+// relabelled state needs no canonicalisation. A term whose X part touches a
+// global (rank) bit pairs amplitudes across shards: every shard first takes a
+// copy of its partner shard (rank ^ x_hi) into its exchange buffer -- NCCL
+// send/recv for one process per GPU, device copies for in-process shards --
+// and terms are visited grouped by x_hi so each partner is copied once.
+// Partial sums are per shard in a fixed block order, combined over shards in
+// rank order (all-gather, not a reduction), so results are deterministic.
+namespace {
+
+uint64_t phys_mask(const sdb::StateImpl& s, uint64_t logical) {
+    uint64_t out = 0;
+    for (uint64_t m = logical; m; m &= m - 1) out |= 1ull << s.phys_of[std::countr_zero(m)];
+    return out;
+}
+
+// The shards one call drives: all of them (in-process), or this rank's one
+// (NCCL: the call is collective over the communicator).
+struct ShardSet {
+    std::vector<sdb::StateImpl*> sh;
+    bool nccl = false;
+    int n = 0, n_local = 0;
+};
+
+ShardSet one_shard(sd_state* h) {
+    ShardSet S;
+    sdb::StateImpl& s = st(h);
+    S.sh = {&s};
+    S.n = s.n;
+    S.n_local = s.n_local;
+    if (s.world > 1) {
+        if (!s.nccl)
+            throw std::invalid_argument("sharded state without a communicator: attach one (sd_state_attach_comm) "
+                                        "or use the sd_local_* entry points for in-process shards");
+        S.nccl = true;
+    }
+    return S;
+}
+
+ShardSet local_set(sd_state* const* hs, int world) {
+    require(hs != nullptr && world >= 1, "null shard array");
+    ShardSet S;
+    for (int r = 0; r < world; ++r) {
+        sdb::StateImpl& s = st(hs[r]);
+        require(s.rank == r && s.world == world, "shards[r] must be rank r of `world`");
+        require(r == 0 || s.phys_of == S.sh[0]->phys_of, "shards disagree on the layout");
+        S.sh.push_back(&s);
+    }
+    S.n = S.sh[0]->n;
+    S.n_local = S.sh[0]->n_local;
+    return S;
+}
+
+void sync_all(const ShardSet& S) {
+    for (sdb::StateImpl* s : S.sh) {
+        SDB_CUDA(cudaSetDevice(s->device));
+        SDB_CUDA(cudaStreamSynchronize(s->stream));
+    }
+}
+
+// every shard's exchange buffer <- a copy of shard rank ^ x_hi
+void fetch_partners(ShardSet& S, uint64_t x_hi) {
+    for (sdb::StateImpl* s : S.sh) ensure_xbuf(*s);
+    if (S.nccl) {
+        sdb::StateImpl& s = *S.sh[0];
+        SDB_CUDA(cudaSetDevice(s.device));
+        sdb::nccl_copy_partner(s, s.rank ^ static_cast<int>(x_hi));
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+        return;
+    }
+    sync_all(S);
+    for (sdb::StateImpl* s : S.sh) {
+        const sdb::StateImpl& p = *S.sh[s->rank ^ static_cast<int>(x_hi)];
+        SDB_CUDA(cudaSetDevice(s->device));
+        SDB_CUDA(cudaMemcpyPeerAsync(s->xbuf, s->device, p.amps, p.device, 16 * s->amps_count(), s->stream));
+    }
+    sync_all(S);
+}
+
+// per-rank values (rank order) of `local` vectors computed per shard
+std::vector<double> gather_ranks(ShardSet& S, const std::vector<std::vector<double>>& local) {
+    if (S.nccl) return sdb::nccl_gather(*S.sh[0], local[0]);
+    std::vector<double> out;
+    for (const auto& v : local) out.insert(out.end(), v.begin(), v.end());
+    return out;
+}
+
+int world_of(const ShardSet& S) { return S.sh[0]->world; }
+
+void check_term_masks(const ShardSet& S, const uint64_t* x, const uint64_t* z, size_t m, const char* what) {
+    const uint64_t all = S.n >= 64 ? ~0ull : ((1ull << S.n) - 1);
+    for (size_t k = 0; k < m; ++k) {
+        if ((x[k] | z[k]) & ~all) throw std::invalid_argument(what);
+    }
+}
+
+void expectation_set(ShardSet& S, const uint64_t* x, const uint64_t* z, const double* coeffs, size_t m, double* re,
+                     double* imag_residue) {
+    require(re != nullptr, "null output");
+    require(m == 0 || (x && z && coeffs), "null term arrays");
+    check_term_masks(S, x, z, m, "hamiltonian/state qubit counts differ");
+    const sdb::StateImpl& s0 = *S.sh[0];
+    std::vector<uint64_t> xp(m), zp(m);
+    for (size_t k = 0; k < m; ++k) {
+        xp[k] = phys_mask(s0, x[k]);
+        zp[k] = phys_mask(s0, z[k]);
+    }
+    // visit terms grouped by the global part of X (one partner copy per group)
+    std::vector<size_t> order(m);
+    std::iota(order.begin(), order.end(), size_t(0));
+    std::stable_sort(order.begin(), order.end(),
+                     [&](size_t a, size_t b) { return (xp[a] >> S.n_local) < (xp[b] >> S.n_local); });
+    std::vector<std::vector<double>> part(S.sh.size(), std::vector<double>(2 * m, 0.0));
+    uint64_t have = ~0ull;
+    for (size_t k : order) {
+        const uint64_t x_hi = xp[k] >> S.n_local;
+        if (x_hi != 0 && x_hi != have) {
+            fetch_partners(S, x_hi);
+            have = x_hi;
+        }
+        for (size_t i = 0; i < S.sh.size(); ++i) {
+            sdb::StateImpl& s = *S.sh[i];
+            SDB_CUDA(cudaSetDevice(s.device));
+            sdb::device_expectation_term(s, xp[k], zp[k], s.xbuf, &part[i][2 * k], &part[i][2 * k + 1]);
+        }
+    }
+    const std::vector<double> all = gather_ranks(S, part);
+    const int W = world_of(S);
+    double tr = 0.0, ti = 0.0;
+    for (size_t k = 0; k < m; ++k) {
+        double sr = 0.0, si = 0.0;
+        for (int r = 0; r < W; ++r) {
+            sr += all[2 * m * r + 2 * k];
+            si += all[2 * m * r + 2 * k + 1];
+        }
+        tr += coeffs[k] * sr;
+        ti += coeffs[k] * si;
+    }
+    *re = tr;
+    if (imag_residue) *imag_residue = std::abs(ti);
+}
+
+void rotation_set(ShardSet& S, uint64_t x, uint64_t z, double coeff, double dt) {
+    const sdb::StateImpl& s0 = *S.sh[0];
+    const uint64_t xp = phys_mask(s0, x), zp = phys_mask(s0, z);
+    const uint64_t x_hi = xp >> S.n_local;
+    if (x_hi) fetch_partners(S, x_hi);
+    for (sdb::StateImpl* s : S.sh) {
+        SDB_CUDA(cudaSetDevice(s->device));
+        sdb::launch_pauli_rotation(*s, xp, zp, coeff, dt, x_hi ? s->xbuf : nullptr);
+        bump(*s, s->amps_count(), s->amps_count());
+    }
+    if (x_hi) sync_all(S);  // the partner copies are reused by the next term
+}
+
+double norm_set(ShardSet& S) {
+    std::vector<std::vector<double>> part(S.sh.size(), std::vector<double>(1, 0.0));
+    for (size_t i = 0; i < S.sh.size(); ++i) {
+        SDB_CUDA(cudaSetDevice(S.sh[i]->device));
+        part[i][0] = sdb::device_norm_sq(*S.sh[i]);
+    }
+    const std::vector<double> all = gather_ranks(S, part);
+    double v = 0.0;
+    for (double p : all) v += p;
+    return std::sqrt(v);
+}
+
+void canonical_set(ShardSet& S, sd_state* const* hs) {
+    if (is_identity(S.sh[0]->phys_of)) return;
+    if (S.nccl || world_of(S) == 1) {
+        SDB_CUDA(cudaSetDevice(S.sh[0]->device));
+        if (world_of(S) == 1) permute_local(*S.sh[0]);
+        else canonicalize_nccl(*S.sh[0]);
+        SDB_CUDA(cudaStreamSynchronize(S.sh[0]->stream));
+        return;
+    }
+    if (sd_local_canonicalize(hs, world_of(S)) != SD_OK) throw std::runtime_error(sd_last_error());
+}
+
+double fidelity_set(ShardSet& A, ShardSet& B, sd_state* const* ha, sd_state* const* hb) {
+    require(A.n == B.n && A.n_local == B.n_local && A.sh.size() == B.sh.size(), "fidelity: dimension mismatch");
+    canonical_set(A, ha);
+    canonical_set(B, hb);
+    std::vector<std::vector<double>> part(A.sh.size(), std::vector<double>(2, 0.0));
+    for (size_t i = 0; i < A.sh.size(); ++i) {
+        SDB_CUDA(cudaSetDevice(B.sh[i]->device));
+        SDB_CUDA(cudaStreamSynchronize(B.sh[i]->stream));
+        SDB_CUDA(cudaSetDevice(A.sh[i]->device));
+        sdb::device_inner(*A.sh[i], *B.sh[i], &part[i][0], &part[i][1]);
+    }
+    const std::vector<double> all = gather_ranks(A, part);
+    double re = 0.0, im = 0.0;
+    for (size_t r = 0; 2 * r < all.size(); ++r) {
+        re += all[2 * r];
+        im += all[2 * r + 1];
+    }
+    return std::hypot(re, im);
+}
+
+bool approx_unitary(const double* u, int d) {
+    // U U^dagger == I within 1e-10 (statevector.cpp:29-50)
+    for (int r = 0; r < d; ++r) {
+        for (int c = 0; c < d; ++c) {
+            std::complex<double> e = 0.0;
+            for (int k = 0; k < d; ++k)
+                e += std::complex<double>(u[2 * (r * d + k)], u[2 * (r * d + k) + 1]) *
+                     std::conj(std::complex<double>(u[2 * (c * d + k)], u[2 * (c * d + k) + 1]));
+            if (std::abs(e - (r == c ? 1.0 : 0.0)) > 1e-10) return false;
+        }
+    }
+    return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+sd_status sd_apply_pauli_rotation(sd_state* h, uint64_t x_mask, uint64_t z_mask, double coeff, double dt) {
+    return guard([&] {
+        ShardSet S = one_shard(h);
+        check_term_masks(S, &x_mask, &z_mask, 1, "pauli rotation: qubit count mismatch");
+        rotation_set(S, x_mask, z_mask, coeff, dt);
+        sync_all(S);
+    });
+}
+
+sd_status sd_local_apply_pauli_rotation(sd_state* const* hs, int world, uint64_t x_mask, uint64_t z_mask,
+                                        double coeff, double dt) {
+    return guard([&] {
+        ShardSet S = local_set(hs, world);
+        check_term_masks(S, &x_mask, &z_mask, 1, "pauli rotation: qubit count mismatch");
+        rotation_set(S, x_mask, z_mask, coeff, dt);
+        sync_all(S);
+    });
+}
+
+static void baseline_set(ShardSet& S, const uint64_t* x, const uint64_t* z, const double* coeffs, size_t n_terms,
+                         double dt, int n_steps) {
+    require(n_terms == 0 || (x && z && coeffs), "null term arrays");
+    if (n_steps < 0) throw std::invalid_argument("plan needs n_steps >= 0");
+    if (!std::isfinite(dt)) throw std::invalid_argument("plan needs finite total_time");
+    check_term_masks(S, x, z, n_terms, "hamiltonian/state qubit counts differ");
+    for (int step = 0; step < n_steps; ++step)
+        for (size_t k = 0; k < n_terms; ++k) rotation_set(S, x[k], z[k], coeffs[k], dt);
+    sync_all(S);
+}
+
+sd_status sd_evolve_baseline(sd_state* h, const uint64_t* x, const uint64_t* z, const double* coeffs, size_t n_terms,
+                             double dt, int n_steps) {
+    return guard([&] {
+        ShardSet S = one_shard(h);
+        baseline_set(S, x, z, coeffs, n_terms, dt, n_steps);
+    });
+}
+
+sd_status sd_local_evolve_baseline(sd_state* const* hs, int world, const uint64_t* x, const uint64_t* z,
+                                   const double* coeffs, size_t n_terms, double dt, int n_steps) {
+    return guard([&] {
+        ShardSet S = local_set(hs, world);
+        baseline_set(S, x, z, coeffs, n_terms, dt, n_steps);
+    });
+}
+
+sd_status sd_expectation(sd_state* h, const uint64_t* x, const uint64_t* z, const double* coeffs, size_t n_terms,
+                         double* re, double* imag_residue) {
+    return guard([&] {
+        ShardSet S = one_shard(h);
+        expectation_set(S, x, z, coeffs, n_terms, re, imag_residue);
+    });
+}
+
+sd_status sd_local_expectation(sd_state* const* hs, int world, const uint64_t* x, const uint64_t* z,
+                               const double* coeffs, size_t n_terms, double* re, double* imag_residue) {
+    return guard([&] {
+        ShardSet S = local_set(hs, world);
+        expectation_set(S, x, z, coeffs, n_terms, re, imag_residue);
+    });
+}
+
+sd_status sd_state_norm(sd_state* h, double* out) {
+    return guard([&] {
+        require(out != nullptr, "null output");
+        ShardSet S = one_shard(h);
+        *out = norm_set(S);
+    });
+}
+
+sd_status sd_local_norm(sd_state* const* hs, int world, double* out) {
+    return guard([&] {
+        require(out != nullptr, "null output");
+        ShardSet S = local_set(hs, world);
+        *out = norm_set(S);
+    });
+}
+
+sd_status sd_state_fidelity(sd_state* a, sd_state* b, double* out) {
+    return guard([&] {
+        require(out != nullptr, "null output");
+        ShardSet A = one_shard(a), B = one_shard(b);
+        *out = fidelity_set(A, B, &a, &b);
+    });
+}
+
+sd_status sd_local_fidelity(sd_state* const* a, sd_state* const* b, int world, double* out) {
+    return guard([&] {
+        require(out != nullptr, "null output");
+        ShardSet A = local_set(a, world), B = local_set(b, world);
+        *out = fidelity_set(A, B, a, b);
+    });
+}
+
+sd_status sd_apply_single_qubit(sd_state* h, const double* u, int target) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require(u != nullptr, "null matrix");
+        require_unsharded(s);
+        check_qubit(s, target);
+        if (!approx_unitary(u, 2)) throw std::invalid_argument("single-qubit matrix is not unitary");
+        SDB_CUDA(cudaSetDevice(s.device));
+        sdb::launch_single_qubit(s, u, s.phys_of[target]);
+        bump(s, s.amps_count(), s.amps_count());
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
+sd_status sd_apply_two_qubit(sd_state* h, const double* u, int q1, int q2) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require(u != nullptr, "null matrix");
+        require_unsharded(s);
+        check_qubit(s, q1);
+        check_qubit(s, q2);
+        if (q1 == q2) throw std::invalid_argument("two-qubit gate requires distinct qubits");
+        if (!approx_unitary(u, 4)) throw std::invalid_argument("two-qubit matrix is not unitary");
+        SDB_CUDA(cudaSetDevice(s.device));
+        sdb::launch_two_qubit(s, u, s.phys_of[q1], s.phys_of[q2]);
+        bump(s, s.amps_count(), s.amps_count());
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
+sd_status sd_exact_evolve(sd_state* h, const uint64_t* x, const uint64_t* z, const double* coeffs, size_t n_terms,
+                          double t) {
+    return guard([&] {
+        sdb::StateImpl& s = st(h);
+        require_unsharded(s);
+        if (s.n > 12) throw std::invalid_argument("exact_evolve limited to n <= 12 qubits");
+        require(n_terms == 0 || (x && z && coeffs), "null term arrays");
+        if (!std::isfinite(t)) throw std::invalid_argument("exact_evolve: non-finite time");
+        check_term_masks(one_shard(h), x, z, n_terms, "hamiltonian/state qubit counts differ");
+        require_identity_layout(s);
+        SDB_CUDA(cudaSetDevice(s.device));
+        sdb::launch_exact_evolve(s, x, z, coeffs, n_terms, t);
+        SDB_CUDA(cudaStreamSynchronize(s.stream));
+    });
+}
+
+}  // extern "C"
+

@@ -9,6 +9,7 @@
 #include "guard.hpp"
 #include "simdiag/diagonalize.hpp"
 #include "simdiag/hamiltonian.hpp"
+#include "simdiag/models.hpp"
 
 struct sd_hamiltonian {
     simdiag::Hamiltonian h;
@@ -71,6 +72,28 @@ extern "C" {
 
 const char* sd_last_error(void) { return sdb::last_error(); }
 const char* sd_version(void) { return "simdiag-b200 0.1 (sm_100a)"; }
+
+sd_status sd_gen_tfim(int n_qubits, uint64_t seed, sd_hamiltonian** out) {
+    return guard([&] {
+        require(out != nullptr, "out is null");
+        auto h = std::make_unique<sd_hamiltonian>();
+        h->h = simdiag::gen_tfim(n_qubits, seed);
+        *out = h.release();
+    });
+}
+
+sd_status sd_gen_syk(int n_qubits, uint64_t seed, size_t* candidate_quadruples, size_t* merge_collisions,
+                     sd_hamiltonian** out) {
+    return guard([&] {
+        require(out != nullptr, "out is null");
+        simdiag::SykInfo info;
+        auto h = std::make_unique<sd_hamiltonian>();
+        h->h = simdiag::gen_syk(n_qubits, seed, &info);
+        if (candidate_quadruples) *candidate_quadruples = info.candidate_quadruples;
+        if (merge_collisions) *merge_collisions = info.merge_collisions;
+        *out = h.release();
+    });
+}
 
 sd_status sd_hamiltonian_from_terms(int n_qubits, const uint64_t* x, const uint64_t* z, const double* c,
                                     size_t m, double tol, size_t* merged, sd_hamiltonian** out) {

@@ -37,6 +37,7 @@ struct NcclApi {
     ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     const char* (*errorString)(ncclResult_t) = nullptr;
 };
 
@@ -63,6 +64,7 @@ const NcclApi& nccl() {
         sym(api.send, "ncclSend");
         sym(api.recv, "ncclRecv");
         sym(api.allReduce, "ncclAllReduce");
+        sym(api.allGather, "ncclAllGather");
         sym(api.errorString, "ncclGetErrorString");
     });
     if (!err.empty()) throw NcclError(err);
@@ -151,6 +153,33 @@ double nccl_sum(StateImpl& s, double v) {
     SDB_CUDA(cudaMemcpyAsync(&v, d, sizeof(double), cudaMemcpyDeviceToHost, s.stream));
     SDB_CUDA(cudaStreamSynchronize(s.stream));
     return v;
+}
+
+std::vector<double> nccl_gather(StateImpl& s, const std::vector<double>& local) {
+    if (!s.nccl) throw std::runtime_error("sharded state has no communicator (sd_state_attach_comm)");
+    const size_t m = local.size();
+    std::vector<double> out(m * static_cast<size_t>(s.world));
+    if (m == 0) return out;
+    double* d = nullptr;
+    SDB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(double) * m * (1 + s.world), s.stream));
+    SDB_CUDA(cudaMemcpyAsync(d, local.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s.stream));
+    nccl_check(nccl().allGather(d, d + m, m, ncclDouble, static_cast<ncclComm_t>(s.nccl), s.stream), "ncclAllGather");
+    SDB_CUDA(cudaMemcpyAsync(out.data(), d + m, sizeof(double) * out.size(), cudaMemcpyDeviceToHost, s.stream));
+    SDB_CUDA(cudaFreeAsync(d, s.stream));
+    SDB_CUDA(cudaStreamSynchronize(s.stream));
+    return out;
+}
+
+void nccl_copy_partner(StateImpl& s, int partner) {
+    if (!s.nccl) throw std::runtime_error("sharded state has no communicator (sd_state_attach_comm)");
+    if (!s.xbuf) throw std::logic_error("partner copy needs the exchange buffer");
+    const NcclApi& a = nccl();
+    auto comm = static_cast<ncclComm_t>(s.nccl);
+    const size_t count = 2 * s.amps_count();
+    nccl_check(a.groupStart(), "ncclGroupStart");
+    nccl_check(a.send(s.amps, count, ncclDouble, partner, comm, s.stream), "ncclSend");
+    nccl_check(a.recv(s.xbuf, count, ncclDouble, partner, comm, s.stream), "ncclRecv");
+    nccl_check(a.groupEnd(), "ncclGroupEnd");
 }
 
 void exchange_nccl(StateImpl& s, const ExchangeSpec& ex) {

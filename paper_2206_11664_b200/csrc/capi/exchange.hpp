@@ -15,6 +15,11 @@ void nccl_detach(StateImpl& s);
 void nccl_barrier(StateImpl& s);
 // sum of v over all ranks of the state's communicator
 double nccl_sum(StateImpl& s, double v);
+// all-gather of a small host vector: result[r * size + i] = rank r's local[i]
+std::vector<double> nccl_gather(StateImpl& s, const std::vector<double>& local);
+// whole-shard copy of rank `partner` into s.xbuf (every rank calls it with its
+// own partner; partner(partner(r)) == r), stream-ordered
+void nccl_copy_partner(StateImpl& s, int partner);
 // Chunk routing of one exchange for `rank` (offsets and counts in amplitudes):
 // send B[send_off, +count) to `peer`, receive into A[recv_off, +count);
 // peer == rank is a local copy. Both transports use exactly this.

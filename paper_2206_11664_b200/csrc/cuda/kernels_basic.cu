@@ -8,6 +8,7 @@
 // amplitude pairs with 16-byte vector loads.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -114,16 +115,19 @@ __global__ void k_reduce(const double2* __restrict__ a, const double2* __restric
 
 // <psi| P |psi> partial sums for one Pauli term P = i^{phase} X^x Z^z
 // (expectation, reference evolve.cpp:99-135): sum_b conj(psi[b]) ph(b) psi[b^x],
-// ph(b) = base * (-1)^{popc((b^x) & z)}; same fixed-order block partials as k_reduce.
-__global__ void k_expect(const double2* __restrict__ a, uint64_t n, uint64_t x, uint64_t z, double2 base,
-                         double2* __restrict__ partial) {
+// ph(b) = base * (-1)^{popc((b^x) & z)}; same fixed-order block partials as
+// k_reduce. Sharded: b = rank_bits | i over this shard, psi[b^x] is element
+// i ^ x_lo of `p` (this shard, or a copy of shard rank ^ x_hi when x has
+// global bits); x and z are physical masks including the global bits.
+__global__ void k_expect(const double2* __restrict__ a, const double2* __restrict__ p, uint64_t n, uint64_t x_lo,
+                         uint64_t x, uint64_t z, uint64_t rank_bits, double2 base, double2* __restrict__ partial) {
     __shared__ double2 red[kThreads];
     double sr = 0.0, si = 0.0;
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
         const double2 u = a[i];
-        const double2 w = a[i ^ x];
-        const bool odd = __popcll((i ^ x) & z) & 1;
+        const double2 w = p[i ^ x_lo];
+        const bool odd = __popcll(((rank_bits | i) ^ x) & z) & 1;
         const double pr = odd ? -base.x : base.x, pi = odd ? -base.y : base.y;
         const double tr = pr * w.x - pi * w.y, ti = pr * w.y + pi * w.x;  // ph * psi[b^x]
         sr += u.x * tr + u.y * ti;                                        // conj(psi[b]) * (...)
@@ -141,16 +145,101 @@ __global__ void k_expect(const double2* __restrict__ a, uint64_t n, uint64_t x, 
     if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
 }
 
+// exp(-i theta P) on a shard whose partner amplitudes b^x live on another
+// rank (x has global bits): new[b] = cos(theta) a[b] + (-1)^{popc((b^x)&z)} w
+// a[b^x], the per-amplitude form of the reference's pair update
+// (statevector.cpp:313-333), with a[b^x] = element i ^ x_lo of p, a copy of
+// shard rank ^ x_hi taken before the update.
+__global__ void k_pauli_rotation_remote(double2* __restrict__ a, const double2* __restrict__ p, uint64_t n,
+                                        uint64_t x_lo, uint64_t x, uint64_t z, uint64_t rank_bits, double c,
+                                        double2 w) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const bool par = __popcll(((rank_bits | i) ^ x) & z) & 1;
+        const double2 wi = par ? make_double2(-w.x, -w.y) : w;
+        const double2 a0 = a[i], a1 = p[i ^ x_lo];
+        a[i] = make_double2(c * a0.x + (wi.x * a1.x - wi.y * a1.y), c * a0.y + (wi.x * a1.y + wi.y * a1.x));
+    }
+}
+
+// One Taylor term of exact_evolve: nxt = f * H cur, acc += nxt, with H the
+// Pauli sum (H cur)[b'] = sum_k c_k i^{s_k} (-1)^{popc(z_k & (b' ^ x_k))}
+// cur[b' ^ x_k] (P|b> = i^s (-1)^{<z,b>} |b^x>, reference evolve.cpp:70-79).
+__global__ void k_taylor_term(const double2* __restrict__ cur, double2* __restrict__ nxt, double2* __restrict__ acc,
+                              uint64_t n, const uint64_t* __restrict__ xm, const uint64_t* __restrict__ zm,
+                              const double2* __restrict__ cb, int m, double2 f) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        double sr = 0.0, si = 0.0;
+        for (int k = 0; k < m; ++k) {
+            const uint64_t x = __ldg(xm + k);
+            const double2 b = __ldg(cb + k);
+            const double2 v = cur[i ^ x];
+            const double sg = (__popcll(__ldg(zm + k) & (i ^ x)) & 1) ? -1.0 : 1.0;
+            sr += sg * (b.x * v.x - b.y * v.y);
+            si += sg * (b.x * v.y + b.y * v.x);
+        }
+        const double2 t = make_double2(f.x * sr - f.y * si, f.x * si + f.y * sr);
+        nxt[i] = t;
+        acc[i] = make_double2(acc[i].x + t.x, acc[i].y + t.y);
+    }
+}
+
+// apply_single_qubit (reference statevector.cpp:101-122): one sweep over the
+// pairs (i0, i0|t), u row-major 2x2 complex.
+struct Mat2D {
+    double2 u[4];
+};
+struct Mat4D {
+    double2 u[16];
+};
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cadd2(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+
+__global__ void k_single_qubit(double2* __restrict__ a, uint64_t pairs, int t, Mat2D m) {
+    const uint64_t tb = 1ull << t;
+    for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < pairs;
+         q += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i0 = insert_zero(q, t), i1 = i0 | tb;
+        const double2 a0 = a[i0], a1 = a[i1];
+        a[i0] = cadd2(cmul(m.u[0], a0), cmul(m.u[1], a1));
+        a[i1] = cadd2(cmul(m.u[2], a0), cmul(m.u[3], a1));
+    }
+}
+
+// apply_two_qubit (reference statevector.cpp:124-154): local index
+// 2*bit(q1) + bit(q2); row r accumulates u[r][0] v0 + u[r][1] v1 + ... in order.
+__global__ void k_two_qubit(double2* __restrict__ a, uint64_t quads, int lo, int hi, uint64_t b1, uint64_t b2,
+                            Mat4D m) {
+    for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < quads;
+         q += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i00 = insert_zero(insert_zero(q, lo), hi);
+        const uint64_t idx[4] = {i00, i00 | b2, i00 | b1, i00 | b1 | b2};
+        double2 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = a[idx[k]];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            double2 acc = cmul(m.u[r * 4], v[0]);
+#pragma unroll
+            for (int k = 1; k < 4; ++k) acc = cadd2(acc, cmul(m.u[r * 4 + k], v[k]));
+            a[idx[r]] = acc;
+        }
+    }
+}
+
 // apply_pauli_rotation (reference statevector.cpp:288-337): exp(-i theta P).
 // x == 0: a[b] *= (cos, -+sin) by the parity of b & z; otherwise over pairs
 // (b, b^x): a0' = c a0 + w0 a1, a1' = c a1 + w1 a0 with w = -i sin(theta) i^{phase}
 // and its sign from the parities of the pair's z bits.
 __global__ void k_pauli_rotation(double2* __restrict__ a, uint64_t n, uint64_t x, uint64_t z, double c, double s,
-                                 double2 w, int t0, int y_parity) {
+                                 double2 w, int t0, int y_parity, uint64_t rank_bits) {
     if (x == 0) {
         for (uint64_t b = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; b < n;
              b += uint64_t(gridDim.x) * blockDim.x) {
-            const bool odd = __popcll(b & z) & 1;
+            const bool odd = __popcll((rank_bits | b) & z) & 1;
             const double fr = c, fi = odd ? s : -s;
             const double2 v = a[b];
             a[b] = make_double2(v.x * fr - v.y * fi, v.x * fi + v.y * fr);
@@ -162,7 +251,7 @@ __global__ void k_pauli_rotation(double2* __restrict__ a, uint64_t n, uint64_t x
          p += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t i0 = insert_zero(p, t0);
         const uint64_t i1 = i0 ^ x;
-        const bool par0 = __popcll(i0 & z) & 1;
+        const bool par0 = __popcll((rank_bits | i0) & z) & 1;
         const bool par1 = par0 ^ (y_parity != 0);
         const double2 w0 = par1 ? make_double2(-w.x, -w.y) : w;
         const double2 w1 = par0 ? make_double2(-w.x, -w.y) : w;
@@ -374,9 +463,8 @@ void launch_diag_exp(StateImpl& s, const std::vector<uint64_t>& masks,
     if (dc) SDB_CUDA(cudaFreeAsync(dc, s.stream));
 }
 
-void launch_pauli_rotation(StateImpl& s, uint64_t x, uint64_t z, double coeff, double dt) {
-    const double theta = coeff * dt;
-    const double c = std::cos(theta), sn = std::sin(theta);
+namespace {
+double2 rotation_w(uint64_t x, uint64_t z, double sn) {
     // w = -i sin(theta) * i^{phase_exp}, phase_exp = popc(x & z) & 3 (pauli.cpp:64-66)
     double wr = 0.0, wi = -sn;
     const int ph = __builtin_popcountll(x & z) & 3;
@@ -385,22 +473,41 @@ void launch_pauli_rotation(StateImpl& s, uint64_t x, uint64_t z, double coeff, d
         wr = -wi;
         wi = t;
     }
+    return make_double2(wr, wi);
+}
+}  // namespace
+
+void launch_pauli_rotation(StateImpl& s, uint64_t x, uint64_t z, double coeff, double dt, const double* partner) {
+    const double theta = coeff * dt;
+    const double c = std::cos(theta), sn = std::sin(theta);
+    const double2 w = rotation_w(x, z, sn);
     const uint64_t n = s.amps_count();
-    const int t0 = x ? __builtin_ctzll(x) : 0;
-    const int ypar = __builtin_popcountll(z & x) & 1;
-    k_pauli_rotation<<<grid_for(x ? n >> 1 : n), kThreads, 0, s.stream>>>(d2(s), n, x, z, c, sn, make_double2(wr, wi),
-                                                                         t0, ypar);
+    const uint64_t rank_bits = uint64_t(s.rank) << s.n_local;
+    const uint64_t x_lo = x & (n - 1);
+    if (x >> s.n_local) {
+        if (!partner) throw std::logic_error("pauli rotation across shards needs the partner shard");
+        k_pauli_rotation_remote<<<grid_for(n), kThreads, 0, s.stream>>>(
+            d2(s), reinterpret_cast<const double2*>(partner), n, x_lo, x, z, rank_bits, c, w);
+    } else {
+        const int t0 = x ? __builtin_ctzll(x) : 0;
+        const int ypar = __builtin_popcountll(z & x) & 1;
+        k_pauli_rotation<<<grid_for(x ? n >> 1 : n), kThreads, 0, s.stream>>>(d2(s), n, x, z, c, sn, w, t0, ypar,
+                                                                             rank_bits);
+    }
     SDB_CUDA(cudaGetLastError());
 }
 
-void device_expectation_term(StateImpl& s, uint64_t x, uint64_t z, double* re, double* im) {
+void device_expectation_term(StateImpl& s, uint64_t x, uint64_t z, const double* partner, double* re, double* im) {
     const uint64_t n = s.amps_count();
     const unsigned blocks = grid_for(n);
     if (!s.reduce_buf) SDB_CUDA(cudaMalloc(reinterpret_cast<void**>(&s.reduce_buf), 148 * 16 * sizeof(double2)));
     double2* part = reinterpret_cast<double2*>(s.reduce_buf);
     const int ph = __builtin_popcountll(x & z) & 3;
     const double2 base[4] = {{1, 0}, {0, 1}, {-1, 0}, {0, -1}};
-    k_expect<<<blocks, kThreads, 0, s.stream>>>(d2(s), n, x, z, base[ph], part);
+    const double2* p = (x >> s.n_local) ? reinterpret_cast<const double2*>(partner) : d2(s);
+    if (!p) throw std::logic_error("expectation across shards needs the partner shard");
+    k_expect<<<blocks, kThreads, 0, s.stream>>>(d2(s), p, n, x & (n - 1), x, z, uint64_t(s.rank) << s.n_local,
+                                                base[ph], part);
     SDB_CUDA(cudaGetLastError());
     std::vector<double2> h(blocks);
     SDB_CUDA(cudaMemcpyAsync(h.data(), part, blocks * sizeof(double2), cudaMemcpyDeviceToHost, s.stream));
@@ -418,6 +525,61 @@ void device_expectation_term(StateImpl& s, uint64_t x, uint64_t z, double* re, d
     }
     *re = h[0].x;
     *im = h[0].y;
+}
+
+// exact_evolve (reference evolve.cpp:60-97) for n <= 12: psi <- exp(-i H t)
+// psi by a Taylor series, time-sliced so each slice has ||H dt|| <= 1/2
+// (||H|| <= sum |c_k|) and truncated at 24 terms (remainder < 2^-24/24! ~ 1e-31
+// of the slice's norm); the reference diagonalises the dense matrix instead.
+void launch_exact_evolve(StateImpl& s, const uint64_t* x, const uint64_t* z, const double* c, size_t m, double t) {
+    const uint64_t n = s.amps_count();
+    double hnorm = 0.0;
+    std::vector<double2> cb(m);
+    for (size_t k = 0; k < m; ++k) {
+        hnorm += std::fabs(c[k]);
+        const int ph = __builtin_popcountll(x[k] & z[k]) & 3;
+        const double2 ip[4] = {{1, 0}, {0, 1}, {-1, 0}, {0, -1}};
+        cb[k] = make_double2(c[k] * ip[ph].x, c[k] * ip[ph].y);
+    }
+    if (m == 0 || t == 0.0) return;
+    const int slices = std::max(1, static_cast<int>(std::ceil(2.0 * hnorm * std::fabs(t))));
+    const double dt = t / slices;
+    uint64_t* dx = upload_scratch(std::vector<uint64_t>(x, x + m), s.stream);
+    uint64_t* dz = upload_scratch(std::vector<uint64_t>(z, z + m), s.stream);
+    double2* dc = upload_scratch(cb, s.stream);
+    double2* buf = nullptr;
+    SDB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), 2 * n * sizeof(double2), s.stream));
+    for (int sl = 0; sl < slices; ++sl) {
+        SDB_CUDA(cudaMemcpyAsync(buf, s.amps, n * sizeof(double2), cudaMemcpyDeviceToDevice, s.stream));
+        for (int j = 1; j <= 24; ++j) {
+            const double2 f = make_double2(0.0, -dt / j);  // (-i dt) / j
+            const double2* cur = buf + ((j - 1) & 1) * n;
+            double2* nxt = buf + (j & 1) * n;
+            k_taylor_term<<<grid_for(n), kThreads, 0, s.stream>>>(cur, nxt, d2(s), n, dx, dz, dc, static_cast<int>(m), f);
+            SDB_CUDA(cudaGetLastError());
+        }
+    }
+    SDB_CUDA(cudaFreeAsync(buf, s.stream));
+    SDB_CUDA(cudaFreeAsync(dx, s.stream));
+    SDB_CUDA(cudaFreeAsync(dz, s.stream));
+    SDB_CUDA(cudaFreeAsync(dc, s.stream));
+}
+
+void launch_single_qubit(StateImpl& s, const double* u, int t) {
+    Mat2D m;
+    for (int k = 0; k < 4; ++k) m.u[k] = make_double2(u[2 * k], u[2 * k + 1]);
+    const uint64_t pairs = s.amps_count() >> 1;
+    k_single_qubit<<<grid_for(pairs), kThreads, 0, s.stream>>>(d2(s), pairs, t, m);
+    SDB_CUDA(cudaGetLastError());
+}
+
+void launch_two_qubit(StateImpl& s, const double* u, int q1, int q2) {
+    Mat4D m;
+    for (int k = 0; k < 16; ++k) m.u[k] = make_double2(u[2 * k], u[2 * k + 1]);
+    const uint64_t quads = s.amps_count() >> 2;
+    const int lo = q1 < q2 ? q1 : q2, hi = q1 < q2 ? q2 : q1;
+    k_two_qubit<<<grid_for(quads), kThreads, 0, s.stream>>>(d2(s), quads, lo, hi, 1ull << q1, 1ull << q2, m);
+    SDB_CUDA(cudaGetLastError());
 }
 
 void launch_permute_bits(StateImpl& s, const double* src, double* dst, const int* new_pos_host,

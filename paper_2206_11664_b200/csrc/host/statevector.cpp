@@ -17,6 +17,17 @@
 
 namespace simdiag {
 
+// evolve_grouped's compiled schedules (sd_plan) for one state, keyed by the
+// exact bytes of the group list and the Trotter order: a caller that steps and
+// measures in a loop plans once. Bounded, least recently used first out.
+struct PlanCache {
+    static constexpr size_t kMax = 4;
+    std::vector<std::pair<std::string, sd_plan*>> entries;  // most recent last
+    ~PlanCache() {
+        for (auto& e : entries) sd_plan_destroy(e.second);
+    }
+};
+
 namespace {
 
 void check(sd_status st) {
@@ -62,22 +73,30 @@ StateVector::StateVector(int n_qubits, int device) : n_qubits_(n_qubits) {
     check(sd_state_create(n_qubits, device, &s_));
 }
 
-StateVector::~StateVector() { sd_state_destroy(s_); }
+StateVector::~StateVector() {
+    delete plans_;  // plans reference the state: destroyed first
+    sd_state_destroy(s_);
+}
 
 StateVector::StateVector(StateVector&& o) noexcept
-    : n_qubits_(o.n_qubits_), s_(o.s_), host_(std::move(o.host_)), host_valid_(o.host_valid_), host_dirty_(o.host_dirty_) {
+    : n_qubits_(o.n_qubits_), s_(o.s_), host_(std::move(o.host_)), host_valid_(o.host_valid_), host_dirty_(o.host_dirty_),
+      plans_(o.plans_) {
     o.s_ = nullptr;
+    o.plans_ = nullptr;
 }
 
 StateVector& StateVector::operator=(StateVector&& o) noexcept {
     if (this != &o) {
+        delete plans_;
         sd_state_destroy(s_);
         n_qubits_ = o.n_qubits_;
         s_ = o.s_;
         host_ = std::move(o.host_);
         host_valid_ = o.host_valid_;
         host_dirty_ = o.host_dirty_;
+        plans_ = o.plans_;
         o.s_ = nullptr;
+        o.plans_ = nullptr;
     }
     return *this;
 }
@@ -126,6 +145,19 @@ Amplitude& StateVector::operator[](std::uint64_t i) {
 const Amplitude& StateVector::operator[](std::uint64_t i) const {
     fetch();
     return host_.at(i);
+}
+
+void StateVector::apply_single_qubit(const Mat2& u, int target) {
+    check(sd_apply_single_qubit(sync_to_device(), reinterpret_cast<const double*>(u.data()), target));
+}
+
+void StateVector::apply_two_qubit(const Mat4& u, int q1, int q2) {
+    check(sd_apply_two_qubit(sync_to_device(), reinterpret_cast<const double*>(u.data()), q1, q2));
+}
+
+void StateVector::apply_pauli_rotation(const WeightedTerm& term, double dt) {
+    if (term.pauli.n_qubits() != n_qubits_) throw std::invalid_argument("pauli rotation: qubit count mismatch");
+    check(sd_apply_pauli_rotation(sync_to_device(), term.pauli.x_mask(), term.pauli.z_mask(), term.coeff, dt));
 }
 
 void StateVector::apply_hadamard(int target) { check(sd_apply_hadamard(sync_to_device(), target)); }
@@ -210,20 +242,121 @@ void EvolutionPlan::validate() const {
     if (order != 1 && order != 2) throw std::invalid_argument("trotter order must be 1 or 2");
 }
 
+namespace {
+
+void append_bytes(std::string& k, const void* p, size_t n) { k.append(static_cast<const char*>(p), n); }
+
+std::string plan_key(std::span<const DiagonalGroup> groups, int order) {
+    std::string k;
+    append_bytes(k, &order, sizeof order);
+    for (const DiagonalGroup& g : groups) {
+        const CliffordCircuit& c = g.circuit;
+        const size_t sizes[6] = {c.h_pre.size(), c.cnots.size(), c.czs.size(), c.s_layer.size(), c.h_post.size(),
+                                 g.z_masks.size()};
+        append_bytes(k, sizes, sizeof sizes);
+        append_bytes(k, &c.n_qubits, sizeof c.n_qubits);
+        append_bytes(k, c.h_pre.data(), c.h_pre.size() * sizeof(int));
+        append_bytes(k, c.cnots.data(), c.cnots.size() * sizeof(c.cnots[0]));
+        append_bytes(k, c.czs.data(), c.czs.size() * sizeof(c.czs[0]));
+        append_bytes(k, c.s_layer.data(), c.s_layer.size() * sizeof(int));
+        append_bytes(k, c.h_post.data(), c.h_post.size() * sizeof(int));
+        append_bytes(k, g.z_masks.data(), g.z_masks.size() * sizeof(std::uint64_t));
+        append_bytes(k, g.signed_coeffs.data(), g.signed_coeffs.size() * sizeof(double));
+    }
+    return k;
+}
+
+struct TermArrays {
+    std::vector<std::uint64_t> x, z;
+    std::vector<double> c;
+    void add(const WeightedTerm& t) {
+        x.push_back(t.pauli.x_mask());
+        z.push_back(t.pauli.z_mask());
+        c.push_back(t.coeff);
+    }
+};
+
+TermArrays arrays_of(const Hamiltonian& h) {
+    TermArrays a;
+    for (const WeightedTerm& t : h.terms()) a.add(t);
+    return a;
+}
+
+}  // namespace
+
 void evolve_grouped(std::span<const DiagonalGroup> groups, StateVector& psi, const EvolutionPlan& plan) {
     plan.validate();
     if (plan.n_steps == 0) return;
-    std::deque<std::vector<int32_t>> keep;  // stable element addresses
-    std::vector<sd_group_desc> descs;
-    for (const DiagonalGroup& g : groups) descs.push_back(desc_of(g, keep));
-    sd_plan_options o;
-    check(sd_plan_options_default(&o));
-    o.order = plan.order;
+    sd_state* h = psi.handle();
+    if (!psi.plans_) psi.plans_ = new PlanCache();
+    PlanCache& cache = *psi.plans_;
+    const std::string key = plan_key(groups, plan.order);
     sd_plan* p = nullptr;
-    check(sd_plan_create(psi.handle(), descs.data(), descs.size(), &o, &p));
-    const sd_status st = sd_evolve(p, plan.dt(), plan.n_steps);
-    sd_plan_destroy(p);
-    check(st);
+    for (size_t i = 0; i < cache.entries.size(); ++i) {
+        if (cache.entries[i].first == key) {
+            auto e = cache.entries[i];
+            cache.entries.erase(cache.entries.begin() + static_cast<std::ptrdiff_t>(i));
+            cache.entries.push_back(e);
+            p = e.second;
+            break;
+        }
+    }
+    if (!p) {
+        std::deque<std::vector<int32_t>> keep;  // stable element addresses
+        std::vector<sd_group_desc> descs;
+        for (const DiagonalGroup& g : groups) descs.push_back(desc_of(g, keep));
+        sd_plan_options o;
+        check(sd_plan_options_default(&o));
+        o.order = plan.order;
+        check(sd_plan_create(h, descs.data(), descs.size(), &o, &p));
+        if (cache.entries.size() >= PlanCache::kMax) {
+            sd_plan_destroy(cache.entries.front().second);
+            cache.entries.erase(cache.entries.begin());
+        }
+        cache.entries.emplace_back(key, p);
+    }
+    check(sd_evolve(p, plan.dt(), plan.n_steps));
+}
+
+void evolve_baseline(const Hamiltonian& h, StateVector& psi, const EvolutionPlan& plan) {
+    plan.validate();
+    if (h.n_qubits() != psi.n_qubits()) throw std::invalid_argument("hamiltonian/state qubit counts differ");
+    const TermArrays a = arrays_of(h);
+    const double dt = plan.n_steps > 0 ? plan.dt() : 0.0;
+    check(sd_evolve_baseline(psi.handle(), a.x.data(), a.z.data(), a.c.data(), a.c.size(), dt, plan.n_steps));
+}
+
+void evolve_baseline(std::span<const CommutingGroup> groups, StateVector& psi, const EvolutionPlan& plan) {
+    plan.validate();
+    TermArrays a;
+    for (const CommutingGroup& g : groups)
+        for (const WeightedTerm& t : g.terms) a.add(t);
+    const double dt = plan.n_steps > 0 ? plan.dt() : 0.0;
+    check(sd_evolve_baseline(psi.handle(), a.x.data(), a.z.data(), a.c.data(), a.c.size(), dt, plan.n_steps));
+}
+
+StateVector exact_evolve(const Hamiltonian& h, const StateVector& psi, double t) {
+    const int n = h.n_qubits();
+    if (n != psi.n_qubits()) throw std::invalid_argument("hamiltonian/state qubit counts differ");
+    if (n > kExactEvolveMaxQubits) {
+        throw std::invalid_argument("exact_evolve limited to n <= " + std::to_string(kExactEvolveMaxQubits) +
+                                    " qubits");
+    }
+    StateVector out(n);
+    check(sd_state_copy(out.handle(), const_cast<StateVector&>(psi).handle()));
+    const TermArrays a = arrays_of(h);
+    check(sd_exact_evolve(out.handle(), a.x.data(), a.z.data(), a.c.data(), a.c.size(), t));
+    return out;
+}
+
+double expectation(const Hamiltonian& h, const StateVector& psi, double* imag_residue) {
+    if (h.n_qubits() != psi.n_qubits()) throw std::invalid_argument("hamiltonian/state qubit counts differ");
+    const TermArrays a = arrays_of(h);
+    double re = 0.0, im = 0.0;
+    check(sd_expectation(const_cast<StateVector&>(psi).handle(), a.x.data(), a.z.data(), a.c.data(), a.c.size(), &re,
+                         &im));
+    if (imag_residue) *imag_residue = im;
+    return re;
 }
 
 }  // namespace simdiag

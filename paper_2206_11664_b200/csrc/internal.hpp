@@ -77,9 +77,18 @@ void launch_diag_exp(StateImpl& s, const std::vector<uint64_t>& masks,
 void launch_permute_bits(StateImpl& s, const double* src, double* dst, const int* new_pos,
                          int n_bits);
 // apply_pauli_rotation (statevector.cpp:288-337) and one term of expectation
-// (evolve.cpp:99-135): <psi| i^{phase} X^x Z^z |psi>
-void launch_pauli_rotation(StateImpl& s, uint64_t x, uint64_t z, double coeff, double dt);
-void device_expectation_term(StateImpl& s, uint64_t x, uint64_t z, double* re, double* im);
+// (evolve.cpp:99-135): <psi| i^{phase} X^x Z^z |psi>. x and z are PHYSICAL
+// masks including the global (rank) bits; when x has global bits, `partner`
+// is a copy of shard rank ^ (x >> n_local) taken before the update.
+void launch_pauli_rotation(StateImpl& s, uint64_t x, uint64_t z, double coeff, double dt,
+                           const double* partner = nullptr);
+void device_expectation_term(StateImpl& s, uint64_t x, uint64_t z, const double* partner, double* re, double* im);
+// apply_single_qubit / apply_two_qubit (statevector.cpp:101-154); u holds
+// row-major complex entries as (re, im) pairs; physical qubit positions.
+void launch_single_qubit(StateImpl& s, const double* u, int target);
+void launch_two_qubit(StateImpl& s, const double* u, int q1, int q2);
+// exact_evolve (evolve.cpp:60-97): psi <- exp(-i H t) psi, H = sum_k c_k P_k
+void launch_exact_evolve(StateImpl& s, const uint64_t* x, const uint64_t* z, const double* c, size_t m, double t);
 
 // Fused pass launcher (pass_kernel.cu).
 // out: destination buffer (nullptr = in place on s.amps); xdst: device table of

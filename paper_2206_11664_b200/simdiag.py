@@ -183,6 +183,23 @@ class Hamiltonian:
         return [WeightedTerm(float(ci), PauliString(n, int(xi), int(zi))) for xi, zi, ci in zip(x, z, c)]
 
 
+def gen_tfim(n_qubits: int, seed: int) -> Hamiltonian:
+    """Fully connected TFIM (models.hpp:13, models.cpp:17-35)."""
+    out = C.c_void_p()
+    check(A.sd_gen_tfim(n_qubits, seed, C.byref(out)))
+    return Hamiltonian(out.value)
+
+
+def gen_syk(n_qubits: int, seed: int, with_info: bool = False):
+    """SYK quartic Majorana model over 2n modes (models.hpp:29-34,
+    models.cpp:48-90); with_info adds (candidate_quadruples, merge_collisions)."""
+    out = C.c_void_p()
+    q, col = C.c_size_t(0), C.c_size_t(0)
+    check(A.sd_gen_syk(n_qubits, seed, C.byref(q), C.byref(col), C.byref(out)))
+    h = Hamiltonian(out.value)
+    return (h, (q.value, col.value)) if with_info else h
+
+
 # ----------------------------------------------------------------- circuits
 
 
@@ -377,7 +394,13 @@ class StateVector:
         return v.value
 
     def norm(self) -> float:
-        return math.sqrt(self.norm_sq_local())
+        """norm() of the whole state (statevector.cpp:403-407); for a shard of
+        a multi-process state this is collective over the communicator."""
+        if self.world == 1:
+            return math.sqrt(self.norm_sq_local())
+        v = C.c_double()
+        check(A.sd_state_norm(self._s, C.byref(v)))
+        return v.value
 
     def stats(self) -> dict:
         k = A.KernelStats()
@@ -457,18 +480,35 @@ class StateVector:
         check(A.sd_apply_clifford_inverse(self._s, C.byref(d)))
 
     def apply_pauli_rotation(self, term: WeightedTerm, dt: float) -> None:
-        """exp(-i coeff dt P) (statevector.cpp:288-337)."""
+        """exp(-i coeff dt P) (statevector.cpp:288-337); collective for a
+        shard of a multi-process state."""
         check(A.sd_apply_pauli_rotation(self._s, term.pauli.x_mask, term.pauli.z_mask, term.coeff, dt))
+
+    def apply_single_qubit(self, u, target: int) -> None:
+        """Generic 2x2 unitary (statevector.cpp:101-122), row-major."""
+        m = np.ascontiguousarray(np.asarray(u, dtype=np.complex128).reshape(4))
+        check(A.sd_apply_single_qubit(self._s, m.ctypes.data_as(C.POINTER(C.c_double)), target))
+
+    def apply_two_qubit(self, u, q1: int, q2: int) -> None:
+        """Generic 4x4 unitary (statevector.cpp:124-154); local index
+        2*bit(q1) + bit(q2)."""
+        m = np.ascontiguousarray(np.asarray(u, dtype=np.complex128).reshape(16))
+        check(A.sd_apply_two_qubit(self._s, m.ctypes.data_as(C.POINTER(C.c_double)), q1, q2))
 
 
 def norm(psi: StateVector) -> float:
     return psi.norm()
 
 
-def fidelity(a: StateVector, b: StateVector) -> float:
-    re, im = C.c_double(), C.c_double()
-    check(A.sd_state_inner(a._s, b._s, C.byref(re), C.byref(im)))
-    return math.hypot(re.value, im.value)
+def fidelity(a, b) -> float:
+    """|<a|b>| (statevector.cpp:409-418) of whole states: StateVectors
+    (collective for multi-process shards) or LocalShards."""
+    v = C.c_double()
+    if isinstance(a, LocalShards):
+        check(A.sd_local_fidelity(a._arr(), b._arr(), a.world, C.byref(v)))
+    else:
+        check(A.sd_state_fidelity(a._s, b._s, C.byref(v)))
+    return v.value
 
 
 # ----------------------------------------------------------------- evolution
@@ -587,10 +627,11 @@ def _term_arrays(terms):
     return xs, zs, cs
 
 
-def evolve_baseline(h, psi: StateVector, plan: EvolutionPlan) -> None:
+def evolve_baseline(h, psi, plan: EvolutionPlan) -> None:
     """The paper's per-term baseline (evolve.cpp:21-45): n_steps x one rotation
     sweep per term; `h` is a Hamiltonian (input order) or a list of
-    CommutingGroup/DiagonalGroup (group-major order)."""
+    CommutingGroup/DiagonalGroup (group-major order). `psi` is a StateVector
+    (collective for a multi-process shard) or LocalShards."""
     plan.validate()
     if isinstance(h, Hamiltonian):
         if h.n_qubits != psi.n:
@@ -600,19 +641,41 @@ def evolve_baseline(h, psi: StateVector, plan: EvolutionPlan) -> None:
         terms = [t for g in h for t in g.terms]
     dt = plan.dt() if plan.n_steps > 0 else 0.0
     xs, zs, cs = _term_arrays(terms)
-    check(A.sd_evolve_baseline(psi._s, xs, zs, cs, len(terms), dt, plan.n_steps))
+    if isinstance(psi, LocalShards):
+        check(A.sd_local_evolve_baseline(psi._arr(), psi.world, xs, zs, cs, len(terms), dt, plan.n_steps))
+    else:
+        check(A.sd_evolve_baseline(psi._s, xs, zs, cs, len(terms), dt, plan.n_steps))
 
 
-def expectation(h: "Hamiltonian", psi: StateVector, with_residue: bool = False):
+def expectation(h: "Hamiltonian", psi, with_residue: bool = False):
     """<psi|H|psi> (evolve.cpp:99-135) as device reductions; returns the real
-    part (and the |imaginary residue| when with_residue)."""
+    part (and the |imaginary residue| when with_residue). `psi` is a
+    StateVector (collective for a multi-process shard) or LocalShards."""
     if h.n_qubits != psi.n:
         raise ValueError("hamiltonian/state qubit counts differ")
     terms = h.terms()
     xs, zs, cs = _term_arrays(terms)
     re, im = C.c_double(), C.c_double()
-    check(A.sd_expectation(psi._s, xs, zs, cs, len(terms), C.byref(re), C.byref(im)))
+    if isinstance(psi, LocalShards):
+        check(A.sd_local_expectation(psi._arr(), psi.world, xs, zs, cs, len(terms), C.byref(re), C.byref(im)))
+    else:
+        check(A.sd_expectation(psi._s, xs, zs, cs, len(terms), C.byref(re), C.byref(im)))
     return (re.value, im.value) if with_residue else re.value
+
+
+K_EXACT_EVOLVE_MAX_QUBITS = 12
+
+
+def exact_evolve(h: "Hamiltonian", psi: StateVector, t: float) -> StateVector:
+    """exp(-i H t) psi for n <= 12 (evolve.cpp:60-97, the reference's dense
+    test oracle) as a new state; computed on the device."""
+    if h.n_qubits != psi.n:
+        raise ValueError("hamiltonian/state qubit counts differ")
+    out = StateVector(psi.n, device=psi.device)
+    check(A.sd_state_copy(out._s, psi._s))
+    xs, zs, cs = _term_arrays(h.terms())
+    check(A.sd_exact_evolve(out._s, xs, zs, cs, h.term_count(), t))
+    return out
 
 
 def comm_unique_id() -> bytes:
@@ -658,10 +721,21 @@ class LocalShards:
         arr = (C.c_void_p * self.world)(*[p._p.value for p in self.plans])
         check(A.sd_evolve_local(arr, self.world, dt, n_steps))
 
+    def _arr(self):
+        return (C.c_void_p * self.world)(*[s._s.value for s in self.shards])
+
     def amplitudes(self) -> np.ndarray:
-        arr = (C.c_void_p * self.world)(*[s._s.value for s in self.shards])
-        check(A.sd_local_canonicalize(arr, self.world))
+        check(A.sd_local_canonicalize(self._arr(), self.world))
         return np.concatenate([s.amplitudes() for s in self.shards])
+
+    def norm(self) -> float:
+        v = C.c_double()
+        check(A.sd_local_norm(self._arr(), self.world, C.byref(v)))
+        return v.value
+
+    def apply_pauli_rotation(self, term: WeightedTerm, dt: float) -> None:
+        check(A.sd_local_apply_pauli_rotation(self._arr(), self.world, term.pauli.x_mask, term.pauli.z_mask,
+                                              term.coeff, dt))
 
 
 def exchange_routes(n_qubits: int, n_local: int, rank: int, swaps) -> List[Tuple[int, int, int, int]]:

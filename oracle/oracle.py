@@ -252,6 +252,7 @@ class Ref:
 
         L.ref_gen_save_text.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t),
                                         u64p]
+        L.ref_partition_timed.argtypes = [C.c_char_p, C.c_size_t, dblp, C.POINTER(C.c_size_t)]
         L.ref_generic_gate.argtypes = [dblp, C.c_int, dblp, C.c_int, C.c_int]
         L.ref_evolve_baseline_groups.argtypes = [C.c_void_p, dblp, C.c_int, C.c_double, C.c_int]
         L.ref_sv_create.argtypes = [C.c_int]
@@ -365,6 +366,13 @@ class Ref:
         buf = C.create_string_buffer(ln.value + 1)
         self._err(self.lib.ref_gen_save_text(which, n, seed, buf, ln.value + 1, C.byref(ln), _p(info, u64p)))
         return buf.value.decode(), (int(info[0]), int(info[1]))
+
+    def partition_timed(self, text: str):
+        """(seconds, n_groups) of greedy_partition alone on a loaded Hamiltonian."""
+        b = text.encode()
+        secs, ng = C.c_double(0), C.c_size_t(0)
+        self._err(self.lib.ref_partition_timed(b, len(b), C.byref(secs), C.byref(ng)))
+        return secs.value, ng.value
 
     def generic_gate(self, psi, n, u, q1, q2=-1):
         """apply_single_qubit (q2 < 0) / apply_two_qubit (statevector.cpp:101-154)."""

@@ -10,6 +10,7 @@
 // composition SURVEY §8a D1 defines (the reference has no S2).
 #include <algorithm>
 #include <bit>
+#include <chrono>
 #include <complex>
 #include <cstring>
 #include <memory>
@@ -113,6 +114,18 @@ int ref_gen_save_text(int model, int n, uint64_t seed, char* buf, size_t cap, si
             std::memcpy(buf, s.data(), k);
             buf[k] = 0;
         }
+    });
+}
+
+// greedy_partition alone (hamiltonian.cpp:135-158), timed: seconds and group count.
+int ref_partition_timed(const char* text, size_t len, double* secs, size_t* n_groups) {
+    return guarded([&] {
+        std::istringstream in(std::string(text, len));
+        const auto h = simdiag::Hamiltonian::load(in);
+        const auto t0 = std::chrono::steady_clock::now();
+        const auto parts = simdiag::greedy_partition(h);
+        *secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *n_groups = parts.size();
     });
 }
 

@@ -497,13 +497,19 @@ struct PassCtx {
         return r;
     }
 
-    __device__ __forceinline__ void phys_offsets(uint64_t (&o)[NR]) const {
-        o[0] = off_of(rc.tb);
+    // Register part of the physical offsets (the thread part is off_of(rc.tb)):
+    // local coordinates are distinct bits, so base | thread | register ==
+    // base + thread + register, and a tile address is one per-thread pointer
+    // plus a per-register offset (an immediate when the JIT bakes the
+    // config's offsets in).
+    __device__ __forceinline__ void reg_offsets(uint64_t (&o)[NR], const uint64_t (&coff)[4]) const {
+        o[0] = 0;
 #pragma unroll
         for (int j = 0; j < R; ++j)
 #pragma unroll
-            for (int s = 0; s < (1 << j); ++s) o[s + (1 << j)] = o[s] | rc.coff[j];
+            for (int s = 0; s < (1 << j); ++s) o[s + (1 << j)] = o[s] | coff[j];
     }
+
 
     __device__ __forceinline__ void slots(uint32_t (&a)[NR]) const {
         a[0] = rc.swt;
@@ -516,15 +522,17 @@ struct PassCtx {
     __device__ __forceinline__ void load(const RegCfg& r, double2 (&v)[NR]) {
         rc = r;
         uint64_t o[NR];
-        phys_offsets(o);
+        reg_offsets(o, rc.coff);
+        const uint64_t o0 = off_of(rc.tb);
+        const double2* gt = g + o0;
 #pragma unroll
-        for (int s = 0; s < NR; ++s) v[s] = SDB_TILE_LOAD(g + o[s]);
+        for (int s = 0; s < NR; ++s) v[s] = SDB_TILE_LOAD(gt + o[s]);
         // Pull this CTA's next tile into L2 while the current one is
         // transformed: HBM keeps streaming through the compute phase
         // without holding registers or shared memory.
 #ifndef SDB_NO_PREFETCH
         if (t + stride < t_last) {
-            const double2* gn = psi + tile_base(t + stride);
+            const double2* gn = psi + (tile_base(t + stride) + o0);
 #pragma unroll
             for (int s = 0; s < NR; ++s) prefetch_l2(gn + o[s]);
         }
@@ -805,22 +813,35 @@ struct PassCtx {
         }
     }
 
+    // STORE flags: the specialised kernels pass them as a template constant
+    // (F >= 0), so only the path the op takes is compiled; the interpreter
+    // decodes them from the staged op (F < 0).
+    static constexpr int kStPerm = 1, kStSigma = 2, kStScale = 4, kStSync = 8, kStXchg = 16;
+    __device__ __forceinline__ int store_flags(const MicroOpDev& op) const {
+        return (op.perm >= 0 ? kStPerm : 0) | (store_perm ? kStSigma : 0) | ((op.mask & 2u) ? kStScale : 0) |
+               ((op.mask & 4u) ? kStSync : 0) | (P.x_bits > 0 ? kStXchg : 0);
+    }
+
     __device__ __forceinline__ void store(const MicroOpDev& op, double2 (&v)[NR]) {
-        if (op.mask & 4u) __syncthreads();  // cross-warp in-place store with no barrier since the load
+        store_f<-1>(op, op.c_off, v);
+    }
+
+    // soff: sigma-mapped physical offsets of the register coordinates (kStSigma)
+    template <int F>
+    __device__ __forceinline__ void store_f(const MicroOpDev& op, const uint64_t (&soff)[4], double2 (&v)[NR]) {
+        const int f = F >= 0 ? F : store_flags(op);
+        if (f & kStSync) __syncthreads();  // cross-warp in-place store with no barrier since the load
         uint64_t o[NR];
         double2* go;
-        if (store_perm) {
+        if (f & kStSigma) {
             // sigma is a bit permutation: sigma(base | off) = sigma(base) | sigma(off)
             uint64_t sb = 0;
 #pragma unroll
             for (int c = 0; c < kTbaseChunks; ++c) sb |= st_tbase[c * 128 + ((t >> (7 * c)) & 127)];
             go = out + sb;
-            o[0] = st_lo[rc.tb & ((1u << LO) - 1u)] | st_hi[rc.tb >> LO];
-#pragma unroll
-            for (int j = 0; j < R; ++j)
-#pragma unroll
-                for (int s = 0; s < (1 << j); ++s) o[s + (1 << j)] = o[s] | op.c_off[j];
-        } else if (op.perm >= 0) {
+            go += st_lo[rc.tb & ((1u << LO) - 1u)] | st_hi[rc.tb >> LO];
+            reg_offsets(o, soff);
+        } else if (f & kStPerm) {
             // pending CNOT map applied by the addressing: register s (local
             // index l) goes to P(l) = swz(lo[l & 63] ^ hi[l >> 6] ^ b(h))
             go = out + base;
@@ -828,7 +849,6 @@ struct PassCtx {
             uint32_t sb = 0;
             for (int j = 0; j < pm->n_ctrl; ++j)
                 if ((full >> pm->ctrl_phys[j]) & 1ull) sb ^= pm->flip[j];
-            uint32_t l = rc.tb;
 #pragma unroll
             for (int s = 0; s < NR; ++s) {
                 uint32_t ls = rc.tb;
@@ -839,13 +859,12 @@ struct PassCtx {
                                        static_cast<uint32_t>(__ldg(&pm->hi[ls >> 6])) ^ sb);
                 o[s] = off_of(m);
             }
-            (void)l;
         } else {
-            go = out + base;
-            phys_offsets(o);
+            go = out + (base + off_of(rc.tb));
+            reg_offsets(o, rc.coff);
         }
-        const bool sc = (op.mask & 2u) != 0;
-        if (xdst && P.x_bits > 0) {
+        const bool sc = (f & kStScale) != 0;
+        if ((f & kStXchg) && xdst) {
             // fused exchange: every amplitude goes straight to its receiving
             // rank's buffer (peer memory over NVLink), at its final position
             const uint64_t sb = static_cast<uint64_t>(go - out);

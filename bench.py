@@ -463,7 +463,11 @@ def run_ours(args, rank, world, local_rank):
                    "l2": "state (16 GiB at n=30) >> 126 MB L2; no flush needed",
                    "tile_qubits": info["tile_qubits"], "passes_per_step": info["n_passes_per_step"],
                    "ref_sweeps_per_step": info["n_ref_sweeps_per_step"],
-                   "floor_group_applications": info["n_group_applications"]},
+                   "floor_group_applications": info["n_group_applications"],
+                   "schedule": ("per-term diagonal ops, <= 2 Hadamard levels per pass" if info["schedule"] == 1
+                                else "whole-group diagonal ops"),
+                   "autotune_ms_per_step": ({"whole_group": info["tune_ms_whole"], "per_term": info["tune_ms_split"]}
+                                            if info["tune_ms_whole"] > 0 else None)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": load_traffic(), "peak_source": peak_src,
                      "kernel": "fused Clifford/diagonal tile pass (sdb_pass: NVRTC-specialised per program for n_local >= 22; k_tile_pass interpreter otherwise)",

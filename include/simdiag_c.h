@@ -264,7 +264,11 @@ typedef struct sd_plan_options {
 
 sd_status sd_plan_options_default(sd_plan_options* o);
 /* groups: DiagonalGroups in evolution order (as passed to evolve_grouped).
- * Host data is copied. */
+ * Host data is copied. For unsharded states of >= 22 qubits the plan is
+ * autotuned: when per-term diagonal ops schedule into fewer passes, both
+ * schedules are built and one step of each is timed on the state's second
+ * buffer (the state itself is untouched); the faster one is kept
+ * (sd_plan_info::schedule). SDB_AUTOTUNE=0 disables it. */
 sd_status sd_plan_create(sd_state* s, const sd_group_desc* groups, size_t n_groups,
                          const sd_plan_options* opts, sd_plan** out);
 void sd_plan_destroy(sd_plan* p);
@@ -277,6 +281,9 @@ typedef struct sd_plan_info {
     int tile_qubits;
     int n_kernels_per_step;     /* kernel launches per step */
     double bytes_per_step;      /* algorithmic HBM bytes per step, this shard */
+    int schedule;               /* 0: whole-group diagonal ops, 1: per-term diagonal ops */
+    double tune_ms_whole;       /* plan-time autotune: ms per step of each schedule (0: not timed) */
+    double tune_ms_split;
 } sd_plan_info;
 
 sd_status sd_plan_get_info(const sd_plan* p, sd_plan_info* out);

@@ -71,6 +71,9 @@ class PlanInfo(C.Structure):
         ("tile_qubits", C.c_int),
         ("n_kernels_per_step", C.c_int),
         ("bytes_per_step", dbl),
+        ("schedule", C.c_int),
+        ("tune_ms_whole", dbl),
+        ("tune_ms_split", dbl),
     ]
 
 

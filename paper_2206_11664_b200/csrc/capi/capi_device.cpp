@@ -64,6 +64,12 @@ struct sd_plan {
     size_t ev_used = 0;
     int n_ref_sweeps = 0;
     std::vector<int> layout;  // unsharded: physical layout the steps run in (empty: identity)
+    // Schedule family: -1 the cost model / SDB_SPLIT_DIAG decide, 0 whole-group
+    // diagonal ops, 1 per-term diagonal ops (with knobs.max_hdepth). Set by the
+    // plan-time autotuner (sd_plan_create), which times the candidates.
+    int split = -1;
+    sdb::PlannerKnobs knobs;
+    double tune_ms[2] = {0.0, 0.0};  // measured ms/step of the candidates (0: not timed)
 };
 
 namespace {
@@ -97,7 +103,8 @@ int split_diag_mode() {
 // passes (an exchange counts as two passes of traffic) from the identity
 // layout; resynthesis wins on CNOT-heavy groups (config 5) and can lose a
 // pass or two where the given CNOT order commutes better (config 3).
-std::vector<sdb::Op> best_step_ops(const std::vector<sdb::GroupSpec>& gs, int n, int order, int k, int n_local) {
+std::vector<sdb::Op> best_step_ops(const std::vector<sdb::GroupSpec>& gs, int n, int order, int k, int n_local,
+                                   int split_force = -1) {
     std::vector<int> ident(n);
     std::iota(ident.begin(), ident.end(), 0);
     const bool sharded = n_local < n;
@@ -119,7 +126,7 @@ std::vector<sdb::Op> best_step_ops(const std::vector<sdb::GroupSpec>& gs, int n,
         return a.cost < b.cost;
     };
     const int cap = resynth_cap(k);
-    const int split_env = split_diag_mode();
+    const int split_env = split_force >= 0 ? split_force : split_diag_mode();
     std::vector<sdb::Op> best;
     Score best_score{0, 0.0};
     for (int split = 0; split < 2; ++split) {
@@ -351,6 +358,7 @@ void upload_step(sd_plan& p, StepExec& E, const sdb::StepPlan& combined) {
 // step's last pass out of place through the relabelling (no extra pass).
 StepExec& step_for(sd_plan& p, const std::vector<int>& layout, const std::vector<int>* end = nullptr) {
     sdb::StateImpl& s = p.state->impl;
+    const sdb::KnobScope knobs(&p.knobs);
     const bool relabel = end && s.world == 1 && *end != layout;
     std::vector<int> key = layout;
     if (relabel) key.insert(key.end(), end->begin(), end->end());
@@ -447,6 +455,10 @@ void choose_layout(sd_plan& p) {
     uint64_t rng = 0x243f6a8885a308d3ull;
     // deterministic budget by plan size (~1 s of planning for config 4's 13 passes)
     const int trials = std::clamp(5200 / std::max(1, static_cast<int>(base)), 0, 400);
+    static const bool fix_line = [] {
+        const char* e = std::getenv("SDB_LAYOUT_FIX_LINE");
+        return !e || std::atoi(e) != 0;
+    }();
     for (int trial = 0; trial < trials; ++trial) {
         std::vector<int> cand = best_l.empty() ? ident : best_l;
         // a few random transpositions away from the best layout so far
@@ -455,7 +467,11 @@ void choose_layout(sd_plan& p) {
             rng ^= rng << 13;
             rng ^= rng >> 7;
             rng ^= rng << 17;
-            const int a = static_cast<int>(rng % n), b = static_cast<int>((rng >> 20) % n);
+            // the always-local line bits 0..fb-1 keep their qubits, so the
+            // relabelling stores entering / leaving the layout move whole
+            // 128-byte lines (SDB_LAYOUT_FIX_LINE=0: search them too)
+            const int fb = fix_line ? sdb::fixed_bits_for(p.k) : 0;
+            const int a = fb + static_cast<int>(rng % (n - fb)), b = fb + static_cast<int>((rng >> 20) % (n - fb));
             std::swap(cand[a], cand[b]);
         }
         const double c = layout_cost(p, cand);
@@ -475,11 +491,94 @@ void plan_build(sd_plan& p) {
     if (!p.opts.fuse) return;
     int k = p.opts.tile_qubits > 0 ? p.opts.tile_qubits : 12;
     p.k = std::min({k, sdb::max_tile_qubits(), s.n_local});
-    p.ops = best_step_ops(p.groups, s.n, order, p.k, s.n_local);
+    const sdb::KnobScope knobs(&p.knobs);
+    p.ops = best_step_ops(p.groups, s.n, order, p.k, s.n_local, p.split);
     choose_layout(p);
     std::vector<int> ident(s.n);
     std::iota(ident.begin(), ident.end(), 0);
     p.first = &step_for(p, p.layout.empty() ? ident : p.layout);
+}
+
+// ---- plan-time autotuning of the schedule family (unsharded states)
+//
+// Whole-group diagonal ops (the default schedule) and per-term diagonal ops
+// with at most two Hadamard levels per pass trade pass count against
+// per-pass compute: config 4 runs 13 light passes or 10 heavier ones, and which
+// is faster depends on how compute-bound the heavier passes are (config 4:
+// 89.7 vs 82.4 ms; config 3: 469 vs 703 ms; config 2: 1.14 vs 2.0 ms). When
+// the per-term schedule needs fewer passes, both plans are built and one
+// steady-state step of each is timed on the exchange buffer as scratch (the
+// state is untouched); the faster plan is kept. SDB_AUTOTUNE=0 disables it,
+// and an explicit SDB_SPLIT_DIAG / SDB_MAX_HDEPTH experiment bypasses it.
+bool autotune_wanted(const sd_plan& p) {
+    const sdb::StateImpl& s = p.state->impl;
+    if (const char* e = std::getenv("SDB_AUTOTUNE"); e && std::atoi(e) == 0) return false;
+    if (std::getenv("SDB_SPLIT_DIAG") || std::getenv("SDB_MAX_HDEPTH")) return false;
+    return s.world == 1 && s.n_local >= 22 && p.opts.fuse && p.opts.use_graph <= 0 && p.opts.order >= 1;
+}
+
+bool ensure_scratch(sdb::StateImpl& s) {
+    if (s.xbuf) return true;
+    size_t free_b = 0, total_b = 0;
+    SDB_CUDA(cudaSetDevice(s.device));
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    if (free_b < 16 * s.amps_count() + (size_t(4) << 30)) return false;
+    if (cudaMalloc(reinterpret_cast<void**>(&s.xbuf), 16 * s.amps_count()) != cudaSuccess) {
+        cudaGetLastError();
+        s.xbuf = nullptr;
+        return false;
+    }
+    s.xbuf_amps = s.amps_count();
+    return true;
+}
+
+void run_step_fused(sd_plan& p, double dt, const std::vector<int>* end);
+
+// ms per steady-state step of plan P, run on the exchange buffer (zeroed
+// scratch); the state's buffer, layout and counters are restored
+double time_steady_step(sd_plan& P) {
+    sdb::StateImpl& s = P.state->impl;
+    std::vector<int> L(s.n);
+    std::iota(L.begin(), L.end(), 0);
+    if (!P.layout.empty()) L = P.layout;
+    const std::vector<int> saved_layout = s.phys_of;
+    const sd_kernel_stats saved_stats = s.stats;
+    const double dt = 0.01;
+    SDB_CUDA(cudaSetDevice(s.device));
+    SDB_CUDA(cudaMemsetAsync(s.xbuf, 0, 16 * s.amps_count(), s.stream));
+    std::swap(s.amps, s.xbuf);
+    cudaEvent_t a = nullptr, b = nullptr;
+    double ms = 0.0;
+    try {
+        s.phys_of = L;
+        run_step_fused(P, dt, &L);  // warm-up: builds and uploads the steady-state step
+        SDB_CUDA(cudaEventCreate(&a));
+        SDB_CUDA(cudaEventCreate(&b));
+        SDB_CUDA(cudaEventRecord(a, s.stream));
+        constexpr int kSteps = 2;
+        for (int i = 0; i < kSteps; ++i) run_step_fused(P, dt, &L);
+        SDB_CUDA(cudaEventRecord(b, s.stream));
+        SDB_CUDA(cudaEventSynchronize(b));
+        float f = 0.0f;
+        SDB_CUDA(cudaEventElapsedTime(&f, a, b));
+        ms = f / kSteps;
+    } catch (...) {
+        std::swap(s.amps, s.xbuf);
+        s.phys_of = saved_layout;
+        s.stats = saved_stats;
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+        throw;
+    }
+    std::swap(s.amps, s.xbuf);
+    s.phys_of = saved_layout;
+    s.stats = saved_stats;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return ms;
 }
 
 void record_start(sd_plan& p, int cls) {
@@ -1121,7 +1220,28 @@ sd_status sd_plan_create(sd_state* h, const sd_group_desc* groups, size_t n_grou
             p->groups.push_back(std::move(g));
         }
         if (!p->opts.fuse) require_unsharded(s);
-        plan_build(*p);
+        if (autotune_wanted(*p)) {
+            // candidate B: per-term diagonal ops, <= 2 Hadamard levels per pass
+            auto q = std::make_unique<sd_plan>();
+            q->state = h;
+            q->opts = p->opts;
+            q->groups = p->groups;
+            q->split = 1;
+            q->knobs.max_hdepth = 2;
+            p->split = 0;
+            plan_build(*p);
+            plan_build(*q);
+            const bool fewer = q->first && p->first && q->first->ss.n_passes < p->first->ss.n_passes;
+            if (fewer && ensure_scratch(s)) {
+                const double ta = time_steady_step(*p), tb = time_steady_step(*q);
+                p->tune_ms[0] = q->tune_ms[0] = ta;
+                p->tune_ms[1] = q->tune_ms[1] = tb;
+                if (tb < ta) std::swap(p, q);
+            }
+            sd_plan_destroy(q.release());
+        } else {
+            plan_build(*p);
+        }
         *out = p.release();
     });
 }
@@ -1159,6 +1279,9 @@ sd_status sd_plan_get_info(const sd_plan* p, sd_plan_info* o) {
             o->tile_qubits = p->k;
             o->n_kernels_per_step = o->n_passes_per_step;
             o->bytes_per_step = 2.0 * 16.0 * double(s.amps_count()) * o->n_passes_per_step;
+            o->schedule = p->split == 1 ? 1 : 0;
+            o->tune_ms_whole = p->tune_ms[0];
+            o->tune_ms_split = p->tune_ms[1];
         } else {
             o->n_passes_per_step = p->n_ref_sweeps;
             o->n_kernels_per_step = 0;

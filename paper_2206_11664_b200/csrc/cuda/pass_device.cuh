@@ -531,8 +531,11 @@ struct PassCtx {
         // transformed: HBM keeps streaming through the compute phase
         // without holding registers or shared memory.
 #ifndef SDB_NO_PREFETCH
-        if (t + stride < t_last) {
-            const double2* gn = psi + (tile_base(t + stride) + o0);
+#ifndef SDB_PREFETCH_DIST
+#define SDB_PREFETCH_DIST 1
+#endif
+        if (t + SDB_PREFETCH_DIST * stride < t_last) {
+            const double2* gn = psi + (tile_base(t + SDB_PREFETCH_DIST * stride) + o0);
 #pragma unroll
             for (int s = 0; s < NR; ++s) prefetch_l2(gn + o[s]);
         }

@@ -423,8 +423,11 @@ namespace {
 
 constexpr size_t kMaxDiagPerPass = 16384;
 
-// SDB_MAX_HDEPTH: WHT levels per pass (0 = unlimited)
+thread_local const PlannerKnobs* g_knobs = nullptr;
+
+// WHT levels per pass (0 = unlimited): the plan's knob, else SDB_MAX_HDEPTH
 int max_hadamard_depth() {
+    if (g_knobs && g_knobs->max_hdepth >= 0) return g_knobs->max_hdepth;
     const char* e = std::getenv("SDB_MAX_HDEPTH");
     return e ? std::atoi(e) : 0;
 }
@@ -1101,5 +1104,8 @@ std::string describe_json(const StepPlan& p) {
     os << "]}";
     return os.str();
 }
+
+KnobScope::KnobScope(const PlannerKnobs* k) : prev_(g_knobs) { g_knobs = k; }
+KnobScope::~KnobScope() { g_knobs = prev_; }
 
 }  // namespace sdb

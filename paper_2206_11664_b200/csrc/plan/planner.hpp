@@ -18,6 +18,22 @@ constexpr int kMaxOpsPerPass = 96;
 // line); tiles of <= 3 qubits keep at least one free coordinate.
 int fixed_bits_for(int k);
 
+// Per-plan planner settings (override the SDB_* environment knobs) for the
+// planning calls made while a KnobScope is alive on this thread.
+struct PlannerKnobs {
+    int max_hdepth = -1;  // WHT levels per pass, -1: SDB_MAX_HDEPTH / unlimited
+};
+class KnobScope {
+  public:
+    explicit KnobScope(const PlannerKnobs* k);
+    ~KnobScope();
+    KnobScope(const KnobScope&) = delete;
+    KnobScope& operator=(const KnobScope&) = delete;
+
+  private:
+    const PlannerKnobs* prev_;
+};
+
 // One group as the planner sees it (a flattened DiagonalGroup).
 struct GroupSpec {
     std::vector<int> h_pre, s_layer, h_post;

@@ -485,6 +485,8 @@ def run_ours(args, rank, world, local_rank):
         "norm_error": norm_err,
         "e2e": e2e,
     }
+    if rank == 0 and world == 1 and not args.no_other_configs and cfg == 4:
+        line["other_configs"] = other_configs(dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"], line["parity"] = cpu_baseline_and_parity(cfg, n, psi, plan)
@@ -497,6 +499,47 @@ def run_ours(args, rank, world, local_rank):
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
+
+
+def other_configs(dev):
+    """Configs 2 and 3 at their BASELINE sizes on the same GPU (device-timed
+    steps after warm-up; the main line stays config 4). Reported, never fatal."""
+    import torch
+
+    import paper_2206_11664_b200 as S
+    from paper_2206_11664_b200 import models as M
+
+    out = {}
+    for cfg, steps in ((2, 200), (3, 3)):
+        try:
+            n = M.CONFIGS[cfg]["n"]
+            _, _, groups = build_workload(cfg, n)
+            psi = S.StateVector(n, device=dev)
+            init_state(psi, cfg, n, 0)
+            plan = S.TrotterPlan(psi, groups, order=M.CONFIGS[cfg]["order"])
+            dt = M.CONFIGS[cfg]["dt"]
+            plan.evolve(dt, 2)
+            stream = torch.cuda.ExternalStream(psi.stream(), device=dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            e0.record(stream)
+            plan.evolve(dt, steps, wait=False)
+            e1.record(stream)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1) / steps
+            info = plan.info()
+            peak, _ = load_peaks()
+            gbs = info["bytes_per_step"] / (ms / 1e3) / 1e9
+            out[f"config{cfg}"] = {
+                "workload": CONFIG_DESC[cfg], "n_qubits": n, "steps": steps, "ms_per_step": ms,
+                "steps_per_s": 1000.0 / ms, "passes_per_step": info["n_passes_per_step"],
+                "ref_sweeps_per_step": info["n_ref_sweeps_per_step"],
+                "schedule": "per-term diagonal ops" if info["schedule"] == 1 else "whole-group diagonal ops",
+                "step_hbm_gbs": gbs, "step_frac": gbs / peak, "norm_error": abs(psi.norm() - 1.0)}
+            del plan, psi
+        except Exception as ex:  # reported, never fatal
+            out[f"config{cfg}"] = {"error": repr(ex)}
+    return out
 
 
 def run_baseline_method(args, rank, world, local_rank):
@@ -578,6 +621,8 @@ def main():
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the configs 2 and 3 side measurements of the default (config 4) run")
     ap.add_argument("--ref-budget-total", type=float, default=150.0,
                     help="--impl reference: stop timing further full steps once this many seconds are spent")
     ap.add_argument("--launch-check", action="store_true",

@@ -52,6 +52,45 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
 
+// ---- TMA staging of tile loads (specialised kernels, SDB_TMA): one thread
+// issues cp.async.bulk.tensor boxes of the tile into the transpose buffer
+// once the previous tile's last transpose has read it, completing on an
+// mbarrier; the LOAD op then reads its register config from shared memory.
+// The tensor map (a __grid_constant__ kernel parameter) views the shard as a
+// rank-5 tensor whose dimensions start at the pass's runs of consecutive local
+// physical bits (host side: jit.cpp tma_spec).
+struct alignas(64) TmapParam {
+    unsigned long long w[16];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t mbar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mbar));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint32_t mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(mbar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const void* tmap, int c0, int c1, int c2, int c3, int c4,
+                                            uint32_t mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(dst),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(mbar)
+        : "memory");
+}
+
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 
@@ -352,6 +391,9 @@ struct PassCtx {
     int tpar;  // tile parity (double-buffered phase tables)
     uint64_t last_pat;  // sign pattern the current phase tables were built for
     RegCfg rc;
+    uint32_t mbar = 0;       // TMA: mbarrier of the tile staged in buf
+    const void* tmap = nullptr;  // TMA: the tensor map (address of the __grid_constant__ parameter)
+    uint32_t tma_phase = 0;  // TMA: parity of the next completion to wait for
 
     __device__ __forceinline__ PassCtx(const PassDev& P_, const PlanDev& plan_, const double2* psi_, double2* out_,
                                        double2* const* xdst_, double neg_dt_, uint64_t rank_bits_, uint64_t n_tiles_,
@@ -525,8 +567,14 @@ struct PassCtx {
         reg_offsets(o, rc.coff);
         const uint64_t o0 = off_of(rc.tb);
         const double2* gt = g + o0;
+#ifdef SDB_EXPERIMENT_NOLOAD
+        // timing experiment only (wrong results): tile data from shared memory
+#pragma unroll
+        for (int s = 0; s < NR; ++s) v[s] = buf[(static_cast<uint32_t>(o0 + o[s]) ^ static_cast<uint32_t>(t)) & (N - 1)];
+#else
 #pragma unroll
         for (int s = 0; s < NR; ++s) v[s] = SDB_TILE_LOAD(gt + o[s]);
+#endif
         // Pull this CTA's next tile into L2 while the current one is
         // transformed: HBM keeps streaming through the compute phase
         // without holding registers or shared memory.
@@ -552,6 +600,43 @@ struct PassCtx {
                 build_tables<NT>(tabc(), plan, plan.points[P.table_point], full, neg_dt, P.table_scale, false);
             }
         }
+    }
+
+    // LOAD from the TMA-staged tile: amplitude of local index l sits at slot
+    // tsl(l) (the box layout, GF(2)-linear in l); tsl0 is this thread's
+    // register-0 slot, tso[j] the slot offset of register coordinate j.
+    __device__ __forceinline__ void load_tma(const RegCfg& r, double2 (&v)[NR], uint32_t tsl0,
+                                             const uint32_t (&tso)[4]) {
+        rc = r;
+        // per-tile phase tables are built while the tile's boxes are in flight
+        if (has_table) {
+            const uint64_t pat = P.pat_shift >= 64 ? t : (t >> P.pat_shift);
+            if (pat != last_pat) {
+                if (last_pat != ~0ull) __syncthreads();
+                last_pat = pat;
+                build_tables<NT>(tabc(), plan, plan.points[P.table_point], full, neg_dt, P.table_scale, false);
+            }
+        }
+#ifndef SDB_NO_PREFETCH
+        if (t + SDB_PREFETCH_DIST * stride < t_last) {
+            // next tile into L2 (its TMA boxes are issued from there)
+            uint64_t o[NR];
+            reg_offsets(o, rc.coff);
+            const double2* gn = psi + (tile_base(t + SDB_PREFETCH_DIST * stride) + off_of(rc.tb));
+#pragma unroll
+            for (int s = 0; s < NR; ++s) prefetch_l2(gn + o[s]);
+        }
+#endif
+        mbar_wait(mbar, tma_phase);
+        tma_phase ^= 1u;
+        uint32_t a[NR];
+        a[0] = tsl0;
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+#pragma unroll
+            for (int s = 0; s < (1 << j); ++s) a[s + (1 << j)] = a[s] | tso[j];
+#pragma unroll
+        for (int s = 0; s < NR; ++s) v[s] = buf[a[s]];
     }
 
     // shared-memory transpose into config r; op.perm >= 0 applies a pending
@@ -905,6 +990,30 @@ struct PassCtx {
     Ctx ctx(plan.passes[pass_index], plan, psi, out, xdst, neg_dt, rank_bits, n_tiles, smem_raw, sdb_off_lo, \
             sdb_off_hi, sdb_tbase, sdb_pl, sdb_ph);                                                        \
     ctx.setup();                                                                                           \
+    for (uint64_t t = ctx.t_first; t < ctx.t_last; t += ctx.stride) {                                      \
+        ctx.begin_tile(t);                                                                                 \
+        double2 v[Ctx::NR];                                                                                \
+        PROG(ctx, v);                                                                                      \
+    }
+
+// TMA variant: the first tile's boxes are issued after setup; each program
+// issues the next tile's boxes itself once its last transpose is done
+// (Prog::tma_next), and its LOAD waits on the mbarrier.
+#define SDB_PASS_KERNEL_BODY_TMA(K, RB, PROG)                                                              \
+    using Ctx = ::sdb::dev::PassCtx<K, RB>;                                                                \
+    extern __shared__ __align__(128) unsigned char smem_raw[];                                             \
+    __shared__ uint64_t sdb_off_lo[1 << Ctx::LO];                                                          \
+    __shared__ uint64_t sdb_off_hi[1 << Ctx::HI];                                                          \
+    __shared__ uint64_t sdb_tbase[::sdb::dev::kTbaseChunks * 128];                                         \
+    __shared__ uint32_t sdb_pl[3 * 64], sdb_ph[3 * 64];                                                    \
+    __shared__ __align__(8) uint64_t sdb_mbar;                                                             \
+    Ctx ctx(plan.passes[pass_index], plan, psi, out, xdst, neg_dt, rank_bits, n_tiles, smem_raw, sdb_off_lo, \
+            sdb_off_hi, sdb_tbase, sdb_pl, sdb_ph);                                                        \
+    ctx.mbar = ::sdb::dev::smem_u32(&sdb_mbar);                                                            \
+    ctx.tmap = &tmap;                                                                                      \
+    if (threadIdx.x == 0) ::sdb::dev::mbar_init(ctx.mbar);                                                 \
+    ctx.setup();                                                                                           \
+    if (threadIdx.x == 0 && ctx.t_first < ctx.t_last) PROG.tma_issue(ctx, ctx.tile_base(ctx.t_first));      \
     for (uint64_t t = ctx.t_first; t < ctx.t_last; t += ctx.stride) {                                      \
         ctx.begin_tile(t);                                                                                 \
         double2 v[Ctx::NR];                                                                                \

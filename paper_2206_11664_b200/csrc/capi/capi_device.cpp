@@ -287,6 +287,7 @@ void upload_step(sd_plan& p, StepExec& E, const sdb::StepPlan& combined) {
     int rbits = 4;
     if (const char* e = std::getenv("SDB_RBITS"); e && jit) rbits = std::atoi(e) == 3 ? 3 : 4;
     sdb::HostPlanArrays A = sdb::lower_plan(combined, s.n_local, kTableThreshold, rbits);
+    A.tma = p.knobs.tma;
     sdb::verify_lowering(A);  // register-config bookkeeping of lane swaps (host check, cheap)
     E.pass_class = A.pass_class;
     E.program = sdb::describe_program(A);
@@ -1228,6 +1229,7 @@ sd_status sd_plan_create(sd_state* h, const sd_group_desc* groups, size_t n_grou
             q->groups = p->groups;
             q->split = 1;
             q->knobs.max_hdepth = 2;
+            q->knobs.tma = 1;  // TMA-staged loads pay off on the heavier per-term passes only
             p->split = 0;
             plan_build(*p);
             plan_build(*q);

@@ -344,6 +344,7 @@ struct Cfg {
 };
 
 constexpr int kTbaseChunks = 4;  // outer bits covered by the tile-base tables: 4 x 7
+constexpr int kPatTerms = 6;     // POINT mode 5: at most 2^6 sign patterns per tile
 
 
 // Register config of the current micro-program point: the thread's register-0
@@ -391,6 +392,7 @@ struct PassCtx {
     int tpar;  // tile parity (double-buffered phase tables)
     uint64_t last_pat;  // sign pattern the current phase tables were built for
     RegCfg rc;
+    double2* pat_tab = nullptr;  // POINT mode 5: [1 << kPatTerms] phase per sign pattern of the terms
     uint32_t mbar = 0;       // TMA: mbarrier of the tile staged in buf
     const void* tmap = nullptr;  // TMA: the tensor map (address of the __grid_constant__ parameter)
     uint32_t tma_phase = 0;  // TMA: parity of the next completion to wait for
@@ -677,6 +679,38 @@ struct PassCtx {
         smem_busy = true;
     }
 
+    // Transpose whose write side applies a pending CNOT map, with the map's
+    // images of the register coordinates as literals: the map is GF(2)-linear
+    // (PermDev lo/hi are XORs of its columns), so register s of the thread
+    // lands at slot m(tb) ^ XOR_{j in s} lm[j] -- two table reads per thread
+    // instead of two per amplitude.
+    __device__ __forceinline__ void cfg_lin(const MicroOpDev& op, const RegCfg& r, double2 (&v)[NR],
+                                            const uint32_t (&lm)[4]) {
+        if (smem_busy) __syncthreads();
+        const PermDev* pm = plan.perms + op.perm;
+        uint32_t sb = 0;
+        for (int j = 0; j < pm->n_ctrl; ++j)
+            if ((full >> pm->ctrl_phys[j]) & 1ull) sb ^= pm->flip[j];
+        uint32_t m[NR];
+        m[0] = static_cast<uint32_t>(__ldg(&pm->lo[rc.tb & 63u])) ^ static_cast<uint32_t>(__ldg(&pm->hi[rc.tb >> 6])) ^
+               sb;
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+#pragma unroll
+            for (int s = 0; s < (1 << j); ++s) m[s + (1 << j)] = m[s] ^ lm[j];
+#pragma unroll
+        for (int s = 0; s < NR; ++s) buf[m[s]] = v[s];
+        __syncthreads();
+        rc = r;
+        {
+            uint32_t a[NR];
+            slots(a);
+#pragma unroll
+            for (int s = 0; s < NR; ++s) v[s] = buf[a[s]];
+        }
+        smem_busy = true;
+    }
+
     // register slot J <-> lane bit B by warp shuffles, then config r
     template <int J, int B>
     __device__ __forceinline__ void swap(const RegCfg& r, double2 (&v)[NR]) {
@@ -697,9 +731,13 @@ struct PassCtx {
     //   0 quarter turns only, 1 <= 8 terms summed directly, 2 more terms
     //   summed directly (no table left in the pass), 3 full angle table,
     //   4 factor tables (NFAC of them).
+    //   5 <= kPatTerms terms: per-tile table of the 2^m sign patterns (the
+    //     same angle sums as mode 1, one sincos per pattern instead of one per
+    //     amplitude).
     static __device__ __forceinline__ int point_mode(const PassDev& P, const PointDev& pt, int arg) {
         if (pt.n_terms == 0) return 0;
         if (arg == P.table_point) return pt.n_fac > 0 ? 4 : 3;
+        if (pt.n_terms <= kPatTerms) return 5;
         return pt.n_terms <= 8 ? 1 : 2;
     }
 
@@ -803,9 +841,9 @@ struct PassCtx {
             }
         }
         // ---- direct-mode terms (few) with the tile's outer sign folded in
-        double dc[MODE == 1 ? 8 : 1];
-        uint32_t dz[MODE == 1 ? 8 : 1];
-        if constexpr (MODE == 1) {
+        double dc[(MODE == 1 || MODE == 5) ? 8 : 1];
+        uint32_t dz[(MODE == 1 || MODE == 5) ? 8 : 1];
+        if constexpr (MODE == 1 || MODE == 5) {
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 dc[q] = 0.0;
@@ -817,6 +855,32 @@ struct PassCtx {
                     dz[q] = __ldg(plan.term_lmask + pt.term_off + q);
                 }
             }
+        }
+        // mode 5: the tile's phase per sign pattern of its terms, summed in
+        // term order exactly as mode 1 does per amplitude
+        const double2* ptab = nullptr;
+        if constexpr (MODE == 5) {
+            // barriers on both sides: earlier readers (this tile's previous mode-5
+            // POINT, the previous tile's) are done before the table is rewritten
+            double2* tabp = pat_tab;
+            const int m = pt.n_terms;
+            __syncthreads();
+            for (int e = tid; e < (1 << m); e += NT) {
+                double ang = 0.0;
+#pragma unroll
+                for (int q = 0; q < kPatTerms; ++q)
+                    if (q < m) ang += __longlong_as_double(__double_as_longlong(dc[q]) ^
+                                                           (static_cast<long long>((e >> q) & 1) << 63));
+                double sn, cs;
+                phase_sincos(neg_dt * ang, &sn, &cs);
+                if (scale_here) {
+                    sn *= scale;
+                    cs *= scale;
+                }
+                tabp[e] = make_double2(cs, sn);
+            }
+            __syncthreads();
+            ptab = tabp;
         }
         // q of every register combination, one add each
         unsigned qs[NR];
@@ -845,6 +909,16 @@ struct PassCtx {
                     const double2 t = E[f][x];
                     e = f == 0 ? t : make_double2(e.x * t.x - e.y * t.y, e.x * t.y + e.y * t.x);
                 }
+                a = make_double2(a.x * e.x - a.y * e.y, a.x * e.y + a.y * e.x);
+            } else if constexpr (MODE == 5) {
+                uint32_t l = rc.tb;
+#pragma unroll
+                for (int j = 0; j < R; ++j)
+                    if ((s2 >> j) & 1) l |= cb[j];
+                uint32_t idx = 0;
+#pragma unroll
+                for (int q = 0; q < kPatTerms; ++q) idx |= static_cast<uint32_t>(__popc(l & dz[q]) & 1) << q;
+                const double2 e = ptab[idx];
                 a = make_double2(a.x * e.x - a.y * e.y, a.x * e.y + a.y * e.x);
             } else if constexpr (MODE != 0) {
                 double ang = 0.0;
@@ -891,6 +965,7 @@ struct PassCtx {
         switch (point_mode(P, pt, op.arg)) {
             case 0: point<0, 0>(op, pc, v); break;
             case 1: point<1, 0>(op, pc, v); break;
+            case 5: point<5, 0>(op, pc, v); break;
             case 2: point<2, 0>(op, pc, v); break;
             case 3: point<3, 0>(op, pc, v); break;
             default:
@@ -905,6 +980,9 @@ struct PassCtx {
     // (F >= 0), so only the path the op takes is compiled; the interpreter
     // decodes them from the staged op (F < 0).
     static constexpr int kStPerm = 1, kStSigma = 2, kStScale = 4, kStSync = 8, kStXchg = 16;
+    // with kStPerm: soff holds the physical offsets of the map's images of the
+    // register coordinates (host-computed; the map and the offsets are linear)
+    static constexpr int kStPermLin = 32;
     __device__ __forceinline__ int store_flags(const MicroOpDev& op) const {
         return (op.perm >= 0 ? kStPerm : 0) | (store_perm ? kStSigma : 0) | ((op.mask & 2u) ? kStScale : 0) |
                ((op.mask & 4u) ? kStSync : 0) | (P.x_bits > 0 ? kStXchg : 0);
@@ -929,6 +1007,21 @@ struct PassCtx {
             go = out + sb;
             go += st_lo[rc.tb & ((1u << LO) - 1u)] | st_hi[rc.tb >> LO];
             reg_offsets(o, soff);
+        } else if ((f & kStPerm) && (f & kStPermLin)) {
+            // pending CNOT map by the addressing, linear form: physical offset
+            // of register s = off(P(tb)) ^ XOR_{j in s} soff[j]
+            go = out + base;
+            const PermDev* pm = plan.perms + op.perm;
+            uint32_t sb = 0;
+            for (int j = 0; j < pm->n_ctrl; ++j)
+                if ((full >> pm->ctrl_phys[j]) & 1ull) sb ^= pm->flip[j];
+            const uint32_t m0 = swz(static_cast<uint32_t>(__ldg(&pm->lo[rc.tb & 63u])) ^
+                                    static_cast<uint32_t>(__ldg(&pm->hi[rc.tb >> 6])) ^ sb);
+            o[0] = off_of(m0);
+#pragma unroll
+            for (int j = 0; j < R; ++j)
+#pragma unroll
+                for (int s = 0; s < (1 << j); ++s) o[s + (1 << j)] = o[s] ^ soff[j];
         } else if (f & kStPerm) {
             // pending CNOT map applied by the addressing: register s (local
             // index l) goes to P(l) = swz(lo[l & 63] ^ hi[l >> 6] ^ b(h))
@@ -989,6 +1082,8 @@ struct PassCtx {
     __shared__ uint32_t sdb_pl[3 * 64], sdb_ph[3 * 64];                                                    \
     Ctx ctx(plan.passes[pass_index], plan, psi, out, xdst, neg_dt, rank_bits, n_tiles, smem_raw, sdb_off_lo, \
             sdb_off_hi, sdb_tbase, sdb_pl, sdb_ph);                                                        \
+    __shared__ double2 sdb_pat[1 << ::sdb::dev::kPatTerms];                                                 \
+    ctx.pat_tab = sdb_pat;                                                                                 \
     ctx.setup();                                                                                           \
     for (uint64_t t = ctx.t_first; t < ctx.t_last; t += ctx.stride) {                                      \
         ctx.begin_tile(t);                                                                                 \
@@ -1012,6 +1107,8 @@ struct PassCtx {
     ctx.mbar = ::sdb::dev::smem_u32(&sdb_mbar);                                                            \
     ctx.tmap = &tmap;                                                                                      \
     if (threadIdx.x == 0) ::sdb::dev::mbar_init(ctx.mbar);                                                 \
+    __shared__ double2 sdb_pat[1 << ::sdb::dev::kPatTerms];                                                 \
+    ctx.pat_tab = sdb_pat;                                                                                 \
     ctx.setup();                                                                                           \
     if (threadIdx.x == 0 && ctx.t_first < ctx.t_last) PROG.tma_issue(ctx, ctx.tile_base(ctx.t_first));      \
     for (uint64_t t = ctx.t_first; t < ctx.t_last; t += ctx.stride) {                                      \

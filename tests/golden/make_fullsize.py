@@ -10,6 +10,8 @@ the listed step counts:
     config 2  n=25 TFIM 5x5, |+>^25, S2 dt=0.02      after 20 and 500 steps
     config 3  n=28 random 4-local M=2000, random_state(28, 2), dt=0.005   1 step
     config 4  n=30 XXZ chain, Neel, dt=0.01          after 1 and 3 steps
+    config 5  its generator at n=26 (the reference caps n <= 30; n=33 has no CPU
+              oracle), |1^16 0^10>, dt=0.01              after 1 step
 
 Run where /root/reference exists (needs ~34 GiB host RAM for n=30):
     make -C oracle && python tests/golden/make_fullsize.py [case ...]
@@ -35,14 +37,15 @@ CASES = {
     "cfg4_n30": (4, [1, 3]),
     "cfg3_n28": (3, [1]),
     "cfg2_n25": (2, [20, 500]),
+    "cfg5_n26": (5, [1], 26),
 }
 
 
 def run_case(name: str, ref: O.Ref) -> None:
-    cfg, checkpoints = CASES[name]
-    n = M.CONFIGS[cfg]["n"]
+    cfg, checkpoints = CASES[name][:2]
+    n = CASES[name][2] if len(CASES[name]) > 2 else M.CONFIGS[cfg]["n"]
     dt, order = M.CONFIGS[cfg]["dt"], M.CONFIGS[cfg]["order"]
-    h, nn, _ = ref.partition_text(M.config_text(cfg), synthesize=True)
+    h, nn, _ = ref.partition_text(M.config_text(cfg, None if n == M.CONFIGS[cfg]["n"] else n), synthesize=True)
     assert nn == n
     init = M.CONFIGS[cfg]["init"]
     if init[0] == "basis":

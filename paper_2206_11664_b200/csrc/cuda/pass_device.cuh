@@ -389,7 +389,6 @@ struct PassCtx {
     uint64_t t, base, full;
     const double2* g;
     bool smem_busy;
-    int tpar;  // tile parity (double-buffered phase tables)
     uint64_t last_pat;  // sign pattern the current phase tables were built for
     RegCfg rc;
     double2* pat_tab = nullptr;  // POINT mode 5: [1 << kPatTerms] phase per sign pattern of the terms
@@ -418,7 +417,6 @@ struct PassCtx {
             stride = gridDim.x;
         }
         has_table = P.table_point >= 0;
-        tpar = 1;
         last_pat = ~0ull;
         store_perm = P.store_perm != 0;
         scale = P.scale;  // exact power of two
@@ -521,9 +519,8 @@ struct PassCtx {
         full = rank_bits | base;
         g = psi + base;
         smem_busy = true;  // smem may still be read by other threads (sync before writing)
-        tpar ^= 1;
     }
-    __device__ __forceinline__ double* tabc() const { return tab + ((P.tab_double && tpar) ? P.tab_half : 0); }
+    __device__ __forceinline__ double* tabc() const { return tab; }
 
     // register config from the staged program (interpreter)
     __device__ __forceinline__ RegCfg cfg_of(const MicroOpDev& op) const {
@@ -1110,7 +1107,7 @@ struct PassCtx {
     __shared__ double2 sdb_pat[1 << ::sdb::dev::kPatTerms];                                                 \
     ctx.pat_tab = sdb_pat;                                                                                 \
     ctx.setup();                                                                                           \
-    if (threadIdx.x == 0 && ctx.t_first < ctx.t_last) PROG.tma_issue(ctx, ctx.tile_base(ctx.t_first));      \
+    if (threadIdx.x < 32u && ctx.t_first < ctx.t_last) PROG.tma_issue(ctx, ctx.tile_base(ctx.t_first), threadIdx.x); \
     for (uint64_t t = ctx.t_first; t < ctx.t_last; t += ctx.stride) {                                      \
         ctx.begin_tile(t);                                                                                 \
         double2 v[Ctx::NR];                                                                                \

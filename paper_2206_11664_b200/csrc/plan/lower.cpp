@@ -695,7 +695,6 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
         // of the table terms (PM). Those bits go to the top of the tile index,
         // so a CTA walking t, t + grid, ... keeps the same table for long runs
         // of tiles and rebuilds it only when t >> pat_shift changes.
-        pd.tab_half = pd.tab_words;
         pd.pat_shift = 64;
         pd.tphase_off = -1;
         static const bool reorder = [] {

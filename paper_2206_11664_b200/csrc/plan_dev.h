@@ -151,9 +151,7 @@ struct PassDev {
     int rbits;        // R: register coordinates per config
     int qt_off;       // first QT word of this pass in PlanDev::qt_words
     int n_qt_words;   // QT words staged into shared memory
-    int tab_words;    // 8-byte words of the per-tile table region (even; 0 if none; both copies)
-    int tab_double;   // 1: two copies, tile parity selects (unused: see pat_shift)
-    int tab_half;     // words per copy when tab_double
+    int tab_words;    // 8-byte words of the per-tile table region (even; 0 if none)
     int pat_shift;    // tile-index bits >= pat_shift select the table's sign pattern (rebuild on change)
     int blocked;      // 1: each CTA walks a contiguous block of tiles (table reuse), 0: grid-strided
     int tphase_off;   // >= 0: per-tile phase of the table point's tile-constant terms at PlanDev::tile_phase + off

@@ -1229,7 +1229,6 @@ sd_status sd_plan_create(sd_state* h, const sd_group_desc* groups, size_t n_grou
             q->groups = p->groups;
             q->split = 1;
             q->knobs.max_hdepth = 2;
-            q->knobs.tma = 1;  // TMA-staged loads pay off on the heavier per-term passes only
             p->split = 0;
             plan_build(*p);
             plan_build(*q);

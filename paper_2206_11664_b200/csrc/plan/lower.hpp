@@ -25,8 +25,8 @@ struct HostPlanArrays {
     std::vector<double> term_coeffs;
     std::vector<int> pass_class;   // 0 = transform pass, 1 = diagonal-only pass
     std::vector<int> transposes;   // shared-memory transposes per pass (CFG with a write side)
-    // Specialised kernels stage tile loads through TMA (jit.cpp): -1 SDB_TMA
-    // decides (default off), 0 off, 1 on. Set per plan by the caller.
+    // Specialised kernels stage tile loads through TMA (jit.cpp): -1 default
+    // (on unless SDB_TMA=0), 0 off, 1 on. Set per plan by the caller.
     int tma = -1;
 };
 

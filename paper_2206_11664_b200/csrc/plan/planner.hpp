@@ -22,7 +22,7 @@ int fixed_bits_for(int k);
 // planning calls made while a KnobScope is alive on this thread.
 struct PlannerKnobs {
     int max_hdepth = -1;  // WHT levels per pass, -1: SDB_MAX_HDEPTH / unlimited
-    int tma = -1;         // specialised kernels stage tile loads through TMA (-1: SDB_TMA, default off)
+    int tma = -1;         // specialised kernels stage tile loads through TMA (-1: default on / SDB_TMA)
 };
 class KnobScope {
   public:

@@ -7,7 +7,8 @@ import subprocess
 import sys
 
 tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
-rep = f"gpurun_out/{tag}_full.ncu-rep"
+rep = sys.argv[2] if len(sys.argv) > 2 else f"gpurun_out/{tag}_full.ncu-rep"
+source = sys.argv[3] if len(sys.argv) > 3 else "ncu --set full, tools/profile_pass.py 4 30 1 (config 4, n=30)"
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h = rows[0]
@@ -26,7 +27,7 @@ def to_bytes(v, u):
 per = [to_bytes(l["dram__bytes_read.sum"], units["dram__bytes_read.sum"]) +
        to_bytes(l["dram__bytes_write.sum"], units["dram__bytes_write.sum"]) for l in launches]
 alg = 32.0 * 2 ** 30
-summary = {"source": f"ncu --set full, tools/profile_pass.py 4 30 1 (config 4, n=30), launches 0-{len(launches) - 1}",
+summary = {"source": f"{source}, launches 0-{len(launches) - 1} of the capture",
            "algorithmic_bytes_per_launch": alg, "dram_bytes_per_launch": sum(per) / len(per),
            "dram_over_algorithmic": sum(per) / len(per) / alg,
            "launches": [dict(l, dram_bytes=b) for l, b in zip(launches, per)], "units": units}

@@ -243,7 +243,7 @@ def run_reference_arm(args, rank, world):
     cfg, n = args.config, args.n
     K, W = max(1, args.steps), max(0, args.warmup)
     base = {"metric": METRIC, "unit": "Trotter steps/s", "n_gpus": world, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64 pairs)",
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "c128 (f64 pairs)",
             "data": "synthetic (seeded generator, BASELINE config)",
             "config": {"workload": f"config{cfg}: {CONFIG_DESC[cfg]}", "n_qubits": n, "dt": M.CONFIGS[cfg]["dt"],
                        "order": M.CONFIGS[cfg]["order"]},
@@ -588,8 +588,17 @@ def relaunch(n: int) -> int:
     with socket.socket() as so:
         so.bind(("127.0.0.1", 0))
         port = so.getsockname()[1]
+    # `--n` would prefix-match torchrun's own options: forward it as --qubits
+    fwd = []
+    for a in sys.argv[1:]:
+        if a == "--n":
+            fwd.append("--qubits")
+        elif a.startswith("--n="):
+            fwd.append("--qubits=" + a[4:])
+        else:
+            fwd.append(a)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + fwd
     return subprocess.call(cmd)
 
 
@@ -617,7 +626,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=4)
-    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--n", "--qubits", dest="n", type=int, default=None)
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

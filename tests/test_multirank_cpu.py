@@ -118,3 +118,20 @@ def test_multirank_gloo_schedule_matches_oracle(cfg, n, k, world):
     err, nerr, n_ex = q.get(timeout=10)
     assert err < 1e-11 and nerr < 1e-13
     assert n_ex >= 1  # the run really exercised remaps
+
+
+def test_bench_launcher_starts_one_process_per_gpu():
+    """`bench.py --gpus N` without WORLD_SIZE re-launches itself under
+    torch.distributed.run: every rank joins one gloo group and sees world == N."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--launch-check", "--n", "12"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+    d = json.loads(line)
+    assert d["launch_check"] and d["world"] == 2 and d["ranks"] == [0, 1]

@@ -1231,15 +1231,27 @@ sd_status sd_plan_create(sd_state* h, const sd_group_desc* groups, size_t n_grou
             q->knobs.max_hdepth = 2;
             p->split = 0;
             plan_build(*p);
-            plan_build(*q);
-            const bool fewer = q->first && p->first && q->first->ss.n_passes < p->first->ss.n_passes;
-            if (fewer && ensure_scratch(s)) {
-                const double ta = time_steady_step(*p), tb = time_steady_step(*q);
-                p->tune_ms[0] = q->tune_ms[0] = ta;
-                p->tune_ms[1] = q->tune_ms[1] = tb;
-                if (tb < ta) std::swap(p, q);
+            const bool had_scratch = s.xbuf != nullptr;
+            try {
+                plan_build(*q);
+                const bool fewer = q->first && p->first && q->first->ss.n_passes < p->first->ss.n_passes;
+                if (fewer && ensure_scratch(s)) {
+                    const double ta = time_steady_step(*p), tb = time_steady_step(*q);
+                    p->tune_ms[0] = q->tune_ms[0] = ta;
+                    p->tune_ms[1] = q->tune_ms[1] = tb;
+                    if (tb < ta) std::swap(p, q);
+                }
+            } catch (const sdb::OomError&) {
+                // no room for the second candidate: keep the whole-group plan
             }
             sd_plan_destroy(q.release());
+            // the scratch stays only if the kept plan's layout needs the second buffer
+            if (!had_scratch && s.xbuf && p->layout.empty()) {
+                SDB_CUDA(cudaSetDevice(s.device));
+                SDB_CUDA(cudaFree(s.xbuf));
+                s.xbuf = nullptr;
+                s.xbuf_amps = 0;
+            }
         } else {
             plan_build(*p);
         }

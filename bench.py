@@ -474,6 +474,10 @@ def run_ours(args, rank, world, local_rank):
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "avg_launch_ms": dom["ms"] / max(1, dom["launches"]),
                      "step_hbm_gbs": step_gbs, "step_frac": step_gbs / peak,
+                     # the reference's unfused schedule moves P_ref sweeps per step; the
+                     # same step at this rate corresponds to this many GB/s of its traffic
+                     "reference_schedule_equivalent_gbs": (info["n_ref_sweeps_per_step"] * bytes_per_launch /
+                                                           (ms_per_step / 1e3) / 1e9),
                      "share_of_step": tot_ms / max(1e-9, ms),
                      "timing": ("timed region replays CUDA graphs; kernel split from a separate profiled run"
                                 if graph_steps else "per-launch CUDA events inside the timed region")},

@@ -117,3 +117,32 @@ def test_relabelled_layout_is_transparent(sd, ref):
     sd.TrotterPlan(s2, g2, order=1, use_graph=False).evolve(dt, 1)
     assert np.max(np.abs(got - s2.amplitudes())) < 1e-12
     assert abs(np.linalg.norm(got) - 1) < 1e-12
+
+
+def test_autotune_keeps_state_and_reports_both_schedules(sd, port):
+    """Plan-time autotuning (sd_plan_create, unsharded >= 22 qubits) times both
+    schedule families on the scratch buffer: the state is untouched, both times
+    are reported and the kept schedule is the faster one."""
+    import os
+
+    from paper_2206_11664_b200 import models as M
+
+    if os.environ.get("SDB_AUTOTUNE") == "0":
+        pytest.skip("autotune disabled")
+    n = 22
+    text = M.config_text(4, n)
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
+    a0 = port.random_state(n, 5)
+    psi = sd.StateVector(n)
+    psi.upload(a0)
+    plan = sd.TrotterPlan(psi, groups, order=1)
+    info = plan.info()
+    assert np.array_equal(psi.amplitudes(), a0)
+    if info["tune_ms_whole"] > 0:
+        assert info["tune_ms_split"] > 0
+        faster = 1 if info["tune_ms_split"] < info["tune_ms_whole"] else 0
+        assert info["schedule"] == faster
+    plan.evolve(0.01, 2)
+    _, og = port.partition_and_diagonalize(text)
+    want = port.evolve_grouped(a0, n, og, 0.01, 2, 1)
+    assert np.max(np.abs(psi.amplitudes() - want)) < 1e-10

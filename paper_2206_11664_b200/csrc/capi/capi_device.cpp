@@ -296,6 +296,7 @@ void upload_step(sd_plan& p, StepExec& E, const sdb::StepPlan& combined) {
     for (size_t i = 0; i < A.passes.size(); ++i) E.smem[i] = sdb::tile_pass_smem(A.passes[i]);
     if (jit) {
         E.jit_fn = sdb::jit_pass_kernels(A, s.device);
+        for (size_t i = 0; i < A.passes.size(); ++i) E.smem[i] += sdb::jit_pass_smem_extra(A, i);
     }
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t sizes[] = {

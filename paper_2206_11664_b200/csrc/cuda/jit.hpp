@@ -22,5 +22,7 @@ void launch_tile_pass_jit(void* fn, StateImpl& s, const PassDev& ph, int pass_in
 size_t jit_compile_only(const HostPlanArrays& A);
 // dynamic shared memory of a tile pass (same for both kernel kinds)
 size_t tile_pass_smem(const PassDev& ph);
+// extra dynamic shared memory of pass `pass`'s specialised kernel (TMA split stage)
+size_t jit_pass_smem_extra(const HostPlanArrays& A, size_t pass);
 
 }  // namespace sdb

@@ -399,6 +399,7 @@ struct PassCtx {
     RegCfg rc;
     double2* pat_tab = nullptr;  // POINT mode 5: [1 << kPatTerms] phase per sign pattern of the terms
     uint32_t mbar = 0;       // TMA: mbarrier of the tile staged in buf
+    uint32_t mbar2 = 0;      // TMA split stage: mbarrier of the early half (0: one stage)
     const void* tmap = nullptr;  // TMA: the tensor map (address of the __grid_constant__ parameter)
     uint32_t tma_phase = 0;  // TMA: parity of the next completion to wait for
 
@@ -406,7 +407,7 @@ struct PassCtx {
                                        double2* const* xdst_, double neg_dt_, uint64_t rank_bits_, uint64_t n_tiles_,
                                        unsigned char* smem_raw,
                                        uint64_t* off_lo_, uint64_t* off_hi_, uint64_t* s_tbase_, uint32_t* s_pl_,
-                                       uint32_t* s_ph_)
+                                       uint32_t* s_ph_, int stage_extra = 0)
         : P(P_), plan(plan_), psi(psi_), out(out_), xdst(xdst_), neg_dt(neg_dt_), rank_bits(rank_bits_), n_tiles(n_tiles_),
           off_lo(off_lo_), off_hi(off_hi_), s_tbase(s_tbase_), s_pl(s_pl_), s_ph(s_ph_) {
         tid = threadIdx.x;
@@ -427,7 +428,9 @@ struct PassCtx {
         store_perm = P.store_perm != 0;
         scale = P.scale;  // exact power of two
         buf = reinterpret_cast<double2*>(smem_raw);  // transpose buffer
-        tab = reinterpret_cast<double*>(buf + N);    // per-tile tables (if any)
+        // TMA split stage: stage_extra more amplitude slots after the transpose
+        // buffer hold the early half of the next tile (SDB_PASS_KERNEL_BODY_TMA)
+        tab = reinterpret_cast<double*>(buf + N + stage_extra);  // per-tile tables (if any)
         // The micro-ops are staged in shared memory (the planner caps a pass's
         // length); per-thread config bases and QT tables are read through L1.
         s_ops = reinterpret_cast<MicroOpDev*>(tab + P.tab_words);
@@ -632,14 +635,19 @@ struct PassCtx {
             for (int s = 0; s < NR; ++s) prefetch_l2(gn + o[s]);
         }
 #endif
+        // split stage: the early half (issued during the previous tile's
+        // transposes) first, then the late half
+        if (mbar2) mbar_wait(mbar2, tma_phase);
         mbar_wait(mbar, tma_phase);
         tma_phase ^= 1u;
+        // slots -> buffer positions are GF(2)-affine (the split stage moves the
+        // early half behind the transpose buffer): XOR-combine the offsets
         uint32_t a[NR];
         a[0] = tsl0;
 #pragma unroll
         for (int j = 0; j < R; ++j)
 #pragma unroll
-            for (int s = 0; s < (1 << j); ++s) a[s + (1 << j)] = a[s] | tso[j];
+            for (int s = 0; s < (1 << j); ++s) a[s + (1 << j)] = a[s] ^ tso[j];
 #pragma unroll
         for (int s = 0; s < NR; ++s) v[s] = buf[a[s]];
     }
@@ -1096,20 +1104,27 @@ struct PassCtx {
 
 // TMA variant: the first tile's boxes are issued after setup; each program
 // issues the next tile's boxes itself once its last transpose is done
-// (Prog::tma_next), and its LOAD waits on the mbarrier.
-#define SDB_PASS_KERNEL_BODY_TMA(K, RB, PROG)                                                              \
+// (Prog::tma_next), and its LOAD waits on the mbarrier. With SPLIT the next
+// tile's early half goes to a half-tile stage behind the transpose buffer
+// right after the program's first transpose (Prog::tma_early; mbarrier 1), the
+// late half into the transpose buffer after the last one (mbarrier 0).
+#define SDB_PASS_KERNEL_BODY_TMA(K, RB, PROG, SPLIT)                                                       \
     using Ctx = ::sdb::dev::PassCtx<K, RB>;                                                                \
     extern __shared__ __align__(128) unsigned char smem_raw[];                                             \
     __shared__ uint64_t sdb_off_lo[1 << Ctx::LO];                                                          \
     __shared__ uint64_t sdb_off_hi[1 << Ctx::HI];                                                          \
     __shared__ uint64_t sdb_tbase[::sdb::dev::kTbaseChunks * 128];                                         \
     __shared__ uint32_t sdb_pl[3 * 64], sdb_ph[3 * 64];                                                    \
-    __shared__ __align__(8) uint64_t sdb_mbar;                                                             \
+    __shared__ __align__(8) uint64_t sdb_mbar[2];                                                          \
     Ctx ctx(plan.passes[pass_index], plan, psi, out, xdst, neg_dt, rank_bits, n_tiles, smem_raw, sdb_off_lo, \
-            sdb_off_hi, sdb_tbase, sdb_pl, sdb_ph);                                                        \
-    ctx.mbar = ::sdb::dev::smem_u32(&sdb_mbar);                                                            \
+            sdb_off_hi, sdb_tbase, sdb_pl, sdb_ph, (SPLIT) ? Ctx::N / 2 : 0);                              \
+    ctx.mbar = ::sdb::dev::smem_u32(&sdb_mbar[0]);                                                         \
+    ctx.mbar2 = (SPLIT) ? ::sdb::dev::smem_u32(&sdb_mbar[1]) : 0u;                                         \
     ctx.tmap = &tmap;                                                                                      \
-    if (threadIdx.x == 0) ::sdb::dev::mbar_init(ctx.mbar);                                                 \
+    if (threadIdx.x == 0) {                                                                                \
+        ::sdb::dev::mbar_init(ctx.mbar);                                                                   \
+        if (SPLIT) ::sdb::dev::mbar_init(ctx.mbar2);                                                       \
+    }                                                                                                      \
     __shared__ double2 sdb_pat[1 << ::sdb::dev::kPatTerms];                                                 \
     ctx.pat_tab = sdb_pat;                                                                                 \
     ctx.setup();                                                                                           \

@@ -37,6 +37,7 @@ struct StepExec {
     std::vector<int> seg_first, seg_count;
     std::vector<void*> jit_fn;    // specialised kernel per pass (nullptr = interpreter)
     std::vector<size_t> smem;     // dynamic shared memory per pass
+    std::vector<int> threads;     // block size per specialised pass kernel (0: the kernel's default)
     sdb::PlanDev dev{};
     void* dev_block = nullptr;
     double2* tile_phase = nullptr;  // per-tile constant phases (passes with tphase_off >= 0)
@@ -281,11 +282,20 @@ const int kTableThreshold = [] {
     return e ? std::atoi(e) : 0;  // 0: the pass's largest phase stage always gets the table
 }();
 
+// Register coordinates of specialised kernels (SDB_RBITS=3..5); the
+// interpreter kernel always runs 4.
+int jit_rbits() {
+    static const int r = [] {
+        const char* e = std::getenv("SDB_RBITS");
+        return e ? std::clamp(std::atoi(e), 3, sdb::kMaxR) : 4;
+    }();
+    return r;
+}
+
 void upload_step(sd_plan& p, StepExec& E, const sdb::StepPlan& combined) {
     sdb::StateImpl& s = p.state->impl;
     const bool jit = sdb::jit_wanted(s.n_local);
-    int rbits = 4;
-    if (const char* e = std::getenv("SDB_RBITS"); e && jit) rbits = std::atoi(e) == 3 ? 3 : 4;
+    const int rbits = jit ? jit_rbits() : 4;
     sdb::HostPlanArrays A = sdb::lower_plan(combined, s.n_local, kTableThreshold, rbits);
     A.tma = p.knobs.tma;
     sdb::verify_lowering(A);  // register-config bookkeeping of lane swaps (host check, cheap)
@@ -296,7 +306,11 @@ void upload_step(sd_plan& p, StepExec& E, const sdb::StepPlan& combined) {
     for (size_t i = 0; i < A.passes.size(); ++i) E.smem[i] = sdb::tile_pass_smem(A.passes[i]);
     if (jit) {
         E.jit_fn = sdb::jit_pass_kernels(A, s.device);
-        for (size_t i = 0; i < A.passes.size(); ++i) E.smem[i] += sdb::jit_pass_smem_extra(A, i);
+        E.threads.resize(A.passes.size());
+        for (size_t i = 0; i < A.passes.size(); ++i) {
+            E.smem[i] += sdb::jit_pass_smem_extra(A, i);
+            E.threads[i] = sdb::jit_pass_threads(A, i);
+        }
     }
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t sizes[] = {
@@ -672,7 +686,7 @@ void run_segment(sd_plan& p, StepExec& E, size_t seg, double dt) {
         record_start(p, xdst ? 2 : E.pass_class[i]);
         if (E.jit_fn[i]) {
             sdb::launch_tile_pass_jit(E.jit_fn[i], s, E.host_passes[i], i, E.dev, dt, rank_bits,
-                                      to_buf ? s.xbuf : nullptr, E.smem[i], xdst);
+                                      to_buf ? s.xbuf : nullptr, E.smem[i], xdst, E.threads[i]);
         } else {
             sdb::launch_tile_pass(s, E.host_passes[i], i, E.dev, dt, rank_bits, to_buf ? s.xbuf : nullptr, xdst);
         }
@@ -1562,7 +1576,7 @@ sd_status sd_jit_compile_preview(int n, int world, const sd_group_desc* groups, 
         combined.tile_qubits = k;
         for (const sdb::Segment& sg : ss.segs)
             for (const sdb::PassPlan& pp : sg.plan.passes) combined.passes.push_back(pp);
-        const sdb::HostPlanArrays A = sdb::lower_plan(combined, n_local, kTableThreshold, 4);
+        const sdb::HostPlanArrays A = sdb::lower_plan(combined, n_local, kTableThreshold, jit_rbits());
         const size_t np = sdb::jit_compile_only(A);
         if (n_programs) *n_programs = np;
     });

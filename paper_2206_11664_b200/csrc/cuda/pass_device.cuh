@@ -48,6 +48,33 @@ __device__ __forceinline__ uint32_t pext32(uint32_t v, uint32_t mask) {
 #define SDB_TILE_STORE __stcs
 #endif
 
+// Ring mode (SDB_RING, specialised TMA programs): one CTA per SM runs kGroups
+// warp groups of NT threads on alternate tiles of the CTA's sequence; three
+// shared-memory stages rotate between them, so a tile's TMA boxes are issued
+// when the tile three places earlier has finished its last transpose (about a
+// tile of lead time instead of the tail of one). Group barriers are named
+// barriers 1..kGroups of NT threads; barrier 0 (__syncthreads) stays CTA-wide.
+#ifdef SDB_RING
+constexpr int kGroups = 2;
+constexpr int kStages = 3;
+#else
+constexpr int kGroups = 1;
+constexpr int kStages = 1;
+#endif
+template <int NT>
+__device__ __forceinline__ void gsync() {
+    if constexpr (kGroups > 1) {
+        asm volatile("bar.sync %0, %1;\n" ::"r"(1u + threadIdx.x / NT), "n"(NT) : "memory");
+    } else {
+        __syncthreads();
+    }
+}
+// thread index within its warp group
+template <int NT>
+__device__ __forceinline__ uint32_t ltid() {
+    return kGroups > 1 ? (threadIdx.x & (NT - 1u)) : threadIdx.x;
+}
+
 __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
@@ -174,6 +201,21 @@ __device__ __forceinline__ void lane_swap(double2 (&v)[1 << R]) {
     }
 }
 
+// Butterfly on the coordinate held by lane bit B: the low lane gets a + d, the
+// high lane a - d (fma with +-1 rounds exactly like the register butterfly's
+// add / subtract, so the result is bit-identical). 2 shuffles per double, no
+// selects, config unchanged.
+template <int R, int B>
+__device__ __forceinline__ void lane_bfly(double2 (&v)[1 << R]) {
+    const double sg = ((threadIdx.x >> B) & 1u) ? -1.0 : 1.0;
+#pragma unroll
+    for (int s = 0; s < (1 << R); ++s) {
+        const double yx = __shfl_xor_sync(0xffffffffu, v[s].x, 1 << B);
+        const double yy = __shfl_xor_sync(0xffffffffu, v[s].y, 1 << B);
+        v[s] = make_double2(fma(sg, v[s].x, yx), fma(sg, v[s].y, yy));
+    }
+}
+
 template <int R>
 __device__ __forceinline__ void bfly_dispatch(double2 (&v)[1 << R], uint32_t mask) {
     switch (mask & ((1u << R) - 1u)) {
@@ -195,7 +237,7 @@ __device__ __forceinline__ void wht_round(double* __restrict__ tab, int size) {
     constexpr int M = 1 << RB;
     const int groups = size >> RB;
     constexpr uint32_t lowm = (1u << LO) - 1u;
-    for (int gi = threadIdx.x; gi < groups; gi += NT) {
+    for (int gi = static_cast<int>(ltid<NT>()); gi < groups; gi += NT) {
         const uint32_t g = static_cast<uint32_t>(gi);
         const uint32_t b = tsw(((g >> LO) << (LO + RB)) | (g & lowm));
         double w[M];
@@ -222,7 +264,7 @@ __device__ __forceinline__ void wht_rounds(double* __restrict__ tab) {
     if constexpr (LO < BITS) {
         constexpr int RB = BITS - LO >= 2 ? 2 : 1;
         wht_round<NT, LO, RB>(tab, 1 << BITS);
-        __syncthreads();
+        gsync<NT>();
         wht_rounds<NT, LO + RB, BITS>(tab);
     }
 }
@@ -259,7 +301,7 @@ __device__ __forceinline__ void build_factor_tables(double* __restrict__ tab, co
     const int n0 = 1 << pt.fac_bits[0];
     const int n1 = pt.n_fac > 1 ? 1 << pt.fac_bits[1] : 0;
     const int n2 = pt.n_fac > 2 ? 1 << pt.fac_bits[2] : 0;
-    for (int e = threadIdx.x; e < n0 + n1 + n2; e += NT) {
+    for (int e = static_cast<int>(ltid<NT>()); e < n0 + n1 + n2; e += NT) {
         const int f = e < n0 ? 0 : (e < n0 + n1 ? 1 : 2);
         const uint32_t u = static_cast<uint32_t>(e - (f == 0 ? 0 : (f == 1 ? n0 : n0 + n1)));
         double th = 0.0;
@@ -308,21 +350,21 @@ __device__ __forceinline__ double2 tile_constant_phase(const PlanDev& plan, cons
 template <int NT>
 __device__ void build_tables(double* __restrict__ tab, const PlanDev& plan, const PointDev& pt, uint64_t full,
                              double neg_dt, double tscale, bool nosync) {
-    const int tid = threadIdx.x;
+    const int tid = static_cast<int>(ltid<NT>());
     if (pt.n_fac > 0 && nosync) {
         // double-buffered tables; the program's transposes order the writes
         // before the POINT reads and this tile's reads before the reuse
         build_factor_tables<NT>(tab, plan, pt, full, neg_dt, tscale);
         return;
     }
-    __syncthreads();  // previous tile's readers are done with tab
+    gsync<NT>();  // previous tile's readers are done with tab
     if (pt.n_fac > 0) {
         build_factor_tables<NT>(tab, plan, pt, full, neg_dt, tscale);
-        __syncthreads();
+        gsync<NT>();
         return;
     }
     for (int u = tid; u < (1 << pt.table_bits); u += NT) tab[u] = 0.0;
-    __syncthreads();
+    gsync<NT>();
     const uint64_t* zh = plan.term_hmask + pt.term_off;
     const double* cf = plan.term_coeffs + pt.term_off;
     for (int s = tid; s < pt.n_seg; s += NT) {
@@ -334,7 +376,7 @@ __device__ void build_tables(double* __restrict__ tab, const PlanDev& plan, cons
         }
         tab[tsw(sg.u)] = acc;
     }
-    __syncthreads();
+    gsync<NT>();
     wht_table<NT>(tab, pt.table_bits);
 }
 
@@ -357,9 +399,10 @@ constexpr int kPatTerms = 6;     // POINT mode 5: at most 2^6 sign patterns per 
 // local index / swizzled slot, the local coordinate (byte j of cidx) and
 // slot offset of register coordinate j, and its physical offset.
 struct RegCfg {
-    uint32_t tb, swt, cidx;
-    uint32_t swc[4];
-    uint64_t coff[4];
+    uint32_t tb, swt;
+    uint64_t cidx;
+    uint32_t swc[kMaxR];
+    uint64_t coff[kMaxR];
 };
 
 // Per-CTA state of one tile pass plus the op implementations. The compiled
@@ -402,6 +445,10 @@ struct PassCtx {
     uint32_t mbar2 = 0;      // TMA split stage: mbarrier of the early half (0: one stage)
     const void* tmap = nullptr;  // TMA: the tensor map (address of the __grid_constant__ parameter)
     uint32_t tma_phase = 0;  // TMA: parity of the next completion to wait for
+    double2* ring = nullptr; // ring mode: the kStages tile stages
+    uint32_t mbar0 = 0;      // ring mode: the 2 kStages mbarriers (see set_stage)
+    uint64_t ring_i = 0;     // ring mode: index of the current tile in this CTA's sequence
+    uint64_t ahead;          // tile distance of the TMA issue (ring: kStages tiles of this CTA)
 
     __device__ __forceinline__ PassCtx(const PassDev& P_, const PlanDev& plan_, const double2* psi_, double2* out_,
                                        double2* const* xdst_, double neg_dt_, uint64_t rank_bits_, uint64_t n_tiles_,
@@ -410,7 +457,7 @@ struct PassCtx {
                                        uint32_t* s_ph_, int stage_extra = 0)
         : P(P_), plan(plan_), psi(psi_), out(out_), xdst(xdst_), neg_dt(neg_dt_), rank_bits(rank_bits_), n_tiles(n_tiles_),
           off_lo(off_lo_), off_hi(off_hi_), s_tbase(s_tbase_), s_pl(s_pl_), s_ph(s_ph_) {
-        tid = threadIdx.x;
+        tid = static_cast<int>(ltid<NT>());
         if (P.blocked) {
             // contiguous block of tiles per CTA: consecutive tiles share the
             // phase tables' sign pattern (PassDev::pat_shift)
@@ -423,17 +470,21 @@ struct PassCtx {
             t_last = n_tiles;
             stride = gridDim.x;
         }
+        ahead = stride * kStages;
         has_table = P.table_point >= 0;
         last_pat = ~0ull;
         store_perm = P.store_perm != 0;
         scale = P.scale;  // exact power of two
         buf = reinterpret_cast<double2*>(smem_raw);  // transpose buffer
+        ring = buf;
         // TMA split stage: stage_extra more amplitude slots after the transpose
-        // buffer hold the early half of the next tile (SDB_PASS_KERNEL_BODY_TMA)
-        tab = reinterpret_cast<double*>(buf + N + stage_extra);  // per-tile tables (if any)
+        // buffer hold the early half of the next tile (SDB_PASS_KERNEL_BODY_TMA);
+        // ring mode: kStages stages, then one table region per warp group
+        double* const tab0 = reinterpret_cast<double*>(buf + kStages * N + stage_extra);
+        tab = tab0 + (threadIdx.x / NT) * P.tab_words;  // per-tile tables (if any)
         // The micro-ops are staged in shared memory (the planner caps a pass's
         // length); per-thread config bases and QT tables are read through L1.
-        s_ops = reinterpret_cast<MicroOpDev*>(tab + P.tab_words);
+        s_ops = reinterpret_cast<MicroOpDev*>(tab0 + kGroups * P.tab_words);
         s_cfg = plan.cfg_tb + P.cfg_off;
         s_qt = reinterpret_cast<const uint32_t*>(plan.qt_words + P.qt_off);  // staged into smem in setup()
         // store-side index tables (only for passes that store through a local
@@ -446,6 +497,9 @@ struct PassCtx {
 
     // ---- stage the program and the index tables (once per launch)
     __device__ __forceinline__ void setup() {
+        // every thread of the CTA (all warp groups) stages the shared tables
+        const int tid = static_cast<int>(threadIdx.x);
+        constexpr int NT = C::NT * kGroups;
         const int n_outer = P.n_outer;
         {
             const int4* src = reinterpret_cast<const int4*>(plan.ops + P.op_off);
@@ -509,7 +563,7 @@ struct PassCtx {
                 }
             }
         }
-        __syncthreads();
+        __syncthreads();  // CTA-wide: every group reads the staged tables
     }
 
     __device__ __forceinline__ uint64_t tile_base(uint64_t tt) const {
@@ -521,6 +575,25 @@ struct PassCtx {
     __device__ __forceinline__ uint64_t off_of(uint32_t l) const {
         return off_lo[l & ((1u << LO) - 1u)] | off_hi[l >> LO];
     }
+
+    // Ring mode: tile i of this CTA's sequence is staged in stage i % kStages.
+    // Each stage alternates between two mbarriers, so tile i completes barrier
+    // (stage, (i / kStages) & 1) for the (i / 2 kStages)-th time. With a single
+    // barrier per stage the group waiting for tile i could run ahead of the
+    // other group's tile i - kStages and see that older phase's parity
+    // (aliasing); with two, the previous completion of tile i's barrier is
+    // tile i - 2 kStages, which the same group consumed before.
+    __device__ __forceinline__ uint32_t mbar_of(uint64_t i) const {
+        return mbar0 + 8u * static_cast<uint32_t>((i % kStages) * 2 + ((i / kStages) & 1u));
+    }
+    __device__ __forceinline__ void set_stage(uint64_t i) {
+        ring_i = i;
+        buf = ring + static_cast<uint32_t>(i % kStages) * N;
+        mbar = mbar_of(i);
+        tma_phase = static_cast<uint32_t>((i / (2 * kStages)) & 1u);
+    }
+    // mbarrier the boxes of tile t + ahead complete on (issued from this stage)
+    __device__ __forceinline__ uint32_t mbar_next() const { return kStages > 1 ? mbar_of(ring_i + kStages) : mbar; }
 
     __device__ __forceinline__ void begin_tile(uint64_t tt) {
         t = tt;
@@ -538,12 +611,11 @@ struct PassCtx {
         r.tb = w & 0xffffu;
         r.swt = w >> 16;
         r.cidx = op.cidx;
-        r.swc[0] = op.swc01 & 0xffffu;
-        r.swc[1] = op.swc01 >> 16;
-        r.swc[2] = op.swc23 & 0xffffu;
-        r.swc[3] = op.swc23 >> 16;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) r.coff[j] = op.c_off[j];
+        for (int j = 0; j < kMaxR; ++j) {
+            r.swc[j] = op.swc[j];
+            r.coff[j] = op.c_off[j];
+        }
         return r;
     }
 
@@ -552,7 +624,7 @@ struct PassCtx {
     // base + thread + register, and a tile address is one per-thread pointer
     // plus a per-register offset (an immediate when the JIT bakes the
     // config's offsets in).
-    __device__ __forceinline__ void reg_offsets(uint64_t (&o)[NR], const uint64_t (&coff)[4]) const {
+    __device__ __forceinline__ void reg_offsets(uint64_t (&o)[NR], const uint64_t (&coff)[kMaxR]) const {
         o[0] = 0;
 #pragma unroll
         for (int j = 0; j < R; ++j)
@@ -603,7 +675,7 @@ struct PassCtx {
             if (pat != last_pat) {
                 // the previous tile's POINT may still be reading the tables when
                 // no transpose (block barrier) follows it in the program
-                if (last_pat != ~0ull) __syncthreads();
+                if (last_pat != ~0ull) gsync<NT>();
                 last_pat = pat;
                 build_tables<NT>(tabc(), plan, plan.points[P.table_point], full, neg_dt, P.table_scale, false);
             }
@@ -614,13 +686,13 @@ struct PassCtx {
     // tsl(l) (the box layout, GF(2)-linear in l); tsl0 is this thread's
     // register-0 slot, tso[j] the slot offset of register coordinate j.
     __device__ __forceinline__ void load_tma(const RegCfg& r, double2 (&v)[NR], uint32_t tsl0,
-                                             const uint32_t (&tso)[4]) {
+                                             const uint32_t (&tso)[kMaxR]) {
         rc = r;
         // per-tile phase tables are built while the tile's boxes are in flight
         if (has_table) {
             const uint64_t pat = P.pat_shift >= 64 ? t : (t >> P.pat_shift);
             if (pat != last_pat) {
-                if (last_pat != ~0ull) __syncthreads();
+                if (last_pat != ~0ull) gsync<NT>();
                 last_pat = pat;
                 build_tables<NT>(tabc(), plan, plan.points[P.table_point], full, neg_dt, P.table_scale, false);
             }
@@ -637,8 +709,10 @@ struct PassCtx {
 #endif
         // split stage: the early half (issued during the previous tile's
         // transposes) first, then the late half
+#ifndef SDB_EXPERIMENT_NOTMA
         if (mbar2) mbar_wait(mbar2, tma_phase);
         mbar_wait(mbar, tma_phase);
+#endif
         tma_phase ^= 1u;
         // slots -> buffer positions are GF(2)-affine (the split stage moves the
         // early half behind the transpose buffer): XOR-combine the offsets
@@ -655,7 +729,7 @@ struct PassCtx {
     // shared-memory transpose into config r; op.perm >= 0 applies a pending
     // CNOT index map on the write side
     __device__ __forceinline__ void cfg(const MicroOpDev& op, const RegCfg& r, double2 (&v)[NR]) {
-        if (smem_busy) __syncthreads();
+        if (smem_busy) gsync<NT>();
         if (op.perm >= 0) {
             const PermDev* pm = plan.perms + op.perm;
             uint32_t sb = 0;
@@ -679,7 +753,7 @@ struct PassCtx {
 #pragma unroll
             for (int s = 0; s < NR; ++s) buf[a[s]] = v[s];
         }
-        __syncthreads();
+        gsync<NT>();
         rc = r;
         {
             uint32_t a[NR];
@@ -696,8 +770,8 @@ struct PassCtx {
     // lands at slot m(tb) ^ XOR_{j in s} lm[j] -- two table reads per thread
     // instead of two per amplitude.
     __device__ __forceinline__ void cfg_lin(const MicroOpDev& op, const RegCfg& r, double2 (&v)[NR],
-                                            const uint32_t (&lm)[4]) {
-        if (smem_busy) __syncthreads();
+                                            const uint32_t (&lm)[kMaxR]) {
+        if (smem_busy) gsync<NT>();
         const PermDev* pm = plan.perms + op.perm;
         uint32_t sb = 0;
         for (int j = 0; j < pm->n_ctrl; ++j)
@@ -711,7 +785,7 @@ struct PassCtx {
             for (int s = 0; s < (1 << j); ++s) m[s + (1 << j)] = m[s] ^ lm[j];
 #pragma unroll
         for (int s = 0; s < NR; ++s) buf[m[s]] = v[s];
-        __syncthreads();
+        gsync<NT>();
         rc = r;
         {
             uint32_t a[NR];
@@ -756,8 +830,8 @@ struct PassCtx {
     // passes literals, the interpreter decodes the staged op (point_cfg).
     struct PointCfg {
         uint32_t qr;         // bit s: QT(r_s)
-        uint32_t tc[4];      // full table: swizzled compact offsets of the register coordinates
-        uint32_t fo[3][4];   // factor tables: swizzled compact offsets per factor
+        uint32_t tc[kMaxR];      // full table: swizzled compact offsets of the register coordinates
+        uint32_t fo[3][kMaxR];   // factor tables: swizzled compact offsets per factor
         int coffE[3];        // factor tables: double offsets in the table region
         // S/CZ quadratic form of the tile (literals in specialised kernels;
         // n_lo < 0: read PointDev's pair lists at run time)
@@ -772,15 +846,13 @@ struct PassCtx {
     __device__ __forceinline__ PointCfg point_cfg(const MicroOpDev& op, const PointDev& pt) const {
         PointCfg c;
         c.qr = static_cast<uint32_t>(op.pad);
-        c.tc[0] = tsw(op.swc01 & 0xffffu);
-        c.tc[1] = tsw(op.swc01 >> 16);
-        c.tc[2] = tsw(op.swc23 & 0xffffu);
-        c.tc[3] = tsw(op.swc23 >> 16);
+#pragma unroll
+        for (int j = 0; j < kMaxR; ++j) c.tc[j] = tsw(op.swc[j]);
 #pragma unroll
         for (int f = 0; f < 3; ++f) {
             c.coffE[f] = pt.fac_coff[f];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) c.fo[f][j] = static_cast<uint32_t>(op.c_off[f] >> (16 * j)) & 0xffffu;
+            for (int j = 0; j < kMaxR; ++j) c.fo[f][j] = op.fo[f][j];
         }
         c.n_lo = -1;
         c.n_oo = 0;
@@ -799,14 +871,16 @@ struct PassCtx {
     __device__ __forceinline__ void point(const MicroOpDev& op, const PointCfg& pc, double2 (&v)[NR]) {
         const PointDev& pt = plan.points[op.arg];
         const bool scale_here = (op.mask & 1u) != 0;
-        uint32_t cb[4];
+        uint32_t cb[R];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) cb[j] = 1u << ((rc.cidx >> (8 * j)) & 255u);
+        for (int j = 0; j < R; ++j) cb[j] = 1u << ((rc.cidx >> (8 * j)) & 255u);
         // ---- quarter turns: q(tb ^ r_s) = q0 + sum_{j in s} dq_j + 2 QT(r_s)  (mod 4)
         // (QT is a quadratic form: QT(a^b) = QT(a) + QT(b) + B(a,b), B bilinear)
         uint32_t m2 = pc.s2L;
         unsigned q0 = 0;
-        unsigned dq[4] = {0u, 0u, 0u, 0u};
+        unsigned dq[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) dq[j] = 0u;
         auto oo_term = [&](uint64_t m) -> unsigned {
             // 2 * bit_a * popc(full & partners(a)), a = lowest bit of m
             return ((full & m & (~m + 1ull)) != 0ull) ? 2u * __popcll(full & (m & (m - 1ull))) : 0u;
@@ -832,7 +906,7 @@ struct PassCtx {
         const unsigned qt_tb = qtb(rc.tb);
         q0 += __popc(rc.tb & pc.s1L) + 2u * (__popc(rc.tb & m2) + qt_tb);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < R; ++j) {
             const unsigned bil = qt ? (qtb(rc.tb ^ cb[j]) ^ qt_tb ^ qtb(cb[j])) : 0u;
             dq[j] = __popc(cb[j] & pc.s1L) + 2u * (__popc(cb[j] & m2) + bil);
         }
@@ -875,7 +949,7 @@ struct PassCtx {
             // POINT, the previous tile's) are done before the table is rewritten
             double2* tabp = pat_tab;
             const int m = pt.n_terms;
-            __syncthreads();
+            gsync<NT>();
             for (int e = tid; e < (1 << m); e += NT) {
                 double ang = 0.0;
 #pragma unroll
@@ -890,7 +964,7 @@ struct PassCtx {
                 }
                 tabp[e] = make_double2(cs, sn);
             }
-            __syncthreads();
+            gsync<NT>();
             ptab = tabp;
         }
         // q of every register combination, one add each
@@ -1000,14 +1074,17 @@ struct PassCtx {
     }
 
     __device__ __forceinline__ void store(const MicroOpDev& op, double2 (&v)[NR]) {
-        store_f<-1>(op, op.c_off, v);
+        uint64_t so[kMaxR];
+#pragma unroll
+        for (int j = 0; j < kMaxR; ++j) so[j] = op.c_off[j];
+        store_f<-1>(op, so, v);
     }
 
     // soff: sigma-mapped physical offsets of the register coordinates (kStSigma)
     template <int F>
-    __device__ __forceinline__ void store_f(const MicroOpDev& op, const uint64_t (&soff)[4], double2 (&v)[NR]) {
+    __device__ __forceinline__ void store_f(const MicroOpDev& op, const uint64_t (&soff)[kMaxR], double2 (&v)[NR]) {
         const int f = F >= 0 ? F : store_flags(op);
-        if (f & kStSync) __syncthreads();  // cross-warp in-place store with no barrier since the load
+        if (f & kStSync) gsync<NT>();  // cross-warp in-place store with no barrier since the load
         uint64_t o[NR];
         double2* go;
         if (f & kStSigma) {
@@ -1056,6 +1133,9 @@ struct PassCtx {
             reg_offsets(o, rc.coff);
         }
         const bool sc = (f & kStScale) != 0;
+#ifdef SDB_EXPERIMENT_NOSTORE
+        if (neg_dt != 1234.5) return;
+#endif
         if ((f & kStXchg) && xdst) {
             // fused exchange: every amplitude goes straight to its receiving
             // rank's buffer (peer memory over NVLink), at its final position
@@ -1128,8 +1208,49 @@ struct PassCtx {
     __shared__ double2 sdb_pat[1 << ::sdb::dev::kPatTerms];                                                 \
     ctx.pat_tab = sdb_pat;                                                                                 \
     ctx.setup();                                                                                           \
-    if (threadIdx.x < 32u && ctx.t_first < ctx.t_last) PROG.tma_issue(ctx, ctx.tile_base(ctx.t_first), threadIdx.x); \
+    if (threadIdx.x < 32u && ctx.t_first < ctx.t_last)                                                    \
+        PROG.tma_issue(ctx, ctx.tile_base(ctx.t_first), threadIdx.x, ctx.mbar);                            \
     for (uint64_t t = ctx.t_first; t < ctx.t_last; t += ctx.stride) {                                      \
+        ctx.begin_tile(t);                                                                                 \
+        double2 v[Ctx::NR];                                                                                \
+        PROG(ctx, v);                                                                                      \
+    }
+
+// Ring variant (SDB_RING): kGroups warp groups of NT threads take alternate
+// tiles of the CTA's sequence; stages 0..kStages-1 are issued after setup and
+// each program re-issues its stage for the tile kStages places later once its
+// last transpose is done (Prog::tma_next with ctx.ahead).
+#define SDB_PASS_KERNEL_BODY_RING(K, RB, PROG)                                                             \
+    using Ctx = ::sdb::dev::PassCtx<K, RB>;                                                                \
+    extern __shared__ __align__(128) unsigned char smem_raw[];                                             \
+    __shared__ uint64_t sdb_off_lo[1 << Ctx::LO];                                                          \
+    __shared__ uint64_t sdb_off_hi[1 << Ctx::HI];                                                          \
+    __shared__ uint64_t sdb_tbase[::sdb::dev::kTbaseChunks * 128];                                         \
+    __shared__ uint32_t sdb_pl[3 * 64], sdb_ph[3 * 64];                                                    \
+    __shared__ __align__(8) uint64_t sdb_mbar[2 * ::sdb::dev::kStages];                                    \
+    Ctx ctx(plan.passes[pass_index], plan, psi, out, xdst, neg_dt, rank_bits, n_tiles, smem_raw, sdb_off_lo, \
+            sdb_off_hi, sdb_tbase, sdb_pl, sdb_ph);                                                        \
+    ctx.mbar0 = ::sdb::dev::smem_u32(&sdb_mbar[0]);                                                        \
+    ctx.tmap = &tmap;                                                                                      \
+    if (threadIdx.x == 0) {                                                                                \
+        for (int st = 0; st < 2 * ::sdb::dev::kStages; ++st) ::sdb::dev::mbar_init(ctx.mbar0 + 8u * st);   \
+    }                                                                                                      \
+    __shared__ double2 sdb_pat[::sdb::dev::kGroups][1 << ::sdb::dev::kPatTerms];                           \
+    const uint32_t sdb_group = threadIdx.x / Ctx::NT;                                                      \
+    ctx.pat_tab = sdb_pat[sdb_group];                                                                      \
+    ctx.setup();                                                                                           \
+    if (threadIdx.x < 32u) {                                                                               \
+        for (uint64_t st = 0; st < ::sdb::dev::kStages; ++st) {                                            \
+            const uint64_t tt = ctx.t_first + st * ctx.stride;                                             \
+            if (tt >= ctx.t_last) break;                                                                   \
+            ctx.set_stage(st);                                                                             \
+            PROG.tma_issue(ctx, ctx.tile_base(tt), threadIdx.x, ctx.mbar);                                 \
+        }                                                                                                  \
+    }                                                                                                      \
+    for (uint64_t i = sdb_group;; i += ::sdb::dev::kGroups) {                                              \
+        const uint64_t t = ctx.t_first + i * ctx.stride;                                                   \
+        if (t >= ctx.t_last) break;                                                                        \
+        ctx.set_stage(i);                                                                                  \
         ctx.begin_tile(t);                                                                                 \
         double2 v[Ctx::NR];                                                                                \
         PROG(ctx, v);                                                                                      \

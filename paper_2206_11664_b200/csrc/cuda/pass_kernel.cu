@@ -32,6 +32,9 @@ struct Interpreter {
                 ctx.swap_any(op, ctx.cfg_of(op), v);
             } else if (kind == kOpBfly) {
                 dev::bfly_dispatch<Ctx::R>(v, op.mask);
+            } else if (kind == kOpLaneBfly) {
+                if (op.mask == 3) dev::lane_bfly<Ctx::R, 3>(v);
+                else dev::lane_bfly<Ctx::R, 4>(v);
             } else if (kind == kOpPoint) {
                 ctx.point_any(op, v);
             } else {

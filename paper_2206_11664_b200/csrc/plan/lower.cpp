@@ -109,6 +109,14 @@ int lane_swap_mode() {
     return m;
 }
 bool lane_swaps_enabled() { return (lane_swap_mode() & 3) != 0; }
+// SDB_LANE_BFLY=0: lane swaps only (no in-place cross-lane butterflies)
+bool lane_bfly_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SDB_LANE_BFLY");
+        return !e || std::atoi(e) != 0;
+    }();
+    return on;
+}
 
 // Factor cover of a table point: split the coordinates its terms touch into
 // at most three disjoint sets of <= kMaxFacBits coordinates such that no
@@ -274,7 +282,7 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
         // current config: register slot j holds coordinate regc[j], thread
         // bit b holds thr[b] (lanes are thread bits 0..4)
         uint32_t cur = 0;
-        int regc[4] = {0, 0, 0, 0};
+        int regc[kMaxR] = {0, 0, 0, 0, 0};
         std::vector<int> thr;
         bool loaded = false;
         bool scale_placed = false;
@@ -323,7 +331,7 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
             return idx;
         };
         // a config given explicitly (register coordinates, thread order)
-        auto emit_explicit = [&](int kind, const int (&rc)[4], const std::vector<int>& order, uint32_t mask) {
+        auto emit_explicit = [&](int kind, const int (&rc)[kMaxR], const std::vector<int>& order, uint32_t mask) {
             MicroOpDev op{};
             op.kind = kind;
             op.mask = mask;
@@ -337,18 +345,15 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                 }
                 A.cfg_tb.push_back(tb | (host_swz(tb) << 16));
             }
-            uint32_t sw[4] = {0, 0, 0, 0};
             cur = 0;
             for (int j = 0; j < R; ++j) {
                 const int c = rc[j];
-                sw[j] = host_swz(1u << c);
-                op.cidx |= static_cast<uint32_t>(c) << (8 * j);
+                op.swc[j] = static_cast<uint16_t>(host_swz(1u << c));
+                op.cidx |= static_cast<uint64_t>(c) << (8 * j);
                 op.c_off[j] = 1ull << pp.lpos[c];
                 regc[j] = c;
                 cur |= 1u << c;
             }
-            op.swc01 = sw[0] | (sw[1] << 16);
-            op.swc23 = sw[2] | (sw[3] << 16);
             if (kind == kOpCfg && !P.identity) {
                 op.perm = make_perm();
                 only_point = false;
@@ -359,14 +364,14 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
         };
         // a config by its register set (ascending slots), thread order by rule
         auto emit = [&](int kind, uint32_t cfg, uint32_t prefer34 = 0, uint32_t prefer34b = 0) {
-            int rc[4] = {0, 0, 0, 0};
+            int rc[kMaxR] = {0, 0, 0, 0, 0};
             int j = 0;
-            for (uint32_t m = cfg; m && j < 4; m &= m - 1, ++j) rc[j] = std::countr_zero(m);
+            for (uint32_t m = cfg; m && j < kMaxR; m &= m - 1, ++j) rc[j] = std::countr_zero(m);
             emit_explicit(kind, rc, thread_order(all & ~cfg, prefer34, prefer34b), cfg);
         };
         // register slot j <-> lane bit b through warp shuffles
         auto emit_swap = [&](int j, int b) {
-            int rc[4] = {regc[0], regc[1], regc[2], regc[3]};
+            int rc[kMaxR] = {regc[0], regc[1], regc[2], regc[3], regc[4]};
             std::vector<int> order = thr;
             std::swap(rc[j], order[b]);
             emit_explicit(kOpSwap, rc, order, static_cast<uint32_t>(j | (b << 4)));
@@ -427,6 +432,17 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                         if ((bits & ~lanes34) == 0) {
                             for (int b = 3; b <= 4; ++b) {
                                 if (!((bits >> thr[b]) & 1u)) continue;
+                                if (lane_bfly_enabled() && !((after >> thr[b]) & 1u)) {
+                                    // no later stage of the pass needs the coordinate in a
+                                    // register: butterfly it across lanes in place
+                                    MicroOpDev y{};
+                                    y.kind = kOpLaneBfly;
+                                    y.mask = static_cast<uint32_t>(b);
+                                    y.perm = -1;
+                                    A.ops.push_back(y);
+                                    bits &= ~(1u << thr[b]);
+                                    continue;
+                                }
                                 int jbest = -1;
                                 for (int j = 0; j < R; ++j) {
                                     if ((bits >> regc[j]) & 1u) continue;
@@ -612,20 +628,12 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                     // register combinations r_s (pad, bit s)
                     std::vector<uint32_t> cbits;
                     for (int j = 0; j < R; ++j) cbits.push_back(1u << regc[j]);
-                    uint32_t tic[4] = {0, 0, 0, 0};
                     if (pd.table_point == static_cast<int>(A.points.size())) {
-                        for (size_t j = 0; j < cbits.size() && j < 4; ++j) tic[j] = pext_host(cbits[j], pt.table_mask);
-                    }
-                    po.swc01 = tic[0] | (tic[1] << 16);
-                    po.swc23 = tic[2] | (tic[3] << 16);
-                    if (pd.table_point == static_cast<int>(A.points.size())) {
-                        for (int f = 0; f < pt.n_fac; ++f) {
-                            uint64_t packed = 0;
-                            for (size_t j = 0; j < cbits.size() && j < 4; ++j) {
-                                packed |= uint64_t(host_swz(pext_host(cbits[j], pt.fac_mask[f]))) << (16 * j);
-                            }
-                            po.c_off[f] = packed;
-                        }
+                        for (size_t j = 0; j < cbits.size(); ++j)
+                            po.swc[j] = static_cast<uint16_t>(pext_host(cbits[j], pt.table_mask));
+                        for (int f = 0; f < pt.n_fac; ++f)
+                            for (size_t j = 0; j < cbits.size(); ++j)
+                                po.fo[f][j] = static_cast<uint16_t>(host_swz(pext_host(cbits[j], pt.fac_mask[f])));
                     }
                     uint32_t qr = 0;
                     if (pt.qt_word >= 0) {
@@ -638,7 +646,7 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                             if ((words[r >> 6] >> (r & 63)) & 1ull) qr |= 1u << sidx;
                         }
                     }
-                    po.pad = static_cast<int>(qr);
+                    po.pad = qr;
                     if (pp.scale_exp > 0 && !scale_placed && pt.n_terms > 0) {
                         po.mask = 1u;
                         scale_placed = true;
@@ -785,6 +793,7 @@ std::string describe_program(const HostPlanArrays& a) {
             else if (op.kind == kOpCfg) os << " CFG{" << std::hex << op.mask << std::dec << (op.perm >= 0 ? ",perm" : "") << "}";
             else if (op.kind == kOpBfly) os << " B" << std::popcount(op.mask);
             else if (op.kind == kOpSwap) os << " X" << (op.mask & 15u) << ":" << (op.mask >> 4);
+            else if (op.kind == kOpLaneBfly) os << " Y" << op.mask;
             else if (op.kind == kOpPoint) {
                 const PointDev& pt = a.points[op.arg];
                 std::string tdesc;

@@ -45,27 +45,36 @@ namespace sdb {
 // grouped by outer bit, so a shard of <= 24 outer bits always fits).
 constexpr int kMaxLitPairs = 24;
 
-enum MicroKind : int { kOpLoad = 0, kOpCfg = 1, kOpBfly = 2, kOpPoint = 3, kOpStore = 4, kOpSwap = 5 };
+// kOpLaneBfly: Hadamard butterfly on the coordinate at lane bit `mask` (3 or 4)
+// by warp shuffles, config unchanged (a lane swap plus a register butterfly
+// for a coordinate no later stage of the pass needs in a register).
+enum MicroKind : int { kOpLoad = 0, kOpCfg = 1, kOpBfly = 2, kOpPoint = 3, kOpStore = 4, kOpSwap = 5, kOpLaneBfly = 6 };
+
+// Register coordinates per thread: R <= kMaxR (2^R amplitudes per thread).
+// The interpreter kernel runs R = 4; specialised kernels may run R = 5
+// (32 amplitudes per thread, half the threads, fewer transposes per pass).
+constexpr int kMaxR = 5;
 
 struct MicroOpDev {
     int kind;
-    uint32_t mask;  // LOAD/CFG: register coordinates (R bits among k); BFLY: register slots (bits 0..3);
+    uint32_t mask;  // LOAD/CFG: register coordinates (R bits among k); BFLY: register slots (bits 0..R-1);
                     // POINT: bit 0 = apply the pass scale here (folded into the phase factor);
                     // STORE: bit 1 = apply the pass scale, bit 2 = block barrier first
                     // (in-place store through a CNOT map with no transpose since the load);
-                    // SWAP: register slot (bits 0..3) | lane bit << 4
+                    // SWAP: register slot (bits 0..3) | lane bit << 4; LANEBFLY: lane bit
     int perm;       // CFG: PermDev index applied on the write side, or -1
     int arg;        // LOAD/CFG: index of this config among the pass's configs; POINT: PointDev index
-    uint32_t swc01; // LOAD/CFG: swizzled slot offsets of register coordinates 0,1 (16 bits each);
-                    // POINT: compact angle-table index of register coordinates 0,1
-    uint32_t swc23; //           ... and 2,3
-    uint32_t cidx;  // LOAD/CFG: local coordinate index of register coordinate j in byte j
-    int pad;        // POINT: bit s = QT(r_s) for the register combination s of the current config
-    uint64_t c_off[4];  // LOAD/CFG: physical offsets of the register coordinates;
-                        // STORE with a store permutation: sigma-mapped offsets;
-                        // POINT (factor mode): c_off[f] packs the swizzled compact
-                        // slot offset of register coordinate j in bits 16j..16j+15
+    uint32_t pad;   // POINT: bit s = QT(r_s) for the register combination s of the current config
+    uint32_t pad2;
+    uint64_t cidx;  // LOAD/CFG: local coordinate index of register coordinate j in byte j
+    uint16_t swc[8];     // LOAD/CFG: swizzled slot offset of register coordinate j;
+                         // POINT: compact angle-table index of register coordinate j
+    uint16_t fo[3][8];   // POINT (factor mode): swizzled compact slot offset of register
+                         // coordinate j in factor table f
+    uint64_t c_off[6];   // LOAD/CFG: physical offsets of the register coordinates;
+                         // STORE with a store permutation: sigma-mapped offsets
 };
+static_assert(sizeof(MicroOpDev) % 16 == 0, "micro-ops are staged as int4 words");
 
 // Per-thread constant of one register config (host-computed): the local
 // index of the thread's register-0 amplitude (low 16 bits) and its swizzled

@@ -282,20 +282,26 @@ const int kTableThreshold = [] {
     return e ? std::atoi(e) : 0;  // 0: the pass's largest phase stage always gets the table
 }();
 
-// Register coordinates of specialised kernels (SDB_RBITS=3..5); the
-// interpreter kernel always runs 4.
-int jit_rbits() {
-    static const int r = [] {
+// Register coordinates of specialised kernels; the interpreter kernel always
+// runs 4. SDB_RBITS=3..5 forces a value. By default the per-term schedule
+// runs 5 (32 amplitudes per thread, 128 threads: its passes carry two
+// Hadamard levels, and the fifth register coordinate saves a transpose or a
+// lane swap per level -- config 4 72.2 -> 68.4 ms/step) and the whole-group
+// schedule 4 (config 2 1.05 vs 1.19 ms, config 3 equal, config 5 at n=28
+// 2257 vs 2309 ms with 5).
+int jit_rbits(int split = -1) {
+    static const int env = [] {
         const char* e = std::getenv("SDB_RBITS");
-        return e ? std::clamp(std::atoi(e), 3, sdb::kMaxR) : 4;
+        return e ? std::clamp(std::atoi(e), 3, sdb::kMaxR) : 0;
     }();
-    return r;
+    if (env) return env;
+    return split == 1 ? 5 : 4;
 }
 
 void upload_step(sd_plan& p, StepExec& E, const sdb::StepPlan& combined) {
     sdb::StateImpl& s = p.state->impl;
     const bool jit = sdb::jit_wanted(s.n_local);
-    const int rbits = jit ? jit_rbits() : 4;
+    const int rbits = jit ? jit_rbits(p.split >= 0 ? p.split : split_diag_mode()) : 4;
     sdb::HostPlanArrays A = sdb::lower_plan(combined, s.n_local, kTableThreshold, rbits);
     A.tma = p.knobs.tma;
     sdb::verify_lowering(A);  // register-config bookkeeping of lane swaps (host check, cheap)
@@ -1576,7 +1582,7 @@ sd_status sd_jit_compile_preview(int n, int world, const sd_group_desc* groups, 
         combined.tile_qubits = k;
         for (const sdb::Segment& sg : ss.segs)
             for (const sdb::PassPlan& pp : sg.plan.passes) combined.passes.push_back(pp);
-        const sdb::HostPlanArrays A = sdb::lower_plan(combined, n_local, kTableThreshold, jit_rbits());
+        const sdb::HostPlanArrays A = sdb::lower_plan(combined, n_local, kTableThreshold, jit_rbits(split_diag_mode()));
         const size_t np = sdb::jit_compile_only(A);
         if (n_programs) *n_programs = np;
     });

@@ -68,3 +68,38 @@ def test_jit_sharded_local_shards(sd, ref, force_jit):
     want, _ = ref.evolve_grouped(h, psi0, n, 0.05, 3, 1)
     ref.free(h)
     assert np.max(np.abs(got - want)) < 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,n,ring", [(4, 16, 0), (3, 14, 0), (5, 14, 0), (4, 16, 1), (2, 14, 1)])
+def test_jit_per_term_five_register_coordinates(cfg, n, ring, sd, ref, port, force_jit, monkeypatch):
+    """Per-term diagonal schedule (the one the autotuner keeps for config 4):
+    its specialised kernels run 32 amplitudes per thread (R = 5), optionally
+    through the ring pipeline (two warp groups, three TMA stages) -- against
+    the reference, with few CTAs so each walks many tiles."""
+    monkeypatch.setenv("SDB_SPLIT_DIAG", "1")
+    monkeypatch.setenv("SDB_MAX_HDEPTH", "2")
+    monkeypatch.setenv("SDB_MAX_CTAS", "5")
+    if ring:
+        monkeypatch.setenv("SDB_RING", "1")
+    text = M.config_text(cfg, n=n)
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
+    order, dt, steps = M.CONFIGS[cfg]["order"], M.CONFIGS[cfg]["dt"] * 5, 3
+    init = M.CONFIGS[cfg]["init"]
+    if init[0] == "plus":
+        psi0 = np.full(1 << n, 1 / np.sqrt(1 << n), np.complex128)
+    elif init[0] == "random":
+        psi0 = port.random_state(n, init[1])
+    else:
+        psi0 = np.zeros(1 << n, np.complex128)
+        psi0[M.initial_index(cfg, n)] = 1
+    s = sd.StateVector(n)
+    s.upload(psi0)
+    plan = sd.TrotterPlan(s, groups, order=order, tile_qubits=12)
+    plan.evolve(dt, steps)
+    got = s.amplitudes()
+    h, _, _ = ref.partition_text(text)
+    want, _ = ref.evolve_grouped(h, psi0, n, dt, steps, order)
+    ref.free(h)
+    assert np.max(np.abs(got - want)) < 1e-10
+    assert abs(np.linalg.norm(got) - 1) < 1e-12

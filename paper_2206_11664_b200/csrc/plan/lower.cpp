@@ -109,6 +109,11 @@ int lane_swap_mode() {
     return m;
 }
 bool lane_swaps_enabled() { return (lane_swap_mode() & 3) != 0; }
+// SDB_CX_FOLD=0: trailing CNOT stages keep their own transpose
+bool cx_fold_enabled() {
+    const char* e = std::getenv("SDB_CX_FOLD");
+    return !e || std::atoi(e) != 0;
+}
 // SDB_LANE_BFLY=0: lane swaps only (no in-place cross-lane butterflies)
 bool lane_bfly_enabled() {
     static const bool on = [] {
@@ -395,6 +400,8 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                 }
             }
         }
+        // CNOT stages already folded into an earlier transpose (below)
+        std::vector<char> cx_folded(pp.stages.size(), 0);
         for (size_t si = 0; si < pp.stages.size(); ++si) {
             const PassStage& st = pp.stages[si];
             const uint32_t after = wht_after[si + 1];
@@ -461,10 +468,31 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                         chunk = lowest_bits(bits, R);
                     }
                     const uint32_t cfg = fill(chunk, (bits | after) & ~chunk);
+                    // The pass's last transpose (it takes every remaining coordinate
+                    // of its last WHT stage): CNOT stages right behind this stage
+                    // that touch none of those coordinates commute with the
+                    // butterflies still to come, so they ride this transpose's
+                    // write side instead of costing a transpose of their own
+                    // before the store (config 4: 3 -> 2 transposes in such passes).
+                    if (cx_fold_enabled() && after == 0 && (chunk & ~bits) == 0 && (bits & ~chunk) == 0) {
+                        size_t sj = si + 1;
+                        uint32_t sup = 0;
+                        for (; sj < pp.stages.size() && pp.stages[sj].kind == PassStage::CX; ++sj)
+                            sup |= pp.stages[sj].mask | (pp.stages[sj].ctrl_local >= 0 ? 1u << pp.stages[sj].ctrl_local : 0u);
+                        if (sj > si + 1 && (sup & bits) == 0) {
+                            for (size_t c = si + 1; c < sj; ++c) {
+                                const PassStage& cs = pp.stages[c];
+                                if (cs.ctrl_local >= 0) P.compose_local(cs.ctrl_local, cs.mask);
+                                else P.compose_outer(cs.ctrl_phys, cs.mask);
+                                cx_folded[c] = 1;
+                            }
+                        }
+                    }
                     emit(kOpCfg, cfg, steer ? (bits & ~cfg) : 0u, steer ? (after & ~cfg) : 0u);
                 }
             } else if (st.kind == PassStage::CX) {
                 only_point = false;
+                if (cx_folded[si]) continue;
                 if (st.ctrl_local >= 0) P.compose_local(st.ctrl_local, st.mask);
                 else P.compose_outer(st.ctrl_phys, st.mask);
             } else {

@@ -983,7 +983,6 @@ struct PassCtx {
                 if (q & 1u) a = make_double2(-a.y, a.x);
             }
             if constexpr (MODE == 4) {
-                if (pc.tph) a = make_double2(a.x * tph.x - a.y * tph.y, a.x * tph.y + a.y * tph.x);
                 double2 e;
 #pragma unroll
                 for (int f = 0; f < NFAC; ++f) {
@@ -994,6 +993,11 @@ struct PassCtx {
                     const double2 t = E[f][x];
                     e = f == 0 ? t : make_double2(e.x * t.x - e.y * t.y, e.x * t.y + e.y * t.x);
                 }
+                // the tile's constant phase goes onto the table entry, not the
+                // amplitude: e depends only on the register coordinates the
+                // factors span, so registers that share them share the product
+                // (common-subexpression), one complex multiply per amplitude
+                if (pc.tph) e = make_double2(e.x * tph.x - e.y * tph.y, e.x * tph.y + e.y * tph.x);
                 a = make_double2(a.x * e.x - a.y * e.y, a.x * e.y + a.y * e.x);
             } else if constexpr (MODE == 5) {
                 uint32_t l = rc.tb;

@@ -103,3 +103,15 @@ def test_jit_per_term_five_register_coordinates(cfg, n, ring, sd, ref, port, for
     ref.free(h)
     assert np.max(np.abs(got - want)) < 1e-10
     assert abs(np.linalg.norm(got) - 1) < 1e-12
+
+
+@pytest.mark.parametrize("ring", ["0", "1"])
+def test_jit_per_term_sources_compile_r5(sd, monkeypatch, ring):
+    """Host-only: per-term plans lower to 5 register coordinates (32 amplitudes
+    per thread), pass the lowering's own check, and their NVRTC programs --
+    ring-pipeline variant included -- compile for sm_100a."""
+    monkeypatch.setenv("SDB_SPLIT_DIAG", "1")
+    monkeypatch.setenv("SDB_MAX_HDEPTH", "2")
+    monkeypatch.setenv("SDB_RING", ring)
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(M.config_text(4, n=16)))
+    assert sd.simdiag.jit_compile_preview(16, groups, order=1) >= 1

@@ -118,6 +118,20 @@ __device__ __forceinline__ void tma_load_5d(uint32_t dst, const void* tmap, int 
         : "memory");
 }
 
+// TMA store of one box from shared memory (bulk async-group of the issuing thread)
+__device__ __forceinline__ void tma_store_5d(const void* tmap, int c0, int c1, int c2, int c3, int c4, uint32_t src) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group"
+        " [%0, {%1, %2, %3, %4, %5}], [%6];\n" ::"l"(tmap),
+        "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(src)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+// the thread's committed bulk stores have finished reading shared memory
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+// ... and have completed
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
 __device__ __forceinline__ void tma_prefetch_5d(const void* tmap, int c0, int c1, int c2, int c3, int c4) {
     asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];\n" ::"l"(tmap),
                  "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
@@ -444,6 +458,7 @@ struct PassCtx {
     uint32_t mbar = 0;       // TMA: mbarrier of the tile staged in buf
     uint32_t mbar2 = 0;      // TMA split stage: mbarrier of the early half (0: one stage)
     const void* tmap = nullptr;  // TMA: the tensor map (address of the __grid_constant__ parameter)
+    const void* tmap_out = nullptr;  // TMA store: the same view of the output buffer
     uint32_t tma_phase = 0;  // TMA: parity of the next completion to wait for
     double2* ring = nullptr; // ring mode: the kStages tile stages
     uint32_t mbar0 = 0;      // ring mode: the 2 kStages mbarriers (see set_stage)
@@ -1065,6 +1080,30 @@ struct PassCtx {
         }
     }
 
+    // STORE through TMA (ring pipeline, plain stores): the registers go to the
+    // tile's stage in box layout (slot of local index l = tsl(l), the LOAD's
+    // map), then the group's warp 0 issues the boxes as bulk tensor stores
+    // (Prog::tma_store_issue). The stage is reused for a later tile's load
+    // only after those stores have read it (bulk wait_group.read).
+    __device__ __forceinline__ void store_tma(bool sc, uint32_t tsl0, const uint32_t (&tso)[kMaxR], double2 (&v)[NR]) {
+        if (smem_busy) gsync<NT>();  // every thread has read the last transpose
+        uint32_t a[NR];
+        a[0] = tsl0;
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+#pragma unroll
+            for (int s = 0; s < (1 << j); ++s) a[s + (1 << j)] = a[s] ^ tso[j];
+        if (sc) {
+#pragma unroll
+            for (int s = 0; s < NR; ++s) buf[a[s]] = make_double2(v[s].x * scale, v[s].y * scale);
+        } else {
+#pragma unroll
+            for (int s = 0; s < NR; ++s) buf[a[s]] = v[s];
+        }
+        fence_proxy_async();  // generic-proxy writes visible to the bulk copy
+        gsync<NT>();
+    }
+
     // STORE flags: the specialised kernels pass them as a template constant
     // (F >= 0), so only the path the op takes is compiled; the interpreter
     // decodes them from the staged op (F < 0).
@@ -1236,6 +1275,7 @@ struct PassCtx {
             sdb_off_hi, sdb_tbase, sdb_pl, sdb_ph);                                                        \
     ctx.mbar0 = ::sdb::dev::smem_u32(&sdb_mbar[0]);                                                        \
     ctx.tmap = &tmap;                                                                                      \
+    ctx.tmap_out = &tmap_out;                                                                              \
     if (threadIdx.x == 0) {                                                                                \
         for (int st = 0; st < 2 * ::sdb::dev::kStages; ++st) ::sdb::dev::mbar_init(ctx.mbar0 + 8u * st);   \
     }                                                                                                      \
@@ -1258,7 +1298,8 @@ struct PassCtx {
         ctx.begin_tile(t);                                                                                 \
         double2 v[Ctx::NR];                                                                                \
         PROG(ctx, v);                                                                                      \
-    }
+    }                                                                                                      \
+    if (ctx.tid < 32) ::sdb::dev::bulk_wait0(); /* TMA stores complete before the CTA exits */
 
 }  // namespace dev
 }  // namespace sdb

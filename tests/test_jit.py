@@ -71,17 +71,20 @@ def test_jit_sharded_local_shards(sd, ref, force_jit):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cfg,n,ring", [(4, 16, 0), (3, 14, 0), (5, 14, 0), (4, 16, 1), (2, 14, 1)])
-def test_jit_per_term_five_register_coordinates(cfg, n, ring, sd, ref, port, force_jit, monkeypatch):
+@pytest.mark.parametrize("cfg,n,mode", [(4, 16, "two_ctas"), (3, 14, "two_ctas"), (5, 14, "two_ctas"),
+                                        (4, 16, "ring"), (3, 14, "ring"), (5, 14, "ring"), (2, 14, "ring"),
+                                        (4, 16, "ring_register_stores")])
+def test_jit_per_term_five_register_coordinates(cfg, n, mode, sd, ref, port, force_jit, monkeypatch):
     """Per-term diagonal schedule (the one the autotuner keeps for config 4):
-    its specialised kernels run 32 amplitudes per thread (R = 5), optionally
-    through the ring pipeline (two warp groups, three TMA stages) -- against
-    the reference, with few CTAs so each walks many tiles."""
+    its specialised kernels run 32 amplitudes per thread (R = 5) through the
+    ring pipeline (two warp groups, three TMA stages, TMA stores; the default),
+    the ring with register stores, or two CTAs per SM -- against the
+    reference, with few CTAs so each walks many tiles."""
     monkeypatch.setenv("SDB_SPLIT_DIAG", "1")
     monkeypatch.setenv("SDB_MAX_HDEPTH", "2")
     monkeypatch.setenv("SDB_MAX_CTAS", "5")
-    if ring:
-        monkeypatch.setenv("SDB_RING", "1")
+    monkeypatch.setenv("SDB_RING", "0" if mode == "two_ctas" else "1")
+    monkeypatch.setenv("SDB_TMA_STORE", "0" if mode == "ring_register_stores" else "1")
     text = M.config_text(cfg, n=n)
     groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
     order, dt, steps = M.CONFIGS[cfg]["order"], M.CONFIGS[cfg]["dt"] * 5, 3

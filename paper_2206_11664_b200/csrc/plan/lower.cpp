@@ -115,13 +115,13 @@ bool cx_fold_enabled() {
     return !e || std::atoi(e) != 0;
 }
 // SDB_LANE_BFLY=0: lane swaps only (no in-place cross-lane butterflies)
-bool lane_bfly_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("SDB_LANE_BFLY");
-        return !e || std::atoi(e) != 0;
-    }();
-    return on;
+// SDB_LANE_BFLY=2: also for coordinates a later stage needs (it fetches them
+// with its own transpose)
+int lane_bfly_mode() {
+    const char* e = std::getenv("SDB_LANE_BFLY");  // read per plan (experiments switch it)
+    return e ? std::atoi(e) : 1;
 }
+bool lane_bfly_enabled() { return lane_bfly_mode() != 0; }
 
 // Factor cover of a table point: split the coordinates its terms touch into
 // at most three disjoint sets of <= kMaxFacBits coordinates such that no
@@ -439,7 +439,7 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                         if ((bits & ~lanes34) == 0) {
                             for (int b = 3; b <= 4; ++b) {
                                 if (!((bits >> thr[b]) & 1u)) continue;
-                                if (lane_bfly_enabled() && !((after >> thr[b]) & 1u)) {
+                                if (lane_bfly_enabled() && (lane_bfly_mode() == 2 || !((after >> thr[b]) & 1u))) {
                                     // no later stage of the pass needs the coordinate in a
                                     // register: butterfly it across lanes in place
                                     MicroOpDev y{};

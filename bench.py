@@ -38,6 +38,14 @@ CONFIG_DESC = {
 METRIC = "Trotter steps/s at n=30 complex128; achieved HBM GB/s per GPU vs peak"
 
 
+def schedule_name(info: dict) -> str:
+    """The kept schedule family and kernel pipeline (plan-time autotune)."""
+    if info["schedule"] == 1:
+        return ("per-term diagonal ops, <= 2 Hadamard levels per pass; 32 amplitudes/thread, "
+                "ring pipeline with TMA loads and stores")
+    return "whole-group diagonal ops" + ("; ring pipeline with TMA loads and stores" if info["ring"] == 1 else "")
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -464,9 +472,9 @@ def run_ours(args, rank, world, local_rank):
                    "tile_qubits": info["tile_qubits"], "passes_per_step": info["n_passes_per_step"],
                    "ref_sweeps_per_step": info["n_ref_sweeps_per_step"],
                    "floor_group_applications": info["n_group_applications"],
-                   "schedule": ("per-term diagonal ops, <= 2 Hadamard levels per pass" if info["schedule"] == 1
-                                else "whole-group diagonal ops"),
-                   "autotune_ms_per_step": ({"whole_group": info["tune_ms_whole"], "per_term": info["tune_ms_split"]}
+                   "schedule": schedule_name(info),
+                   "autotune_ms_per_step": ({"whole_group": info["tune_ms_whole"], "per_term": info["tune_ms_split"],
+                                             "whole_group_ring": info["tune_ms_whole_ring"]}
                                             if info["tune_ms_whole"] > 0 else None)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": load_traffic(), "peak_source": peak_src,
@@ -538,7 +546,7 @@ def other_configs(dev):
                 "workload": CONFIG_DESC[cfg], "n_qubits": n, "steps": steps, "ms_per_step": ms,
                 "steps_per_s": 1000.0 / ms, "passes_per_step": info["n_passes_per_step"],
                 "ref_sweeps_per_step": info["n_ref_sweeps_per_step"],
-                "schedule": "per-term diagonal ops" if info["schedule"] == 1 else "whole-group diagonal ops",
+                "schedule": schedule_name(info),
                 "step_hbm_gbs": gbs, "step_frac": gbs / peak, "norm_error": abs(psi.norm() - 1.0)}
             del plan, psi
         except Exception as ex:  # reported, never fatal

@@ -284,6 +284,8 @@ typedef struct sd_plan_info {
     int schedule;               /* 0: whole-group diagonal ops, 1: per-term diagonal ops */
     double tune_ms_whole;       /* plan-time autotune: ms per step of each schedule (0: not timed) */
     double tune_ms_split;
+    double tune_ms_whole_ring;  /* ... whole-group schedule through the ring pipeline */
+    int ring;                   /* ring pipeline: -1 default (per-term plans), 0 off, 1 on */
 } sd_plan_info;
 
 sd_status sd_plan_get_info(const sd_plan* p, sd_plan_info* out);

@@ -74,6 +74,8 @@ class PlanInfo(C.Structure):
         ("schedule", C.c_int),
         ("tune_ms_whole", dbl),
         ("tune_ms_split", dbl),
+        ("tune_ms_whole_ring", dbl),
+        ("ring", C.c_int),
     ]
 
 

@@ -70,7 +70,7 @@ struct sd_plan {
     // plan-time autotuner (sd_plan_create), which times the candidates.
     int split = -1;
     sdb::PlannerKnobs knobs;
-    double tune_ms[2] = {0.0, 0.0};  // measured ms/step of the candidates (0: not timed)
+    double tune_ms[3] = {0.0, 0.0, 0.0};  // measured ms/step: whole-group, per-term, whole-group ring (0: not timed)
 };
 
 namespace {
@@ -304,6 +304,7 @@ void upload_step(sd_plan& p, StepExec& E, const sdb::StepPlan& combined) {
     const int rbits = jit ? jit_rbits(p.split >= 0 ? p.split : split_diag_mode()) : 4;
     sdb::HostPlanArrays A = sdb::lower_plan(combined, s.n_local, kTableThreshold, rbits);
     A.tma = p.knobs.tma;
+    A.ring = p.knobs.ring;
     sdb::verify_lowering(A);  // register-config bookkeeping of lane swaps (host check, cheap)
     E.pass_class = A.pass_class;
     E.program = sdb::describe_program(A);
@@ -1253,19 +1254,35 @@ sd_status sd_plan_create(sd_state* h, const sd_group_desc* groups, size_t n_grou
             p->split = 0;
             plan_build(*p);
             const bool had_scratch = s.xbuf != nullptr;
+            // candidate C: whole-group ops through the ring pipeline (two warp
+            // groups, three TMA stages, TMA stores) -- faster for config 3
+            // (448 -> 415 ms), slower for configs 2 and 4
+            auto r = std::make_unique<sd_plan>();
+            r->state = h;
+            r->opts = p->opts;
+            r->groups = p->groups;
+            r->split = 0;
+            r->knobs.ring = 1;
             try {
                 plan_build(*q);
                 const bool fewer = q->first && p->first && q->first->ss.n_passes < p->first->ss.n_passes;
-                if (fewer && ensure_scratch(s)) {
-                    const double ta = time_steady_step(*p), tb = time_steady_step(*q);
-                    p->tune_ms[0] = q->tune_ms[0] = ta;
-                    p->tune_ms[1] = q->tune_ms[1] = tb;
-                    if (tb < ta) std::swap(p, q);
+                if (ensure_scratch(s)) {
+                    double t[3] = {time_steady_step(*p), 0.0, 0.0};
+                    if (fewer) t[1] = time_steady_step(*q);
+                    plan_build(*r);
+                    t[2] = time_steady_step(*r);
+                    int best = 0;
+                    for (int c = 1; c < 3; ++c)
+                        if (t[c] > 0.0 && t[c] < t[best]) best = c;
+                    for (int c = 0; c < 3; ++c) p->tune_ms[c] = q->tune_ms[c] = r->tune_ms[c] = t[c];
+                    if (best == 1) std::swap(p, q);
+                    if (best == 2) std::swap(p, r);
                 }
             } catch (const sdb::OomError&) {
-                // no room for the second candidate: keep the whole-group plan
+                // no room for another candidate: keep the whole-group plan
             }
             sd_plan_destroy(q.release());
+            sd_plan_destroy(r.release());
             // the scratch stays only if the kept plan's layout needs the second buffer
             if (!had_scratch && s.xbuf && p->layout.empty()) {
                 SDB_CUDA(cudaSetDevice(s.device));
@@ -1316,6 +1333,8 @@ sd_status sd_plan_get_info(const sd_plan* p, sd_plan_info* o) {
             o->schedule = p->split == 1 ? 1 : 0;
             o->tune_ms_whole = p->tune_ms[0];
             o->tune_ms_split = p->tune_ms[1];
+            o->tune_ms_whole_ring = p->tune_ms[2];
+            o->ring = p->knobs.ring;
         } else {
             o->n_passes_per_step = p->n_ref_sweeps;
             o->n_kernels_per_step = 0;

@@ -28,6 +28,7 @@ struct HostPlanArrays {
     // Specialised kernels stage tile loads through TMA (jit.cpp): -1 default
     // (on unless SDB_TMA=0), 0 off, 1 on. Set per plan by the caller.
     int tma = -1;
+    int ring = -1;  // specialised kernels run the ring pipeline: -1 default (R = 5 programs), 0 off, 1 on
 };
 
 // table_threshold: POINT stages with more terms use the per-tile WHT table.

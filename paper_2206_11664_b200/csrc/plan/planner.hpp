@@ -23,6 +23,7 @@ int fixed_bits_for(int k);
 struct PlannerKnobs {
     int max_hdepth = -1;  // WHT levels per pass, -1: SDB_MAX_HDEPTH / unlimited
     int tma = -1;         // specialised kernels stage tile loads through TMA (-1: default on / SDB_TMA)
+    int ring = -1;        // ring pipeline (-1: default for R = 5 programs / SDB_RING; 0 off, 1 on)
 };
 class KnobScope {
   public:

@@ -118,3 +118,33 @@ def test_jit_per_term_sources_compile_r5(sd, monkeypatch, ring):
     monkeypatch.setenv("SDB_RING", ring)
     groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(M.config_text(4, n=16)))
     assert sd.simdiag.jit_compile_preview(16, groups, order=1) >= 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("max_ctas", [None, "3"])
+def test_jit_ring_edge_grids_and_shards(max_ctas, sd, ref, force_jit, monkeypatch):
+    """Ring pipeline (R = 5 per-term plans) at grid extremes -- one tile per CTA
+    (the second warp group idle) and three CTAs walking every tile -- and on
+    four in-process shards, where the passes in front of a remap store into
+    the exchange buffers (register stores inside the ring)."""
+    monkeypatch.setenv("SDB_SPLIT_DIAG", "1")
+    monkeypatch.setenv("SDB_MAX_HDEPTH", "2")
+    if max_ctas:
+        monkeypatch.setenv("SDB_MAX_CTAS", max_ctas)
+    cfg, n = 4, 16
+    text = M.config_text(cfg, n=n)
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
+    psi0 = np.zeros(1 << n, np.complex128)
+    psi0[M.neel_index(n)] = 1
+    h, _, _ = ref.partition_text(text)
+    want, _ = ref.evolve_grouped(h, psi0, n, 0.05, 3, 1)
+    ref.free(h)
+    s = sd.StateVector(n)
+    s.upload(psi0)
+    sd.TrotterPlan(s, groups, order=1, tile_qubits=12).evolve(0.05, 3)
+    assert np.max(np.abs(s.amplitudes() - want)) < 1e-10
+    sh = sd.LocalShards(n, 4)
+    sh.upload(psi0)
+    sh.plan(groups, tile_qubits=12)
+    sh.evolve(0.05, 3)
+    assert np.max(np.abs(sh.amplitudes() - want)) < 1e-10

@@ -959,6 +959,17 @@ struct PassCtx {
         // mode 5: the tile's phase per sign pattern of its terms, summed in
         // term order exactly as mode 1 does per amplitude
         const double2* ptab = nullptr;
+        uint32_t pidx0 = 0, pidx[R];
+        if constexpr (MODE == 5) {
+#pragma unroll
+            for (int j = 0; j < R; ++j) pidx[j] = 0u;
+#pragma unroll
+            for (int q = 0; q < kPatTerms; ++q) {
+                pidx0 |= static_cast<uint32_t>(__popc(rc.tb & dz[q]) & 1) << q;
+#pragma unroll
+                for (int j = 0; j < R; ++j) pidx[j] |= static_cast<uint32_t>(__popc(cb[j] & dz[q]) & 1) << q;
+            }
+        }
         if constexpr (MODE == 5) {
             // barriers on both sides: earlier readers (this tile's previous mode-5
             // POINT, the previous tile's) are done before the table is rewritten
@@ -993,9 +1004,18 @@ struct PassCtx {
         for (int s2 = 0; s2 < NR; ++s2) {
             double2 a = v[s2];
             if (pc.quarter) {
+                // a * i^q: swap the parts for odd q, then flip sign bits on the
+                // integer pipe (re for q = 1, 2; im for q = 2, 3) -- no FP64 work
                 const unsigned q = (qs[s2] + 2u * ((pc.qr >> s2) & 1u)) & 3u;
-                if (q & 2u) a = make_double2(-a.x, -a.y);
+#ifdef SDB_EXPERIMENT_QT_FP64
+                if (q & 2u) a = make_double2(-a.x, -a.y);  // timing comparison: negations as FP64 ops
                 if (q & 1u) a = make_double2(-a.y, a.x);
+#else
+                if (q & 1u) a = make_double2(a.y, a.x);
+                a.x = __longlong_as_double(__double_as_longlong(a.x) ^
+                                           (static_cast<long long>((q ^ (q >> 1)) & 1u) << 63));
+                a.y = __longlong_as_double(__double_as_longlong(a.y) ^ (static_cast<long long>((q >> 1) & 1u) << 63));
+#endif
             }
             if constexpr (MODE == 4) {
                 double2 e;
@@ -1015,13 +1035,12 @@ struct PassCtx {
                 if (pc.tph) e = make_double2(e.x * tph.x - e.y * tph.y, e.x * tph.y + e.y * tph.x);
                 a = make_double2(a.x * e.x - a.y * e.y, a.x * e.y + a.y * e.x);
             } else if constexpr (MODE == 5) {
-                uint32_t l = rc.tb;
+                // the sign pattern is GF(2)-linear in the local index: the
+                // thread's base pattern XOR the patterns of its register bits
+                uint32_t idx = pidx0;
 #pragma unroll
                 for (int j = 0; j < R; ++j)
-                    if ((s2 >> j) & 1) l |= cb[j];
-                uint32_t idx = 0;
-#pragma unroll
-                for (int q = 0; q < kPatTerms; ++q) idx |= static_cast<uint32_t>(__popc(l & dz[q]) & 1) << q;
+                    if ((s2 >> j) & 1) idx ^= pidx[j];
                 const double2 e = ptab[idx];
                 a = make_double2(a.x * e.x - a.y * e.y, a.x * e.y + a.y * e.x);
             } else if constexpr (MODE != 0) {

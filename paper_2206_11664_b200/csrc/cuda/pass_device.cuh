@@ -202,6 +202,17 @@ __device__ __forceinline__ void bfly(double2 (&v)[1 << R]) {
 // coordinate lane bit B held and vice versa. 2^(R-1) double2 move per thread.
 template <int R, int J, int B>
 __device__ __forceinline__ void lane_swap(double2 (&v)[1 << R]) {
+#ifdef SDB_EXPERIMENT_FASTSWAP
+    // timing experiment only (wrong results): the select-free data movement
+#pragma unroll
+    for (int s = 0; s < (1 << R); ++s) {
+        if ((s >> J) & 1) continue;
+        const int s1 = s | (1 << J);
+        v[s1].x = __shfl_xor_sync(0xffffffffu, v[s1].x, 1 << B);
+        v[s1].y = __shfl_xor_sync(0xffffffffu, v[s1].y, 1 << B);
+    }
+    return;
+#endif
     const bool hi = (threadIdx.x >> B) & 1u;
 #pragma unroll
     for (int s = 0; s < (1 << R); ++s) {

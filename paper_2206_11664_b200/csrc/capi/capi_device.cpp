@@ -128,6 +128,11 @@ std::vector<sdb::Op> best_step_ops(const std::vector<sdb::GroupSpec>& gs, int n,
     };
     const int cap = resynth_cap(k);
     const int split_env = split_force >= 0 ? split_force : split_diag_mode();
+    // SDB_CZ_CX: -1 (default) try CZ -> CNOT conversion both ways, 0 off, 1 forced
+    const int czcx_env = [] {
+        const char* e = std::getenv("SDB_CZ_CX");
+        return e ? std::atoi(e) : -1;
+    }();
     std::vector<sdb::Op> best;
     Score best_score{0, 0.0};
     for (int split = 0; split < 2; ++split) {
@@ -137,8 +142,10 @@ std::vector<sdb::Op> best_step_ops(const std::vector<sdb::GroupSpec>& gs, int n,
         if (split_env < 0 && split && !sharded) continue;
         for (int rs = 0; rs < 2; ++rs) {
             if (rs && cap == 0) continue;
-            for (int defer = 1; defer >= 0; --defer) {
-                auto o = sdb::step_ops(gs, n, order, cx_split(k), rs ? cap : 0, split != 0);
+            for (int defer = 1; defer >= 0; --defer)
+            for (int czcx = 1; czcx >= 0; --czcx) {
+                if ((czcx_env == 0 && czcx) || (czcx_env == 1 && !czcx)) continue;
+                auto o = sdb::step_ops(gs, n, order, cx_split(k), rs ? cap : 0, split != 0, czcx != 0);
                 // Hadamards on the always-local qubits deferred out of second WHT
                 // levels (fewer transposes in phase passes: config 4 97.4 -> 95.3 ms)
                 for (sdb::Op& op : o) op.defer_deep = defer != 0;
@@ -151,6 +158,36 @@ std::vector<sdb::Op> best_step_ops(const std::vector<sdb::GroupSpec>& gs, int n,
         }
     }
     return best;
+}
+
+// best_step_ops under the plan's knobs; when the look-ahead growth of the
+// local set (planner.cpp) is not fixed by the plan or SDB_LOOKAHEAD, it is
+// kept where it schedules the step into fewer passes from the identity layout
+// (config 4 per-term: 9 -> 7; config 5 needs more passes with it). Call with
+// a KnobScope on `knobs` alive.
+std::vector<sdb::Op> choose_step_ops(const std::vector<sdb::GroupSpec>& gs, int n, int order, int k, int n_local,
+                                     int split, sdb::PlannerKnobs& knobs) {
+    if (knobs.lookahead >= 0 || std::getenv("SDB_LOOKAHEAD")) return best_step_ops(gs, n, order, k, n_local, split);
+    std::vector<int> ident(n);
+    std::iota(ident.begin(), ident.end(), 0);
+    int best_la = 0, best_passes = 0;
+    std::vector<sdb::Op> best_ops;
+    for (int la = 0; la < 2; ++la) {
+        // the look-ahead's what-if closures cost O(window^2) per growth: plans of
+        // hundreds of passes per step (config 5: 1505, 6 s -> 27 s of planning)
+        // keep list-order growth
+        if (la == 1 && best_passes > 256) break;
+        knobs.lookahead = la;
+        auto o = best_step_ops(gs, n, order, k, n_local, split);
+        const int np_ = sdb::plan_sharded_step(o, gs, n_local, k, sdb::fixed_bits_for(k), ident).n_passes;
+        if (la == 0 || np_ < best_passes) {
+            best_la = la;
+            best_passes = np_;
+            best_ops = std::move(o);
+        }
+    }
+    knobs.lookahead = best_la;
+    return best_ops;
 }
 
 using sdb::guard;
@@ -515,7 +552,7 @@ void plan_build(sd_plan& p) {
     int k = p.opts.tile_qubits > 0 ? p.opts.tile_qubits : 12;
     p.k = std::min({k, sdb::max_tile_qubits(), s.n_local});
     const sdb::KnobScope knobs(&p.knobs);
-    p.ops = best_step_ops(p.groups, s.n, order, p.k, s.n_local, p.split);
+    p.ops = choose_step_ops(p.groups, s.n, order, p.k, s.n_local, p.split, p.knobs);
     choose_layout(p);
     std::vector<int> ident(s.n);
     std::iota(ident.begin(), ident.end(), 0);
@@ -1381,7 +1418,9 @@ sd_status sd_plan_preview(int n, int world, const sd_group_desc* groups, size_t 
         std::iota(phys.begin(), phys.end(), 0);
         int k = o.tile_qubits > 0 ? o.tile_qubits : 12;
         k = std::min({k, sdb::max_tile_qubits(), n_local});
-        const auto ops = best_step_ops(gs, n, o.order, k, n_local);
+        sdb::PlannerKnobs knobs;
+        const sdb::KnobScope scope(&knobs);
+        const auto ops = choose_step_ops(gs, n, o.order, k, n_local, -1, knobs);
         // steps until the layout repeats (the executor caches one plan per layout)
         std::vector<sdb::ShardedStep> steps;
         std::vector<std::vector<int>> seen;
@@ -1595,7 +1634,9 @@ sd_status sd_jit_compile_preview(int n, int world, const sd_group_desc* groups, 
         std::iota(phys.begin(), phys.end(), 0);
         int k = o.tile_qubits > 0 ? o.tile_qubits : 12;
         k = std::min({k, sdb::max_tile_qubits(), n_local});
-        const auto ops = best_step_ops(gs, n, o.order, k, n_local);
+        sdb::PlannerKnobs knobs;
+        const sdb::KnobScope scope(&knobs);
+        const auto ops = choose_step_ops(gs, n, o.order, k, n_local, -1, knobs);
         const sdb::ShardedStep ss = sdb::plan_sharded_step(ops, gs, n_local, k, sdb::fixed_bits_for(k), phys);
         sdb::StepPlan combined;
         combined.tile_qubits = k;

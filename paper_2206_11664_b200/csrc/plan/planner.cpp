@@ -230,10 +230,38 @@ std::vector<std::pair<int, int>> resynth_cnots(const std::vector<std::pair<int, 
 // reversed; statevector.cpp:341-349 applies runs in list order).
 class GroupEmitter {
 public:
-    GroupEmitter(std::vector<Op>& out, int max_targets, int resynth_cap, bool split_diag)
-        : out_(out), max_targets_(max_targets), cap_(resynth_cap), split_(split_diag) {}
+    GroupEmitter(std::vector<Op>& out, int max_targets, int resynth_cap, bool split_diag, bool cz_to_cx)
+        : out_(out), max_targets_(max_targets), cap_(resynth_cap), split_(split_diag), cz_cx_(cz_to_cx) {}
 
-    void group(const GroupSpec& g, int gi, double dt_scale) {
+    void group(const GroupSpec& g_in, int gi, double dt_scale) {
+        // H_b CZ(a_1,b)..CZ(a_r,b) H_b = CX(a_1->b)..CX(a_r->b): a qubit b in
+        // both h_pre and h_post whose only gates between the two layers are CZs
+        // (no CNOT, no S) loses both Hadamards, and its CZs become CNOTs with b
+        // as target -- the same unitary C_j, with two Hadamard levels fewer
+        // (config 4: the Bell-pair groups' odd/even qubits). At most one end of
+        // a CZ may be converted (H_a H_b CZ H_a H_b is no CNOT), so the
+        // candidates are taken greedily in qubit order.
+        const uint64_t conv = cz_cx_ ? convertible(g_in) : 0;
+        const GroupSpec* gp = &g_in;
+        GroupSpec gc;
+        std::vector<std::pair<int, int>> conv_cx;  // (control, target)
+        if (conv) {
+            gc = g_in;
+            gc.h_pre.clear();
+            gc.h_post.clear();
+            gc.czs.clear();
+            for (int q : g_in.h_pre)
+                if (!(conv & bitq(q))) gc.h_pre.push_back(q);
+            for (int q : g_in.h_post)
+                if (!(conv & bitq(q))) gc.h_post.push_back(q);
+            for (auto [a, b] : g_in.czs) {
+                if (conv & bitq(b)) conv_cx.emplace_back(a, b);
+                else if (conv & bitq(a)) conv_cx.emplace_back(b, a);
+                else gc.czs.push_back({a, b});
+            }
+            gp = &gc;
+        }
+        const GroupSpec& g = *gp;
         if (!g.h_pre.empty()) {
             flush();
             for (int q : g.h_pre) h(q);
@@ -242,6 +270,7 @@ public:
         flush();
         const bool has_phase = !g.czs.empty() || !g.s_layer.empty();
         if (has_phase) ph(g, false);
+        for (auto [c, t] : conv_cx) cx(c, bitq(t));
         for (int q : g.h_post) h(q);
         if (split_) {
             for (size_t t = 0; t < g.z_masks.size(); ++t) {
@@ -263,6 +292,7 @@ public:
             out_.push_back(std::move(o));
         }
         for (int q : g.h_post) h(q);
+        for (auto [c, t] : conv_cx) cx(c, bitq(t));
         if (has_phase) ph(g, true);
         pending_.assign(g.cnots.rbegin(), g.cnots.rend());
         if (!g.h_pre.empty()) {
@@ -294,6 +324,23 @@ public:
     }
 
 private:
+    static uint64_t convertible(const GroupSpec& g) {
+        uint64_t pre = 0, post = 0, blocked = 0;
+        for (int q : g.h_pre) pre |= bitq(q);
+        for (int q : g.h_post) post |= bitq(q);
+        for (int q : g.s_layer) blocked |= bitq(q);
+        for (auto [c, t] : g.cnots) blocked |= bitq(c) | bitq(t);
+        uint64_t cand = pre & post & ~blocked, conv = 0;
+        for (uint64_t m = cand; m; m &= m - 1) {
+            const int b = std::countr_zero(m);
+            bool ok = true;
+            for (auto [x, y] : g.czs) {
+                if ((x == b && (conv & bitq(y))) || (y == b && (conv & bitq(x))) || (x == b && y == b)) ok = false;
+            }
+            if (ok) conv |= bitq(b);
+        }
+        return conv;
+    }
     void h(int q) {
         Op o;
         o.kind = Op::H;
@@ -341,7 +388,7 @@ private:
 
     std::vector<Op>& out_;
     int max_targets_, cap_;
-    bool split_;
+    bool split_, cz_cx_;
     std::vector<std::pair<int, int>> pending_;
 };
 
@@ -358,10 +405,10 @@ uint64_t to_phys(uint64_t logical, const std::vector<int>& phys_of) {
 }  // namespace
 
 std::vector<Op> step_ops(const std::vector<GroupSpec>& groups, int /*n_qubits*/, int order, int max_targets,
-                         int resynth_cap, bool split_diag) {
+                         int resynth_cap, bool split_diag, bool cz_to_cx) {
     std::vector<Op> ops;
     const int G = static_cast<int>(groups.size());
-    GroupEmitter em(ops, max_targets, resynth_cap, split_diag);
+    GroupEmitter em(ops, max_targets, resynth_cap, split_diag, cz_to_cx);
     if (order == 1 || G <= 1) {
         for (int g = 0; g < G; ++g) em.group(groups[g], g, 1.0);
     } else if (order == 2) {
@@ -444,6 +491,14 @@ int dram_pattern_heuristic() {
     return e ? std::atoi(e) : 1;
 }
 
+// SDB_LOOKAHEAD: grow a pass's local set by the op whose closure schedules
+// the most gates (1) instead of the first ready op in list order (0)
+bool lookahead_growth() {
+    if (g_knobs && g_knobs->lookahead >= 0) return g_knobs->lookahead != 0;
+    const char* e = std::getenv("SDB_LOOKAHEAD");
+    return e && std::atoi(e) != 0;
+}
+
 bool consolidate_enabled() {
     const char* e = std::getenv("SDB_CONSOLIDATE");
     return !e || std::atoi(e) != 0;
@@ -465,6 +520,14 @@ std::vector<int> stage_order(const std::vector<Op>& ops, std::vector<int> sched)
     if (!any_diag) return sched;
     std::vector<char> taken(m, 0);
     std::vector<int> out;
+    // SDB_CX_BATCH (default 1): every ready CNOT joins one CX run before the
+    // next Hadamards (CNOT maps compose, and a WHT stage behind a pending map
+    // costs a transpose: config 4's CZ -> CNOT passes went from c B c B c B ...
+    // to one c); 0: one CNOT, then look for Hadamards again
+    static const bool batch_cx = [] {
+        const char* e = std::getenv("SDB_CX_BATCH");
+        return !e || std::atoi(e) != 0;
+    }();
     auto ready = [&](size_t j) {
         if (taken[j]) return false;
         for (int i : preds[j])
@@ -483,7 +546,7 @@ std::vector<int> stage_order(const std::vector<Op>& ops, std::vector<int> sched)
                     taken[j] = 1;
                     out.push_back(sched[j]);
                     again = progress = true;
-                    if (cls == 1) break;  // one CNOT, then look for Hadamards again
+                    if (cls == 1 && !batch_cx) break;  // one CNOT, then look for Hadamards again
                 }
                 if (cls == 1 && progress) break;
             }
@@ -623,6 +686,8 @@ StepPlan plan_step(const std::vector<Op>& ops, const std::vector<GroupSpec>& gro
     constexpr size_t kGoodLookahead = 64;
     const int max_depth = max_hadamard_depth();
     const bool defer_fixed = defer_fixed_hadamards();
+    const bool gain_mode = lookahead_growth();
+    constexpr size_t kGainCandidates = 48;
     while (first < N) {
         uint64_t L = fixed_logical;
         std::vector<int> sched;
@@ -659,6 +724,59 @@ StepPlan plan_step(const std::vector<Op>& ops, const std::vector<GroupSpec>& gro
                     pick = static_cast<long>(j);
                     break;
                 }
+            }
+            if (pick < 0 && gain_mode) {
+                // Look-ahead growth: each distinct set of new qubits a ready op
+                // would add is tried on a copy of the scheduler state, and the
+                // one whose closure schedules the most gates per added qubit
+                // wins (keeps the local set spatially coherent on chains, where
+                // first-in-list growth takes every other qubit of a Bell-pair
+                // group); ties keep list order.
+                std::vector<uint64_t> tried;
+                double best_gain = -1.0;
+                for (size_t j = first; j < hi; ++j) {
+                    if (done[j] || blockers[j] != 0 || std::popcount(L | ops[j].need) > k || !depth_ok(ops[j])) continue;
+                    const uint64_t add = ops[j].need & ~L;
+                    if (std::find(tried.begin(), tried.end(), add) != tried.end()) continue;
+                    tried.push_back(add);
+                    if (tried.size() > kGainCandidates) break;
+                    const uint64_t L2 = L | add;
+                    std::vector<char> d2(done.begin() + first, done.begin() + hi);
+                    std::vector<int> b2(blockers.begin() + first, blockers.begin() + hi);
+                    std::vector<int> hq2 = hq, dq2 = dq;
+                    int gates = 0;
+                    for (bool any = true; any;) {
+                        any = false;
+                        for (size_t i = first; i < hi; ++i) {
+                            const size_t r = i - first;
+                            if (d2[r] || b2[r] != 0 || (ops[i].need & ~L2)) continue;
+                            const Op& o = ops[i];
+                            int d = 0;
+                            for (uint64_t m = o.support; m; m &= m - 1) {
+                                const int q = std::countr_zero(m);
+                                d = std::max(d, is_diag(o) ? hq2[q] : std::max(hq2[q], dq2[q]));
+                            }
+                            d += o.kind == Op::H ? 1 : 0;
+                            if (max_depth > 0 && d > max_depth) continue;
+                            for (uint64_t m = o.support; m; m &= m - 1) {
+                                const int q = std::countr_zero(m);
+                                if (is_diag(o)) dq2[q] = std::max(dq2[q], d);
+                                else hq2[q] = std::max(hq2[q], d);
+                            }
+                            d2[r] = 1;
+                            if (!is_diag(o)) ++gates;
+                            for (size_t j2 = i + 1; j2 < hi; ++j2)
+                                if (!d2[j2 - first] && !commute(o, ops[j2])) --b2[j2 - first];
+                            any = true;
+                        }
+                    }
+                    const double gain = double(gates) / double(std::max(1, std::popcount(add)));
+                    if (gain > best_gain) {
+                        best_gain = gain;
+                        pick = static_cast<long>(j);
+                    }
+                }
+                if (pick >= 0) L |= ops[pick].need;
             }
             if (pick < 0) {
                 // HBM pattern: a tile with a local bit at physical 3 or 5 spreads

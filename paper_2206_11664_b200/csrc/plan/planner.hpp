@@ -24,6 +24,7 @@ struct PlannerKnobs {
     int max_hdepth = -1;  // WHT levels per pass, -1: SDB_MAX_HDEPTH / unlimited
     int tma = -1;         // specialised kernels stage tile loads through TMA (-1: default on / SDB_TMA)
     int ring = -1;        // ring pipeline (-1: default for R = 5 programs / SDB_RING; 0 off, 1 on)
+    int lookahead = -1;   // look-ahead growth of a pass's local set (-1: SDB_LOOKAHEAD, default off)
 };
 class KnobScope {
   public:
@@ -67,8 +68,10 @@ struct Op {
 // split_diag: every diagonal term (Pauli-Z string, S, CZ) becomes its own op
 // with its own support, so Hadamards of later layers can run ahead in the
 // same pass wherever a qubit's terms are done (temporal blocking).
+// cz_to_cx: a qubit whose h_pre and h_post Hadamards enclose only CZs drops
+// both, its CZs becoming CNOTs onto it (H_b CZ(a,b) H_b = CX(a->b)).
 std::vector<Op> step_ops(const std::vector<GroupSpec>& groups, int n_qubits, int order, int max_targets,
-                         int resynth_cap = 0, bool split_diag = false);
+                         int resynth_cap = 0, bool split_diag = false, bool cz_to_cx = false);
 
 // A pass in physical bit positions.
 struct PassStage {

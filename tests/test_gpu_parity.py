@@ -145,6 +145,35 @@ def test_planner_modes_on_device(cfg, n, k, jit, env, sd, ref, port, monkeypatch
     assert abs(np.linalg.norm(got) - 1) < TOL_NORM
 
 
+@pytest.mark.parametrize("split", ["0", "1"])
+@pytest.mark.parametrize("czcx", ["0", "1"])
+@pytest.mark.parametrize("cfg,n,k", [(4, 16, 12), (1, 14, 12), (3, 13, 10)])
+def test_cz_to_cnot_conversion_on_device(cfg, n, k, czcx, split, sd, ref, port, monkeypatch):
+    """Groups whose h_pre qubits see only CZs before h_post (config 4's
+    Bell-pair groups, config 1) with the Hadamard pairs dropped and the CZs
+    run as CNOTs onto those qubits (SDB_CZ_CX=1) and without (0), through the
+    NVRTC-specialised kernels, both diagonal-op families."""
+    monkeypatch.setenv("SDB_JIT", "1")
+    monkeypatch.setenv("SDB_CZ_CX", czcx)
+    monkeypatch.setenv("SDB_SPLIT_DIAG", split)
+    if split == "1":
+        monkeypatch.setenv("SDB_MAX_HDEPTH", "2")
+    text = M.config_text(cfg, n=n)
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
+    order, dt = M.CONFIGS[cfg]["order"], M.CONFIGS[cfg]["dt"] * 5
+    psi0 = rand_state(n, 5)
+    s = sd.StateVector(n)
+    s.upload(psi0)
+    plan = sd.TrotterPlan(s, groups, order=order, tile_qubits=k)
+    plan.evolve(dt, 3)
+    got = s.amplitudes()
+    h, _, _ = ref.partition_text(text)
+    want, _ = ref.evolve_grouped(h, psi0, n, dt, 3, order)
+    ref.free(h)
+    assert np.max(np.abs(got - want)) < TOL_AMP
+    assert abs(np.linalg.norm(got) - 1) < TOL_NORM
+
+
 @pytest.mark.parametrize("jit", ["0", "1"])
 @pytest.mark.parametrize("cfg,n", [(3, 16), (5, 16), (4, 17)])
 def test_many_tiles_per_cta(cfg, n, jit, sd, ref, port, monkeypatch):

@@ -41,7 +41,10 @@ METRIC = "Trotter steps/s at n=30 complex128; achieved HBM GB/s per GPU vs peak"
 def schedule_name(info: dict) -> str:
     """The kept schedule family and kernel pipeline (plan-time autotune)."""
     if info["schedule"] == 1:
-        return ("per-term diagonal ops, <= 2 Hadamard levels per pass; 32 amplitudes/thread, "
+        depth = ("no cap on Hadamard levels per pass" if info.get("max_hdepth") == 0 else
+                 f"<= {info['max_hdepth']} Hadamard levels per pass" if info.get("max_hdepth", -1) > 0 else
+                 "default Hadamard levels per pass")
+        return (f"per-term diagonal ops, {depth}; 32 amplitudes/thread, "
                 "ring pipeline with TMA loads and stores")
     return "whole-group diagonal ops" + ("; ring pipeline with TMA loads and stores" if info["ring"] == 1 else "")
 
@@ -474,7 +477,8 @@ def run_ours(args, rank, world, local_rank):
                    "floor_group_applications": info["n_group_applications"],
                    "schedule": schedule_name(info),
                    "autotune_ms_per_step": ({"whole_group": info["tune_ms_whole"], "per_term": info["tune_ms_split"],
-                                             "whole_group_ring": info["tune_ms_whole_ring"]}
+                                             "whole_group_ring": info["tune_ms_whole_ring"],
+                                             "per_term_deep": info["tune_ms_split_deep"]}
                                             if info["tune_ms_whole"] > 0 else None)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": load_traffic(), "peak_source": peak_src,

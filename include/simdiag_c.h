@@ -286,6 +286,8 @@ typedef struct sd_plan_info {
     double tune_ms_split;
     double tune_ms_whole_ring;  /* ... whole-group schedule through the ring pipeline */
     int ring;                   /* ring pipeline: -1 default (per-term plans), 0 off, 1 on */
+    double tune_ms_split_deep;  /* ... per-term schedule with <= 3 Hadamard levels per pass */
+    int max_hdepth;             /* Hadamard levels per pass of the kept plan (0: no cap, -1: default) */
 } sd_plan_info;
 
 sd_status sd_plan_get_info(const sd_plan* p, sd_plan_info* out);

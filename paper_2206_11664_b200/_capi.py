@@ -76,6 +76,8 @@ class PlanInfo(C.Structure):
         ("tune_ms_split", dbl),
         ("tune_ms_whole_ring", dbl),
         ("ring", C.c_int),
+        ("tune_ms_split_deep", dbl),
+        ("max_hdepth", C.c_int),
     ]
 
 

@@ -70,7 +70,9 @@ struct sd_plan {
     // plan-time autotuner (sd_plan_create), which times the candidates.
     int split = -1;
     sdb::PlannerKnobs knobs;
-    double tune_ms[3] = {0.0, 0.0, 0.0};  // measured ms/step: whole-group, per-term, whole-group ring (0: not timed)
+    // measured ms/step: whole-group, per-term (<= 2 Hadamard levels per pass),
+    // whole-group ring, per-term with unlimited levels (0: not timed)
+    double tune_ms[4] = {0.0, 0.0, 0.0, 0.0};
 };
 
 namespace {
@@ -575,6 +577,12 @@ bool autotune_wanted(const sd_plan& p) {
     if (const char* e = std::getenv("SDB_AUTOTUNE"); e && std::atoi(e) == 0) return false;
     if (std::getenv("SDB_SPLIT_DIAG") || std::getenv("SDB_MAX_HDEPTH")) return false;
     return s.world == 1 && s.n_local >= 22 && p.opts.fuse && p.opts.use_graph <= 0 && p.opts.order >= 1;
+}
+
+// SDB_AUTOTUNE_DEEP=0 drops candidate D (per-term, <= 3 Hadamard levels per pass)
+bool deep_candidate_wanted() {
+    const char* e = std::getenv("SDB_AUTOTUNE_DEEP");
+    return !e || std::atoi(e) != 0;
 }
 
 bool ensure_scratch(sdb::StateImpl& s) {
@@ -1300,26 +1308,43 @@ sd_status sd_plan_create(sd_state* h, const sd_group_desc* groups, size_t n_grou
             r->groups = p->groups;
             r->split = 0;
             r->knobs.ring = 1;
+            // candidate D: per-term diagonal ops with <= 3 Hadamard levels per pass
+            // (config 4: same 7 passes as B, 46.3 vs 47.7 ms; with no cap the
+            // step needs 4 passes, but their second and third POINT stages
+            // evaluate terms per amplitude: 160 ms), timed when B is and D needs
+            // no more passes than B
+            auto d = std::make_unique<sd_plan>();
+            d->state = h;
+            d->opts = p->opts;
+            d->groups = p->groups;
+            d->split = 1;
+            d->knobs.max_hdepth = 3;
             try {
                 plan_build(*q);
                 const bool fewer = q->first && p->first && q->first->ss.n_passes < p->first->ss.n_passes;
                 if (ensure_scratch(s)) {
-                    double t[3] = {time_steady_step(*p), 0.0, 0.0};
+                    double t[4] = {time_steady_step(*p), 0.0, 0.0, 0.0};
                     if (fewer) t[1] = time_steady_step(*q);
                     plan_build(*r);
                     t[2] = time_steady_step(*r);
+                    if (fewer && deep_candidate_wanted()) {
+                        plan_build(*d);
+                        if (d->first && d->first->ss.n_passes <= q->first->ss.n_passes) t[3] = time_steady_step(*d);
+                    }
                     int best = 0;
-                    for (int c = 1; c < 3; ++c)
+                    for (int c = 1; c < 4; ++c)
                         if (t[c] > 0.0 && t[c] < t[best]) best = c;
-                    for (int c = 0; c < 3; ++c) p->tune_ms[c] = q->tune_ms[c] = r->tune_ms[c] = t[c];
+                    for (int c = 0; c < 4; ++c) p->tune_ms[c] = q->tune_ms[c] = r->tune_ms[c] = d->tune_ms[c] = t[c];
                     if (best == 1) std::swap(p, q);
                     if (best == 2) std::swap(p, r);
+                    if (best == 3) std::swap(p, d);
                 }
             } catch (const sdb::OomError&) {
                 // no room for another candidate: keep the whole-group plan
             }
             sd_plan_destroy(q.release());
             sd_plan_destroy(r.release());
+            sd_plan_destroy(d.release());
             // the scratch stays only if the kept plan's layout needs the second buffer
             if (!had_scratch && s.xbuf && p->layout.empty()) {
                 SDB_CUDA(cudaSetDevice(s.device));
@@ -1371,7 +1396,9 @@ sd_status sd_plan_get_info(const sd_plan* p, sd_plan_info* o) {
             o->tune_ms_whole = p->tune_ms[0];
             o->tune_ms_split = p->tune_ms[1];
             o->tune_ms_whole_ring = p->tune_ms[2];
+            o->tune_ms_split_deep = p->tune_ms[3];
             o->ring = p->knobs.ring;
+            o->max_hdepth = p->knobs.max_hdepth;
         } else {
             o->n_passes_per_step = p->n_ref_sweeps;
             o->n_kernels_per_step = 0;

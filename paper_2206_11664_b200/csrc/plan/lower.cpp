@@ -109,6 +109,19 @@ int lane_swap_mode() {
     return m;
 }
 bool lane_swaps_enabled() { return (lane_swap_mode() & 3) != 0; }
+// POINT mode 5's sign-pattern table size (pass_device.cuh kPatTerms)
+constexpr int kPatTermsHost = 6;
+
+// SDB_SPLIT_POINTS: most pattern-table points a non-table POINT may be cut
+// into (default 4, i.e. <= 24 terms; 1 or 0: never cut)
+int point_split_max() {
+    static const int v = [] {
+        const char* e = std::getenv("SDB_SPLIT_POINTS");
+        return e ? std::atoi(e) : 4;
+    }();
+    return v;
+}
+
 // SDB_CX_FOLD=0: trailing CNOT stages keep their own transpose
 bool cx_fold_enabled() {
     const char* e = std::getenv("SDB_CX_FOLD");
@@ -646,7 +659,29 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                         A.term_coeffs.push_back(t.coeff * t.dt_scale);
                     }
                 }
-                {
+                // A point other than the pass's table point with more terms than
+                // one sign-pattern table holds (kPatTermsHost) would sum its terms
+                // and take a sincos per amplitude (modes 1/2); it is cut into
+                // consecutive points of <= kPatTermsHost terms instead, each a
+                // per-tile pattern table (mode 5) and one complex multiply per
+                // amplitude. The first carries the S/CZ quarter turns; the phases
+                // multiply, so only the summation order changes.
+                int n_chunks = 1;
+                if (pd.table_point != static_cast<int>(A.points.size()) && pt.n_terms > kPatTermsHost) {
+                    const int c = (pt.n_terms + kPatTermsHost - 1) / kPatTermsHost;
+                    if (c <= point_split_max()) n_chunks = c;
+                }
+                const int all_terms = pt.n_terms;
+                if (n_chunks > 1) pt.n_terms = kPatTermsHost;
+                for (int chunk = 0; chunk < n_chunks; ++chunk) {
+                    if (chunk > 0) {
+                        pt.term_off += kPatTermsHost;
+                        pt.n_terms = std::min(kPatTermsHost, all_terms - chunk * kPatTermsHost);
+                        pt.s1L = pt.s2L = 0;
+                        pt.s1H = pt.s2H = 0;
+                        pt.n_lo = pt.n_oo = 0;
+                        pt.qt_word = -1;
+                    }
                     MicroOpDev po{};
                     po.kind = kOpPoint;
                     po.perm = -1;
@@ -681,8 +716,8 @@ HostPlanArrays lower_plan(const StepPlan& sp, int n_local, int table_threshold, 
                         if (pd.table_point == static_cast<int>(A.points.size()) && pt.n_fac > 0) pd.table_scale = pd.scale;
                     }
                     A.ops.push_back(po);
+                    A.points.push_back(pt);
                 }
-                A.points.push_back(pt);
             }
         }
         if (!loaded) {

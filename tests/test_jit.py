@@ -148,3 +148,39 @@ def test_jit_ring_edge_grids_and_shards(max_ctas, sd, ref, force_jit, monkeypatc
     sh.plan(groups, tile_qubits=12)
     sh.evolve(0.05, 3)
     assert np.max(np.abs(sh.amplitudes() - want)) < 1e-10
+
+
+def test_jit_deep_per_term_split_points_compile(sd, monkeypatch):
+    """Host-only: per-term plans with no cap on Hadamard levels (config 4 at
+    n=30: 4 passes) carry POINT stages of up to 12 terms besides the table
+    point; those are cut into <= 6-term sign-pattern points (lower.cpp), and
+    the programs compile for sm_100a."""
+    monkeypatch.setenv("SDB_SPLIT_DIAG", "1")
+    monkeypatch.setenv("SDB_MAX_HDEPTH", "0")
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(M.config_text(4, n=30)))
+    assert sd.simdiag.jit_compile_preview(30, groups, order=1) == 4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("split_points", ["1", "4"])
+@pytest.mark.parametrize("cfg,n", [(4, 22), (3, 22)])
+def test_jit_deep_per_term_matches_reference(cfg, n, split_points, sd, ref, port, force_jit, monkeypatch):
+    """Per-term plans with no cap on Hadamard levels per pass, with the
+    non-table POINT stages summed per amplitude (SDB_SPLIT_POINTS=1) or cut
+    into sign-pattern points (4, the default), through the specialised kernels."""
+    monkeypatch.setenv("SDB_SPLIT_DIAG", "1")
+    monkeypatch.setenv("SDB_MAX_HDEPTH", "0")
+    monkeypatch.setenv("SDB_SPLIT_POINTS", split_points)
+    text = M.config_text(cfg, n=n)
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
+    order, dt = M.CONFIGS[cfg]["order"], M.CONFIGS[cfg]["dt"] * 5
+    psi0 = port.random_state(n, 11)
+    s = sd.StateVector(n)
+    s.upload(psi0)
+    sd.TrotterPlan(s, groups, order=order).evolve(dt, 2)
+    h, _, _ = ref.partition_text(text)
+    want, _ = ref.evolve_grouped(h, psi0, n, dt, 2, order)
+    ref.free(h)
+    got = s.amplitudes()
+    assert np.max(np.abs(got - want)) < 1e-10
+    assert abs(np.linalg.norm(got) - 1) < 1e-12

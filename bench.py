@@ -38,15 +38,26 @@ CONFIG_DESC = {
 METRIC = "Trotter steps/s at n=30 complex128; achieved HBM GB/s per GPU vs peak"
 
 
+def passes_per_step(info: dict) -> float:
+    """Full-state passes per Trotter step in the steady state: a plan with a
+    macro step runs macro_passes per macro_steps Trotter steps."""
+    if info.get("macro_steps", 0) > 0:
+        return info["macro_passes"] / info["macro_steps"]
+    return info["n_passes_per_step"]
+
+
 def schedule_name(info: dict) -> str:
     """The kept schedule family and kernel pipeline (plan-time autotune)."""
     if info["schedule"] == 1:
         depth = ("no cap on Hadamard levels per pass" if info.get("max_hdepth") == 0 else
                  f"<= {info['max_hdepth']} Hadamard levels per pass" if info.get("max_hdepth", -1) > 0 else
                  "default Hadamard levels per pass")
+        macro = (f"; {info['macro_steps']} Trotter steps planned as one macro step"
+                 if info.get("macro_steps", 0) > 0 else "")
         return (f"per-term diagonal ops, {depth}; 32 amplitudes/thread, "
-                "ring pipeline with TMA loads and stores")
-    return "whole-group diagonal ops" + ("; ring pipeline with TMA loads and stores" if info["ring"] == 1 else "")
+                "ring pipeline with TMA loads and stores" + macro)
+    return ("whole-group diagonal ops" + ("; ring pipeline with TMA loads and stores" if info["ring"] == 1 else "")
+            + (f"; {info['macro_steps']} Trotter steps planned as one macro step" if info.get("macro_steps", 0) > 0 else ""))
 
 
 def load_peaks():
@@ -472,13 +483,15 @@ def run_ours(args, rank, world, local_rank):
                    if world > 1 else "single GPU",
                    "exchanges_per_step": info["n_exchanges_per_step"],
                    "l2": "state (16 GiB at n=30) >> 126 MB L2; no flush needed",
-                   "tile_qubits": info["tile_qubits"], "passes_per_step": info["n_passes_per_step"],
+                   "tile_qubits": info["tile_qubits"], "passes_per_step": passes_per_step(info),
+                   "macro_steps": info["macro_steps"],
                    "ref_sweeps_per_step": info["n_ref_sweeps_per_step"],
                    "floor_group_applications": info["n_group_applications"],
                    "schedule": schedule_name(info),
                    "autotune_ms_per_step": ({"whole_group": info["tune_ms_whole"], "per_term": info["tune_ms_split"],
                                              "whole_group_ring": info["tune_ms_whole_ring"],
-                                             "per_term_deep": info["tune_ms_split_deep"]}
+                                             "per_term_deep": info["tune_ms_split_deep"],
+                                             "macro_step": info["tune_ms_macro"]}
                                             if info["tune_ms_whole"] > 0 else None)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": load_traffic(), "peak_source": peak_src,
@@ -548,7 +561,7 @@ def other_configs(dev):
             gbs = info["bytes_per_step"] / (ms / 1e3) / 1e9
             out[f"config{cfg}"] = {
                 "workload": CONFIG_DESC[cfg], "n_qubits": n, "steps": steps, "ms_per_step": ms,
-                "steps_per_s": 1000.0 / ms, "passes_per_step": info["n_passes_per_step"],
+                "steps_per_s": 1000.0 / ms, "passes_per_step": passes_per_step(info),
                 "ref_sweeps_per_step": info["n_ref_sweeps_per_step"],
                 "schedule": schedule_name(info),
                 "step_hbm_gbs": gbs, "step_frac": gbs / peak, "norm_error": abs(psi.norm() - 1.0)}

@@ -78,6 +78,9 @@ class PlanInfo(C.Structure):
         ("ring", C.c_int),
         ("tune_ms_split_deep", dbl),
         ("max_hdepth", C.c_int),
+        ("macro_steps", C.c_int),
+        ("macro_passes", C.c_int),
+        ("tune_ms_macro", dbl),
     ]
 
 

@@ -73,6 +73,13 @@ struct sd_plan {
     // measured ms/step: whole-group, per-term (<= 2 Hadamard levels per pass),
     // whole-group ring, per-term with unlimited levels (0: not timed)
     double tune_ms[4] = {0.0, 0.0, 0.0, 0.0};
+    // Temporal blocking across Trotter steps (order 1): a plan of macro_reps
+    // steps (the group list repeated) whose passes let the tail of one step
+    // share passes with the head of the next; evolve() runs whole macro steps
+    // through it and the remainder through this plan. Kept only when it
+    // measures faster per Trotter step (sd_plan_create).
+    sd_plan* macro = nullptr;
+    int macro_reps = 0;
 };
 
 namespace {
@@ -579,6 +586,13 @@ bool autotune_wanted(const sd_plan& p) {
     return s.world == 1 && s.n_local >= 22 && p.opts.fuse && p.opts.use_graph <= 0 && p.opts.order >= 1;
 }
 
+// SDB_MACRO: Trotter steps per macro step tried at plan time (default 2;
+// 0 or 1: none)
+int macro_reps_wanted() {
+    const char* e = std::getenv("SDB_MACRO");
+    return e ? std::atoi(e) : 2;
+}
+
 // SDB_AUTOTUNE_DEEP=0 drops candidate D (per-term, <= 3 Hadamard levels per pass)
 bool deep_candidate_wanted() {
     const char* e = std::getenv("SDB_AUTOTUNE_DEEP");
@@ -830,6 +844,12 @@ void evolve(sd_plan& p, double dt, int n_steps, bool wait) {
     // A relabelled plan layout is entered inside the call's first step and left
     // inside its last one: the state is in logical order between calls.
     const bool relayout = !p.layout.empty() && s.world == 1 && p.opts.fuse && !graphs;
+    if (p.macro && n_steps >= p.macro_reps) {
+        // each call leaves the state in logical order, so the two plans compose
+        const int m = n_steps / p.macro_reps;
+        evolve(*p.macro, dt, m, false);
+        n_steps -= m * p.macro_reps;
+    }
     std::vector<int> ident(s.n);
     std::iota(ident.begin(), ident.end(), 0);
     for (int step = 0; step < n_steps; ++step) {
@@ -1345,8 +1365,40 @@ sd_status sd_plan_create(sd_state* h, const sd_group_desc* groups, size_t n_grou
             sd_plan_destroy(q.release());
             sd_plan_destroy(r.release());
             sd_plan_destroy(d.release());
-            // the scratch stays only if the kept plan's layout needs the second buffer
-            if (!had_scratch && s.xbuf && p->layout.empty()) {
+            // Macro step (order 1 only: repeating an S2 group list is not two S2
+            // steps): the kept schedule family planned over macro_reps steps at
+            // once, kept when it needs fewer passes per Trotter step and times
+            // faster per step (config 4: 7 -> 6 passes per step at 2 steps)
+            const int reps = macro_reps_wanted();
+            if (p->opts.order == 1 && reps >= 2 && p->first) {
+                sd_plan* m = new sd_plan;
+                m->state = h;
+                m->opts = p->opts;
+                for (int rr = 0; rr < reps; ++rr) m->groups.insert(m->groups.end(), p->groups.begin(), p->groups.end());
+                m->split = p->split;
+                m->knobs = p->knobs;
+                m->knobs.lookahead = -1;
+                bool keep = false;
+                try {
+                    plan_build(*m);
+                    if (m->first && m->first->ss.n_passes < reps * p->first->ss.n_passes && ensure_scratch(s)) {
+                        const double tm = time_steady_step(*m) / reps;
+                        const double tp = time_steady_step(*p);
+                        m->tune_ms[0] = tm;
+                        keep = (tm > 0.0 && tm < 0.98 * tp) || std::getenv("SDB_MACRO_FORCE");
+                    }
+                } catch (const sdb::OomError&) {
+                    keep = false;
+                }
+                if (keep) {
+                    p->macro = m;
+                    p->macro_reps = reps;
+                } else {
+                    sd_plan_destroy(m);
+                }
+            }
+            // the scratch stays only if a kept plan's layout needs the second buffer
+            if (!had_scratch && s.xbuf && p->layout.empty() && (!p->macro || p->macro->layout.empty())) {
                 SDB_CUDA(cudaSetDevice(s.device));
                 SDB_CUDA(cudaFree(s.xbuf));
                 s.xbuf = nullptr;
@@ -1361,6 +1413,7 @@ sd_status sd_plan_create(sd_state* h, const sd_group_desc* groups, size_t n_grou
 
 void sd_plan_destroy(sd_plan* p) {
     if (!p) return;
+    sd_plan_destroy(p->macro);
     cudaSetDevice(p->state->impl.device);
     for (auto& e : p->ev_pool) {
         cudaEventDestroy(e.first);
@@ -1397,6 +1450,13 @@ sd_status sd_plan_get_info(const sd_plan* p, sd_plan_info* o) {
             o->tune_ms_split = p->tune_ms[1];
             o->tune_ms_whole_ring = p->tune_ms[2];
             o->tune_ms_split_deep = p->tune_ms[3];
+            if (p->macro && p->macro->first) {
+                o->macro_steps = p->macro_reps;
+                o->macro_passes = p->macro->first->ss.n_passes;
+                o->tune_ms_macro = p->macro->tune_ms[0];
+                // steady state runs whole macro steps: bytes per Trotter step
+                o->bytes_per_step = 2.0 * 16.0 * double(s.amps_count()) * o->macro_passes / p->macro_reps;
+            }
             o->ring = p->knobs.ring;
             o->max_hdepth = p->knobs.max_hdepth;
         } else {
@@ -1499,12 +1559,14 @@ sd_status sd_evolve_async(sd_plan* p, double dt, int n_steps) {
 sd_status sd_plan_set_profiling(sd_plan* p, int enable) {
     return guard([&] {
         require(p != nullptr, "null plan");
-        harvest(*p);
-        p->profiling = enable != 0;
-        for (int c = 0; c < 4; ++c) {
-            p->ms[c] = 0.0;
-            p->launches[c] = 0;
-            p->bytes[c] = 0.0;
+        for (sd_plan* q = p; q; q = q->macro) {
+            harvest(*q);
+            q->profiling = enable != 0;
+            for (int c = 0; c < 4; ++c) {
+                q->ms[c] = 0.0;
+                q->launches[c] = 0;
+                q->bytes[c] = 0.0;
+            }
         }
     });
 }
@@ -1512,11 +1574,18 @@ sd_status sd_plan_set_profiling(sd_plan* p, int enable) {
 sd_status sd_plan_kernel_times(sd_plan* p, double* ms, uint64_t* launches, double* bytes, int n_classes) {
     return guard([&] {
         require(p != nullptr, "null plan");
-        harvest(*p);
         for (int c = 0; c < n_classes && c < 4; ++c) {
-            if (ms) ms[c] = p->ms[c];
-            if (launches) launches[c] = p->launches[c];
-            if (bytes) bytes[c] = p->bytes[c];
+            if (ms) ms[c] = 0.0;
+            if (launches) launches[c] = 0;
+            if (bytes) bytes[c] = 0.0;
+        }
+        for (sd_plan* q = p; q; q = q->macro) {
+            harvest(*q);
+            for (int c = 0; c < n_classes && c < 4; ++c) {
+                if (ms) ms[c] += q->ms[c];
+                if (launches) launches[c] += q->launches[c];
+                if (bytes) bytes[c] += q->bytes[c];
+            }
         }
     });
 }

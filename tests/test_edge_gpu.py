@@ -3,8 +3,12 @@ its sources: the smallest registers (n = 1..4, tile wider than the state),
 identity and constant terms, single-term and diagonal-only groups, terms on
 the top qubit, duplicate terms merged by from_terms, an empty Hamiltonian,
 order-2 steps, and n_steps = 0."""
+import os
+
 import numpy as np
 import pytest
+
+from paper_2206_11664_b200 import models as M
 
 pytestmark = pytest.mark.gpu
 
@@ -146,3 +150,34 @@ def test_autotune_keeps_state_and_reports_both_schedules(sd, port):
     _, og = port.partition_and_diagonalize(text)
     want = port.evolve_grouped(a0, n, og, 0.01, 2, 1)
     assert np.max(np.abs(psi.amplitudes() - want)) < 1e-10
+
+
+@pytest.mark.parametrize("steps", [1, 4, 5])
+def test_macro_step_plan_matches_reference(steps, sd, ref, port, monkeypatch):
+    """Two Trotter steps planned as one macro step (order 1, group list
+    repeated; SDB_MACRO_FORCE keeps it regardless of the timing), whole macro
+    steps plus an odd remainder step through the base plan, against the
+    reference's evolve_grouped loop."""
+    if os.environ.get("SDB_AUTOTUNE") == "0":
+        pytest.skip("autotune disabled")
+    monkeypatch.setenv("SDB_MACRO_FORCE", "1")
+    n = 22
+    text = M.config_text(4, n)
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
+    a0 = port.random_state(n, 7)
+    psi = sd.StateVector(n)
+    psi.upload(a0)
+    plan = sd.TrotterPlan(psi, groups, order=1)
+    info = plan.info()
+    assert np.array_equal(psi.amplitudes(), a0)
+    if info["macro_steps"] == 0:
+        pytest.skip("macro plan needs no fewer passes per step at this size")
+    assert info["macro_steps"] == 2 and info["macro_passes"] < 2 * info["n_passes_per_step"]
+    dt = 0.05
+    plan.evolve(dt, steps)
+    h, _, _ = ref.partition_text(text)
+    want, _ = ref.evolve_grouped(h, a0, n, dt, steps, 1)
+    ref.free(h)
+    got = psi.amplitudes()
+    assert np.max(np.abs(got - want)) < 1e-10
+    assert abs(np.linalg.norm(got) - 1) < 1e-12

@@ -491,7 +491,9 @@ def run_ours(args, rank, world, local_rank):
                    "autotune_ms_per_step": ({"whole_group": info["tune_ms_whole"], "per_term": info["tune_ms_split"],
                                              "whole_group_ring": info["tune_ms_whole_ring"],
                                              "per_term_deep": info["tune_ms_split_deep"],
-                                             "macro_step": info["tune_ms_macro"]}
+                                             "per_term_nocap": info["tune_ms_split_nocap"],
+                                             "macro_step": info["tune_ms_macro"],
+                                             "macro_passes_per_2_steps": info["macro_passes"]}
                                             if info["tune_ms_whole"] > 0 else None)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": load_traffic(), "peak_source": peak_src,

@@ -289,8 +289,9 @@ typedef struct sd_plan_info {
     double tune_ms_split_deep;  /* ... per-term schedule with <= 3 Hadamard levels per pass */
     int max_hdepth;             /* Hadamard levels per pass of the kept plan (0: no cap, -1: default) */
     int macro_steps;            /* > 0: whole groups of this many Trotter steps run as one planned macro step */
-    int macro_passes;           /* passes per macro step (bytes_per_step then counts macro_passes / macro_steps) */
+    int macro_passes;           /* passes per macro step of the kept (or, macro_steps = 0, the tried) macro plan */
     double tune_ms_macro;       /* plan-time autotune: ms per Trotter step of the macro plan (0: not timed) */
+    double tune_ms_split_nocap; /* ... per-term schedule with no cap on Hadamard levels per pass */
 } sd_plan_info;
 
 sd_status sd_plan_get_info(const sd_plan* p, sd_plan_info* out);

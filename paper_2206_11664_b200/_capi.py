@@ -81,6 +81,7 @@ class PlanInfo(C.Structure):
         ("macro_steps", C.c_int),
         ("macro_passes", C.c_int),
         ("tune_ms_macro", dbl),
+        ("tune_ms_split_nocap", dbl),
     ]
 
 

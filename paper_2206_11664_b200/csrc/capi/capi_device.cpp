@@ -71,8 +71,8 @@ struct sd_plan {
     int split = -1;
     sdb::PlannerKnobs knobs;
     // measured ms/step: whole-group, per-term (<= 2 Hadamard levels per pass),
-    // whole-group ring, per-term with unlimited levels (0: not timed)
-    double tune_ms[4] = {0.0, 0.0, 0.0, 0.0};
+    // whole-group ring, per-term <= 3 levels, per-term with no cap (0: not timed)
+    double tune_ms[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     // Temporal blocking across Trotter steps (order 1): a plan of macro_reps
     // steps (the group list repeated) whose passes let the tail of one step
     // share passes with the head of the next; evolve() runs whole macro steps
@@ -80,6 +80,8 @@ struct sd_plan {
     // measures faster per Trotter step (sd_plan_create).
     sd_plan* macro = nullptr;
     int macro_reps = 0;
+    double tune_ms_macro = 0.0;  // measured ms per Trotter step of the macro candidate (0: not timed)
+    int macro_passes_tried = 0;  // passes per macro step of the candidate (0: none built)
 };
 
 namespace {
@@ -1339,25 +1341,38 @@ sd_status sd_plan_create(sd_state* h, const sd_group_desc* groups, size_t n_grou
             d->groups = p->groups;
             d->split = 1;
             d->knobs.max_hdepth = 3;
+            // candidate E: per-term diagonal ops, no cap on Hadamard levels (config 4:
+            // 4 heavy passes, 45.9 ms; their extra POINT stages cut into pattern
+            // points by the lowering), timed when it needs fewer passes than D
+            auto e = std::make_unique<sd_plan>();
+            e->state = h;
+            e->opts = p->opts;
+            e->groups = p->groups;
+            e->split = 1;
+            e->knobs.max_hdepth = 0;
             try {
                 plan_build(*q);
                 const bool fewer = q->first && p->first && q->first->ss.n_passes < p->first->ss.n_passes;
                 if (ensure_scratch(s)) {
-                    double t[4] = {time_steady_step(*p), 0.0, 0.0, 0.0};
+                    double t[5] = {time_steady_step(*p), 0.0, 0.0, 0.0, 0.0};
                     if (fewer) t[1] = time_steady_step(*q);
                     plan_build(*r);
                     t[2] = time_steady_step(*r);
                     if (fewer && deep_candidate_wanted()) {
                         plan_build(*d);
                         if (d->first && d->first->ss.n_passes <= q->first->ss.n_passes) t[3] = time_steady_step(*d);
+                        plan_build(*e);
+                        if (e->first && d->first && e->first->ss.n_passes < d->first->ss.n_passes) t[4] = time_steady_step(*e);
                     }
                     int best = 0;
-                    for (int c = 1; c < 4; ++c)
+                    for (int c = 1; c < 5; ++c)
                         if (t[c] > 0.0 && t[c] < t[best]) best = c;
-                    for (int c = 0; c < 4; ++c) p->tune_ms[c] = q->tune_ms[c] = r->tune_ms[c] = d->tune_ms[c] = t[c];
+                    for (int c = 0; c < 5; ++c)
+                        p->tune_ms[c] = q->tune_ms[c] = r->tune_ms[c] = d->tune_ms[c] = e->tune_ms[c] = t[c];
                     if (best == 1) std::swap(p, q);
                     if (best == 2) std::swap(p, r);
                     if (best == 3) std::swap(p, d);
+                    if (best == 4) std::swap(p, e);
                 }
             } catch (const sdb::OomError&) {
                 // no room for another candidate: keep the whole-group plan
@@ -1365,6 +1380,7 @@ sd_status sd_plan_create(sd_state* h, const sd_group_desc* groups, size_t n_grou
             sd_plan_destroy(q.release());
             sd_plan_destroy(r.release());
             sd_plan_destroy(d.release());
+            sd_plan_destroy(e.release());
             // Macro step (order 1 only: repeating an S2 group list is not two S2
             // steps): the kept schedule family planned over macro_reps steps at
             // once, kept when it needs fewer passes per Trotter step and times
@@ -1381,10 +1397,12 @@ sd_status sd_plan_create(sd_state* h, const sd_group_desc* groups, size_t n_grou
                 bool keep = false;
                 try {
                     plan_build(*m);
+                    if (m->first) p->macro_passes_tried = m->first->ss.n_passes;
                     if (m->first && m->first->ss.n_passes < reps * p->first->ss.n_passes && ensure_scratch(s)) {
                         const double tm = time_steady_step(*m) / reps;
                         const double tp = time_steady_step(*p);
                         m->tune_ms[0] = tm;
+                        p->tune_ms_macro = tm;
                         keep = (tm > 0.0 && tm < 0.98 * tp) || std::getenv("SDB_MACRO_FORCE");
                     }
                 } catch (const sdb::OomError&) {
@@ -1450,10 +1468,12 @@ sd_status sd_plan_get_info(const sd_plan* p, sd_plan_info* o) {
             o->tune_ms_split = p->tune_ms[1];
             o->tune_ms_whole_ring = p->tune_ms[2];
             o->tune_ms_split_deep = p->tune_ms[3];
+            o->tune_ms_split_nocap = p->tune_ms[4];
+            o->tune_ms_macro = p->tune_ms_macro;
+            o->macro_passes = p->macro_passes_tried;
             if (p->macro && p->macro->first) {
                 o->macro_steps = p->macro_reps;
                 o->macro_passes = p->macro->first->ss.n_passes;
-                o->tune_ms_macro = p->macro->tune_ms[0];
                 // steady state runs whole macro steps: bytes per Trotter step
                 o->bytes_per_step = 2.0 * 16.0 * double(s.amps_count()) * o->macro_passes / p->macro_reps;
             }

@@ -184,3 +184,49 @@ def test_jit_deep_per_term_matches_reference(cfg, n, split_points, sd, ref, port
     got = s.amplitudes()
     assert np.max(np.abs(got - want)) < 1e-10
     assert abs(np.linalg.norm(got) - 1) < 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,n,hdepth", [(4, 16, "3"), (4, 16, "0"), (3, 14, "2"), (5, 14, "2"), (5, 16, "0")])
+@pytest.mark.parametrize("fold", ["0", "1", "2"])
+def test_jit_cnot_maps_folded_into_the_stage(cfg, n, hdepth, fold, sd, ref, port, force_jit, monkeypatch):
+    """A CNOT-map transpose right behind the TMA LOAD is read off the staged
+    tile through the inverse map, one in front of a plain TMA STORE is written
+    into the stage through the map (jit.cpp load_fold / store_fold): off,
+    conflict-limited (default) and always, against the reference."""
+    monkeypatch.setenv("SDB_SPLIT_DIAG", "1")
+    monkeypatch.setenv("SDB_MAX_HDEPTH", hdepth)
+    monkeypatch.setenv("SDB_MAX_CTAS", "5")
+    monkeypatch.setenv("SDB_RING", "1")
+    monkeypatch.setenv("SDB_LOAD_FOLD", fold)
+    monkeypatch.setenv("SDB_STORE_FOLD", fold)
+    text = M.config_text(cfg, n=n)
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(text))
+    order, dt, steps = M.CONFIGS[cfg]["order"], M.CONFIGS[cfg]["dt"] * 5, 3
+    init = M.CONFIGS[cfg]["init"]
+    if init[0] == "random":
+        psi0 = port.random_state(n, init[1])
+    else:
+        psi0 = port.random_state(n, 7)  # a dense state: every slot of every tile is checked
+    s = sd.StateVector(n)
+    s.upload(psi0)
+    plan = sd.TrotterPlan(s, groups, order=order, tile_qubits=12)
+    plan.evolve(dt, steps)
+    got = s.amplitudes()
+    h, _, _ = ref.partition_text(text)
+    want, _ = ref.evolve_grouped(h, psi0, n, dt, steps, order)
+    ref.free(h)
+    assert np.max(np.abs(got - want)) < 1e-10
+    assert abs(np.linalg.norm(got) - 1) < 1e-12
+
+
+@pytest.mark.parametrize("cfg,n,hdepth", [(4, 30, "3"), (4, 30, "0"), (5, 16, "0")])
+def test_jit_folded_sources_compile(sd, monkeypatch, cfg, n, hdepth):
+    """Host-only: programs with the LOAD / STORE folds forced compile for sm_100a."""
+    monkeypatch.setenv("SDB_SPLIT_DIAG", "1")
+    monkeypatch.setenv("SDB_MAX_HDEPTH", hdepth)
+    monkeypatch.setenv("SDB_RING", "1")
+    monkeypatch.setenv("SDB_LOAD_FOLD", "2")
+    monkeypatch.setenv("SDB_STORE_FOLD", "2")
+    groups = sd.partition_and_diagonalize(sd.Hamiltonian.load(M.config_text(cfg, n=n)))
+    assert sd.simdiag.jit_compile_preview(n, groups, order=1) >= 1

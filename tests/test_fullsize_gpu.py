@@ -58,7 +58,13 @@ def _check_back_at_start(psi, cfg, n, a0):
     assert dev < TOL_ROUNDTRIP, dev
 
 
-@pytest.mark.parametrize("cfg,steps", [(4, 8), (3, 2)])
+@pytest.mark.parametrize("cfg,steps", [
+    (4, 8),
+    # config 3 builds and autotunes two ~215-pass plans (200-340 s, mostly NVRTC): opt-in; its
+    # full-size oracle parity case (test_fullsize_oracle_gpu.py, cfg3_n28) always runs
+    pytest.param(3, 2, marks=pytest.mark.skipif(os.environ.get("SDB_TEST_SLOW") != "1",
+                                                reason="opt-in (SDB_TEST_SLOW=1)")),
+])
 def test_order1_time_reversal_full_size(cfg, steps, sd, port):
     n = M.CONFIGS[cfg]["n"]
     groups = _groups(sd, cfg)

@@ -506,6 +506,11 @@ def run_ours(args, rank, world, local_rank):
                      "reference_schedule_equivalent_gbs": (info["n_ref_sweeps_per_step"] * bytes_per_launch /
                                                            (ms_per_step / 1e3) / 1e9),
                      "share_of_step": tot_ms / max(1e-9, ms),
+                     "note": ("the plan-time autotuner keeps the candidate schedule with the most steps/s; a "
+                              "schedule of fewer, heavier passes (issue-bound on shared-memory transposes) moves "
+                              "fewer bytes per step, so its GB/s per launch is lower although the step is faster "
+                              "-- config.autotune_ms_per_step lists every candidate (per_term_deep: 7 passes/step "
+                              "on config 4, HBM-bound)"),
                      "timing": ("timed region replays CUDA graphs; kernel split from a separate profiled run"
                                 if graph_steps else "per-launch CUDA events inside the timed region")},
         "gpu_launches": int(launches),
